@@ -1,0 +1,182 @@
+/*
+ * moe_b200.h — C ABI of the B200-native MoE layer (libmoe_b200.so).
+ *
+ * Drop-in boundary for the reference's MoE-layer operator API
+ * (/root/reference/proj/core/include/moeforge/routing.hpp, parallel.hpp).
+ * The reference has no FFI of its own: its "operator API" is that C++ header,
+ * linked statically.  This ABI exposes the same operations with plain
+ * pointers and sizes (no C++ or torch types) so C++, Python (ctypes) or any
+ * other FFI can bind it; include/moe_b200.hpp layers the reference's C++
+ * names (RouterConfig, RoutingDecision, moe_layer_forward, ...) on top.
+ *
+ * Conventions
+ *  - Every tensor argument is a DEVICE pointer (caller-owned; the library
+ *    never frees caller memory) unless the name ends in _host.
+ *  - Row-major layouts identical to the reference:
+ *      x, y, residual, dy, dx      [T, d_model]
+ *      gate_w                      [d_model, E]            (routing.hpp:126)
+ *      w1 [E_local, d_model, d_ff], b1 [E_local, d_ff]      (model.cpp:77-83, ExpertFfn)
+ *      w2 [E_local, d_ff, d_model], b2 [E_local, d_model]
+ *      decisions: entry (t, k) at index t * top_k + k      (routing.hpp:36-37)
+ *  - dtype MOE_F32: activations and expert weights are float32 (parity path,
+ *    1e-5 relative).  MOE_BF16: activations, expert weights and their grads
+ *    are bfloat16 with fp32 accumulation (tcgen05 path).  gate_w, biases,
+ *    gate probabilities and their grads are always float32.
+ *  - Exceptions never cross the ABI: each call returns a moe_status that maps
+ *    1:1 to the reference exception types (common.hpp:10-35); the text is
+ *    available from moe_last_error().  Device-side conditions (non-finite
+ *    values, probability rows not summing to one) are latched in a device
+ *    flag word and reported by moe_check() (which synchronises the stream).
+ *  - One handle = one CUDA stream = one layer's saved context; a handle is
+ *    not re-entrant, distinct handles are thread-safe (SPEC threading model,
+ *    tensor.hpp:22-23).
+ */
+#ifndef MOE_B200_H
+#define MOE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MOE_B200_ABI_VERSION 1
+
+typedef enum {
+    MOE_OK = 0,
+    MOE_SHAPE = 1,         /* moeforge::ShapeError         common.hpp:10-13 */
+    MOE_CONFIG = 2,        /* moeforge::ConfigError        common.hpp:21-24 */
+    MOE_NONFINITE = 3,     /* moeforge::NonFiniteError     common.hpp:15-19, tensor.cpp:23-29 */
+    MOE_UNIFORM_SHAPE = 4, /* moeforge::UniformShapeError  common.hpp:31-35 */
+    MOE_INVALID_ARG = 5,   /* std::invalid_argument (balance_loss routing.cpp:360-361) */
+    MOE_CUDA = 6,          /* CUDA runtime/driver failure */
+    MOE_NCCL = 7,          /* NCCL failure on the expert-parallel path */
+    MOE_UNSUPPORTED = 8    /* valid for the reference, not implemented on this path */
+} moe_status;
+
+typedef enum { MOE_TRAIN = 0, MOE_EVAL = 1 } moe_phase;                       /* routing.hpp:13 */
+typedef enum { MOE_PLAIN = 0, MOE_GROUPED = 1, MOE_RTS = 2 } moe_assignment;  /* routing.hpp:15 */
+typedef enum { MOE_F32 = 0, MOE_BF16 = 1 } moe_dtype;
+
+#define MOE_KDROPPED (-1) /* routing.hpp:34 kDropped */
+
+/* RouterConfig, routing.hpp:17-32 (same fields, same defaults via
+ * moe_router_cfg_default). */
+typedef struct {
+    int num_experts;
+    double capacity_factor_train;
+    double capacity_factor_eval;
+    double jitter_eps;
+    double balance_coeff;
+    int assignment_mode; /* moe_assignment */
+    int group_count;     /* only used by MOE_GROUPED */
+    int top_k;           /* 1 or 2 */
+    uint64_t rng_seed;
+} moe_router_cfg;
+
+typedef struct {
+    int64_t max_tokens; /* per rank; sizes the handle's workspace */
+    int64_t d_model;
+    int64_t d_ff;
+    int dtype;          /* moe_dtype */
+    int ep_size;        /* expert-parallel ranks (1 = single GPU) */
+    int ep_rank;
+} moe_layer_dims;
+
+typedef struct moe_handle moe_handle;
+
+/* Device flag bits latched by kernels, read by moe_check(). */
+#define MOE_FLAG_NONFINITE 0x1u
+#define MOE_FLAG_PROB_ROWS 0x2u /* balance_loss: probs rows must sum to 1 */
+#define MOE_FLAG_CHOICE_RANGE 0x4u
+
+void moe_router_cfg_default(moe_router_cfg* cfg);                    /* routing.hpp:17-27 */
+moe_status moe_router_cfg_validate(const moe_router_cfg* cfg);       /* routing.cpp:13-23 */
+/* capacity(tokens, cfg, phase), routing.cpp:43-49 (host only) */
+moe_status moe_capacity(int64_t tokens, const moe_router_cfg* cfg, int phase, int* cap_out);
+int moe_abi_version(void);
+
+moe_status moe_create(const moe_router_cfg* cfg, const moe_layer_dims* dims, moe_handle** out);
+moe_status moe_destroy(moe_handle* h);
+const char* moe_last_error(const moe_handle* h);
+moe_status moe_set_stream(moe_handle* h, void* cuda_stream);
+/* Synchronise the handle's stream; MOE_NONFINITE / MOE_INVALID_ARG if a
+ * kernel latched a flag since the last check (flags are then cleared). */
+moe_status moe_check(moe_handle* h, uint32_t* flags_out);
+
+/* ---- full layer: moe_layer_forward, routing.cpp:376-424 ---------------- */
+/* Forward.  T <= max_tokens rows of x.  residual == NULL means "x" (the
+ * reference default); pass a zero tensor for the contribution form
+ * (model.cpp:342).  aux: 1 float (device).  Decision outputs are optional
+ * (NULL to skip): expert_id, slot [T*top_k] int32 (slot = kDropped or the
+ * capacity slot, exactly as RoutingDecision), gate_prob [T*top_k] fp32.
+ * The forward context (decision, probabilities, hidden activations) is kept
+ * in the handle for moe_backward. */
+moe_status moe_forward(moe_handle* h, int64_t T, const void* x, const float* gate_w,
+                       const void* w1, const float* b1, const void* w2, const float* b2,
+                       int phase, uint64_t seed, const void* residual, void* y, float* aux,
+                       int32_t* expert_id, int32_t* slot, float* gate_prob);
+
+/* Backward of loss = <dy, y> + daux * aux for the last moe_forward on this
+ * handle (the closures the reference tape runs, tensor.cpp:156-187).
+ * Gradients are WRITTEN (not accumulated).  dgate_w is summed over ranks
+ * under expert parallelism.  dresidual is required iff a residual was passed
+ * to the forward (else ignored; its gradient then flows into dx). */
+moe_status moe_backward(moe_handle* h, const void* dy, float daux, void* dx, float* dgate_w,
+                        void* dw1, float* db1, void* dw2, float* db2, void* dresidual);
+
+/* Capacity and kept/dropped statistics of the last forward (host copy;
+ * synchronises).  kept_per_expert may be NULL, else [E] int64. */
+moe_status moe_last_decision_stats(moe_handle* h, int* capacity, int64_t* drop_count,
+                                   int64_t* kept_per_expert);
+
+/* ---- per-stage entry points (routing.hpp:60-118) ----------------------- */
+/* gate_forward (routing.cpp:51-101): probs [T,E] fp32, choice [T*k] int32,
+ * gate_prob [T*k] fp32.  x has the handle's dtype. */
+moe_status moe_gate(moe_handle* h, int64_t T, const void* x, const float* gate_w, int phase,
+                    uint64_t jitter_seed, float* probs, int32_t* choice, float* gate_prob);
+/* make_assignment (routing.cpp:189-206) over device choices; slot [T*k];
+ * *capacity_host receives RoutingDecision::capacity. */
+moe_status moe_assign(moe_handle* h, int64_t T, const int32_t* choice, int phase,
+                      uint64_t assign_seed, int32_t* slot, int* capacity_host);
+/* assign_plain / assign_grouped / assign_rts with an explicit capacity
+ * (routing.cpp:147-187). mode = moe_assignment. */
+moe_status moe_assign_mode(moe_handle* h, int64_t T, const int32_t* choice, int cap, int mode,
+                           int group_count, uint64_t rts_seed, int32_t* slot, int* capacity_host);
+/* dispatch (routing.cpp:208-243): buf [E*capacity, d] (unoccupied rows are
+ * exactly zero), occupancy [E*capacity] uint8 (may be NULL). */
+moe_status moe_dispatch(moe_handle* h, int64_t T, const void* x, const int32_t* expert_id,
+                        const int32_t* slot, int capacity, void* buf, uint8_t* occupancy);
+/* combine (routing.cpp:258-298): weights [top_k, T] fp32. */
+moe_status moe_combine(moe_handle* h, int64_t T, const void* expert_out, const int32_t* expert_id,
+                       const int32_t* slot, int capacity, const void* residual,
+                       const float* weights, void* y);
+/* balance_loss (routing.cpp:348-374): loss [1] fp32 (device). */
+moe_status moe_balance_loss(moe_handle* h, int64_t T, const float* probs,
+                            const int32_t* expert_id, double alpha, float* loss);
+
+/* ---- expert parallelism (parallel.hpp:100-111, made real) --------------- */
+/* Size of the NCCL unique id blob (ncclUniqueId). */
+size_t moe_ep_unique_id_size(void);
+/* Rank 0 creates the id; all ranks then call moe_ep_init with the same blob
+ * (distributed by the caller, e.g. torch.distributed broadcast). */
+moe_status moe_ep_get_unique_id(void* id_out);
+/* Binds the handle to an NCCL communicator of dims.ep_size ranks.  Rank r
+ * owns experts [r*E/ep, (r+1)*E/ep) (parallel.cpp:260-265); its w1/b1/w2/b2
+ * are those E/ep experts.  Each rank gates its own tokens; moe_forward's
+ * seed is the rank's seed (derive_seed(seed, r), parallel.cpp:272). */
+moe_status moe_ep_init(moe_handle* h, const void* unique_id);
+/* Fixed-shape A2A accounting of the last forward (A2ATrafficLog,
+ * parallel.hpp:83-91): bytes [ep, ep] in the reference's f64 units, and the
+ * bytes actually moved by this rank. */
+moe_status moe_ep_traffic(moe_handle* h, double* logical_bytes_host, double* actual_bytes_sent);
+
+/* ---- RNG streams (rng.cpp:15-102), host, bit-exact -------------------- */
+uint64_t moe_derive_seed_tag(uint64_t seed, const char* tag);
+uint64_t moe_derive_seed_u64(uint64_t seed, uint64_t salt);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOE_B200_H */

@@ -1,0 +1,96 @@
+"""ctypes binding of libmoe_b200.so (include/moe_b200.h).
+
+The library is built in-tree (``python -m paper_2109_10465_b200.build`` or
+``__graft_entry__.build()``).  There is no fallback: if the shared object is
+missing or fails to load, importing the operators raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmoe_b200.so")
+
+MOE_OK, MOE_SHAPE, MOE_CONFIG, MOE_NONFINITE, MOE_UNIFORM_SHAPE, MOE_INVALID_ARG = range(6)
+MOE_CUDA, MOE_NCCL, MOE_UNSUPPORTED = 6, 7, 8
+MOE_F32, MOE_BF16 = 0, 1
+
+
+class moe_router_cfg(C.Structure):
+    _fields_ = [
+        ("num_experts", C.c_int),
+        ("capacity_factor_train", C.c_double),
+        ("capacity_factor_eval", C.c_double),
+        ("jitter_eps", C.c_double),
+        ("balance_coeff", C.c_double),
+        ("assignment_mode", C.c_int),
+        ("group_count", C.c_int),
+        ("top_k", C.c_int),
+        ("rng_seed", C.c_uint64),
+    ]
+
+
+class moe_layer_dims(C.Structure):
+    _fields_ = [
+        ("max_tokens", C.c_int64),
+        ("d_model", C.c_int64),
+        ("d_ff", C.c_int64),
+        ("dtype", C.c_int),
+        ("ep_size", C.c_int),
+        ("ep_rank", C.c_int),
+    ]
+
+
+VP = C.c_void_p
+H = C.c_void_p  # moe_handle*
+
+# name: (restype, argtypes)
+_SIGS = {
+    "moe_abi_version": (C.c_int, []),
+    "moe_router_cfg_default": (None, [C.POINTER(moe_router_cfg)]),
+    "moe_router_cfg_validate": (C.c_int, [C.POINTER(moe_router_cfg)]),
+    "moe_capacity": (C.c_int, [C.c_int64, C.POINTER(moe_router_cfg), C.c_int, C.POINTER(C.c_int)]),
+    "moe_create": (C.c_int, [C.POINTER(moe_router_cfg), C.POINTER(moe_layer_dims), C.POINTER(H)]),
+    "moe_destroy": (C.c_int, [H]),
+    "moe_last_error": (C.c_char_p, [H]),
+    "moe_set_stream": (C.c_int, [H, VP]),
+    "moe_check": (C.c_int, [H, C.POINTER(C.c_uint32)]),
+    "moe_forward": (C.c_int, [H, C.c_int64, VP, VP, VP, VP, VP, VP, C.c_int, C.c_uint64, VP, VP, VP,
+                              VP, VP, VP]),
+    "moe_backward": (C.c_int, [H, VP, C.c_float, VP, VP, VP, VP, VP, VP, VP]),
+    "moe_last_decision_stats": (C.c_int, [H, C.POINTER(C.c_int), C.POINTER(C.c_int64), VP]),
+    "moe_gate": (C.c_int, [H, C.c_int64, VP, VP, C.c_int, C.c_uint64, VP, VP, VP]),
+    "moe_assign": (C.c_int, [H, C.c_int64, VP, C.c_int, C.c_uint64, VP, C.POINTER(C.c_int)]),
+    "moe_assign_mode": (C.c_int, [H, C.c_int64, VP, C.c_int, C.c_int, C.c_int, C.c_uint64, VP,
+                                  C.POINTER(C.c_int)]),
+    "moe_dispatch": (C.c_int, [H, C.c_int64, VP, VP, VP, C.c_int, VP, VP]),
+    "moe_combine": (C.c_int, [H, C.c_int64, VP, VP, VP, C.c_int, VP, VP, VP]),
+    "moe_balance_loss": (C.c_int, [H, C.c_int64, VP, VP, C.c_double, VP]),
+    "moe_ep_unique_id_size": (C.c_size_t, []),
+    "moe_ep_get_unique_id": (C.c_int, [VP]),
+    "moe_ep_init": (C.c_int, [H, VP]),
+    "moe_ep_traffic": (C.c_int, [H, VP, C.POINTER(C.c_double)]),
+    "moe_derive_seed_tag": (C.c_uint64, [C.c_uint64, C.c_char_p]),
+    "moe_derive_seed_u64": (C.c_uint64, [C.c_uint64, C.c_uint64]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load libmoe_b200.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with "
+                              "`python -m paper_2109_10465_b200.build` (no CPU fallback exists)")
+        lib = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib

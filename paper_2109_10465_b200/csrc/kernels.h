@@ -1,0 +1,150 @@
+// kernels.h — launch interfaces of the B200 MoE layer kernels (internal).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace moe {
+
+// device flag bits (mirror MOE_FLAG_* in include/moe_b200.h)
+constexpr uint32_t MOE_FLAG_NONFINITE_DEV = 0x1u;
+constexpr uint32_t MOE_FLAG_PROB_ROWS_DEV = 0x2u;
+constexpr uint32_t MOE_FLAG_CHOICE_RANGE_DEV = 0x4u;
+// fp32 probabilities: |sum_e P - 1| bound used in place of the reference's
+// f64 1e-9 (routing.cpp:360-361).
+constexpr float kProbRowTol = 1e-4f;
+
+// ---- router.cu ------------------------------------------------------------
+int softmax_parts(int64_t T);
+void launch_softmax_topk(const float* logits, int64_t T, int E, int K, float* probs,
+                         int32_t* choice, float* gate_prob, float* colsum_part,
+                         int32_t* count_part, uint32_t* flags, cudaStream_t st);
+void launch_balance_finalize(const float* colsum_part, const int32_t* count_part, int nparts,
+                             int64_t T, int E, double alpha, float* aux, float* fcoef,
+                             int32_t* counts, cudaStream_t st);
+
+struct AssignScratch {
+    int32_t* hist;   // [chunks][K][E]
+    int32_t* base;   // [chunks][K][E]
+    int32_t* gkept;  // [G][2][E]
+    int max_chunks;
+    int max_groups;
+};
+size_t assign_scratch_ints(int64_t T, int E, int K, int G);
+void launch_assign(int64_t T, int E, int K, int cap, int mode, int G, const int32_t* choice,
+                   const uint32_t* ord, int cap_pad, AssignScratch& s, int32_t* slot, int32_t* pos,
+                   int32_t* row_src, int32_t* kept, uint32_t* flags, cudaStream_t st);
+
+template <class TIO>
+void launch_router_bwd(int64_t T, int d, int E, int K, const TIO* dy, const TIO* O, int cap_pad,
+                       const int32_t* choice, const int32_t* pos, const float* gate_prob,
+                       const float* probs, const float* fcoef, float daux, float* dL,
+                       cudaStream_t st);
+
+// ---- rng.cu ---------------------------------------------------------------
+// Jitter noise n[i] = lo + (hi-lo) * ((mt() >> 11) * 2^-53) for i in [0, count)
+// of the mt19937_64 stream seeded with `seed` (routing.cpp:62-70), generated
+// on the device with jump-ahead (see rng.cu).
+struct MtJumpTable;
+void launch_jitter_noise(const MtJumpTable* tab, uint64_t seed, int64_t count, double eps,
+                         float* noise, cudaStream_t st);
+
+// ---- permute.cu -----------------------------------------------------------
+// Buffer geometry: nseg = ep * E_local segments; segment (r, le) holds rows
+// [(r*E_local + le) * cap_pad, ... + cap_pad) of the expert-input buffer,
+// the first counts[r*E_local+le] of which are occupied.
+template <class TIO>
+void launch_dispatch_gather(const TIO* x, int64_t d, int E, int K, int cap_pad,
+                            const int32_t* row_src, const int32_t* kept, TIO* buf,
+                            uint32_t* flags, cudaStream_t st);
+template <class TIO>
+void launch_combine(const TIO* O, int64_t T, int64_t d, int E, int K, int cap_pad,
+                    const int32_t* choice, const int32_t* pos, const float* w,
+                    const TIO* residual, TIO* y, uint32_t* flags, cudaStream_t st);
+template <class TIO>
+void launch_combine_bwd_gather(const TIO* dy, int64_t d, int E, int K, int cap_pad,
+                               const int32_t* row_src, const int32_t* kept, const float* w,
+                               TIO* dO, cudaStream_t st);
+// dx[t] = dxg[t] * noise[t] + sum_k dX[row_k] + (residual is x && none kept ? dy[t] : 0)
+// and dres[t] = none kept ? dy[t] : 0 when residual was explicit.
+template <class TIO>
+void launch_dx_assemble(int64_t T, int64_t d, int E, int K, int cap_pad, const float* dxg,
+                        const float* noise, const TIO* dX, const int32_t* choice,
+                        const int32_t* pos, const TIO* dy, bool residual_is_x, TIO* dx,
+                        TIO* dres, cudaStream_t st);
+void launch_combine_weights(int64_t T, int E, int K, const float* gate_prob, float* w,
+                            cudaStream_t st);
+// db[g][n] = sum over the group's occupied rows of src[row][n]
+template <class TIO>
+void launch_colsum_groups(const TIO* src, int64_t N, int ep, int El, int cap_pad,
+                          const int32_t* counts, float* db, cudaStream_t st);
+// reference-layout per-stage dispatch / combine (routing.cpp:208-298)
+template <class TIO>
+void launch_dispatch_ref(const TIO* x, int64_t T, int64_t d, int E, int K, int cap,
+                         const int32_t* expert_id, const int32_t* slot, TIO* buf, uint8_t* occ,
+                         cudaStream_t st);
+template <class TIO>
+void launch_combine_ref(const TIO* O, int64_t T, int64_t d, int E, int K, int cap,
+                        const int32_t* expert_id, const int32_t* slot, const float* w,
+                        const TIO* residual, TIO* y, cudaStream_t st);
+void launch_check_finite_f32(const float* p, int64_t n, uint32_t* flags, cudaStream_t st);
+
+// ---- gemm_simt.cu (fp32 SIMT; the parity path and the gate GEMMs) ----------
+// Dense C[M,N] = sum_k A(m,k) * B(k,n), A(m,k) = A[m*lda_m + k*lda_k] * (S ? S[same] : 1),
+// B(k,n) = B[k*ldb_k + n*ldb_n].  split_k > 1 writes partial sums to
+// C + s*M*N (caller reduces with launch_splitk_reduce).
+template <class TA>
+void launch_gemm_dense(const TA* A, int64_t lda_m, int64_t lda_k, const float* S,
+                       const float* B, int64_t ldb_k, int64_t ldb_n, float* C, int64_t M,
+                       int64_t N, int64_t K, int split_k, cudaStream_t st);
+void launch_splitk_reduce(const float* part, int split_k, int64_t MN, float* out,
+                          cudaStream_t st);
+
+enum EpiKind { EPI_BIAS_RELU = 0, EPI_BIAS = 1, EPI_RELU_MASK = 2, EPI_NONE = 3 };
+
+// Expert GEMM over buffer rows (fwd1, fwd2, dgrad2, dgrad1):
+//   C[row, n] = epi( sum_k A[row, k] * W_le(k, n) )
+// rows of segment (r, le) are [(r*El+le)*cap_pad, + counts[r*El+le]);
+// W_le(k,n) = W[le*K*N + k*N + n] if w_nmajor else W[le*N*K + n*K + k].
+// Rows in [count, roundup(count,128)) of each segment are written as zero.
+struct RowGemmArgs {
+    const void* A;
+    const void* W;
+    void* C;
+    const float* bias;   // [El][N] (EPI_BIAS*)
+    const void* mask;    // H buffer for EPI_RELU_MASK (same layout as C)
+    const int32_t* counts;
+    int64_t N, K;
+    int ep, El, cap_pad;
+    bool w_nmajor;
+    int epi;
+};
+template <class T>
+void launch_row_gemm_simt(const RowGemmArgs& a, cudaStream_t st);
+
+// Expert weight-gradient GEMM: Cg[m, n] = sum_{r, i < count(r,g)} A[row, m] * B[row, n]
+struct WgradGemmArgs {
+    const void* A;   // [rows][M]
+    const void* B;   // [rows][N]
+    void* C;         // [El][M][N]
+    const int32_t* counts;
+    int64_t M, N;
+    int ep, El, cap_pad;
+};
+template <class T>
+void launch_wgrad_gemm_simt(const WgradGemmArgs& a, cudaStream_t st);
+
+}  // namespace moe
+
+namespace moe {
+// rng.cu: device mt19937_64 jitter stream; returns false if the device
+// generator cannot serve this request (caller then uploads the host stream).
+bool launch_jitter_noise_device(uint64_t seed, int64_t count, double eps, float* noise,
+                                cudaStream_t st);
+// router.cu: balance_loss from explicit probabilities (per-stage API)
+void launch_balance_from_probs(const float* probs, int64_t T, int E, int K,
+                               const int32_t* expert_id, double alpha, float* loss,
+                               float* colsum_part, int32_t* count_part, uint32_t* flags,
+                               cudaStream_t st);
+}  // namespace moe

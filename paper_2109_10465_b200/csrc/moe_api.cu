@@ -1,0 +1,753 @@
+// moe_api.cu — host orchestration of the B200 MoE layer behind the C ABI in
+// include/moe_b200.h.  Implements moe_layer_forward (routing.cpp:376-424),
+// the explicit backward of the tape it builds, the per-stage operators
+// (routing.hpp:60-118) and real expert parallelism over NCCL
+// (simulate_expert_parallel_step, parallel.cpp:231-366, made physical).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/moe_b200.h"
+#include "common.cuh"
+#include "gemm_tc.h"
+#include "kernels.h"
+#include "rng_host.h"
+
+using namespace moe;
+
+namespace {
+
+#define NCCL_CHECK(expr)                                                                   \
+    do {                                                                                   \
+        ncclResult_t _r = (expr);                                                          \
+        if (_r != ncclSuccess)                                                             \
+            throw Status(MOE_NCCL, std::string(#expr) + ": " + ncclGetErrorString(_r));    \
+    } while (0)
+
+struct DevMem {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void alloc(size_t b) {
+        if (b == 0) b = 16;
+        MOE_CUDA_CHECK(cudaMalloc(&p, b));
+        bytes = b;
+    }
+    ~DevMem() {
+        if (p) cudaFree(p);
+    }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+int validate_cfg(const moe_router_cfg* c, std::string& why) {
+    // routing.cpp:13-23
+    if (c->num_experts < 1) { why = "router: num_experts must be >= 1"; return MOE_CONFIG; }
+    if (c->capacity_factor_train <= 0.0 || c->capacity_factor_eval <= 0.0) {
+        why = "router: capacity factors must be positive"; return MOE_CONFIG;
+    }
+    if (c->balance_coeff < 0.0) { why = "router: balance_coeff must be >= 0"; return MOE_CONFIG; }
+    if (c->jitter_eps < 0.0) { why = "router: jitter_eps must be >= 0"; return MOE_CONFIG; }
+    if (c->group_count < 1) { why = "router: group_count must be >= 1"; return MOE_CONFIG; }
+    if (c->top_k != 1 && c->top_k != 2) { why = "router: top_k must be 1 or 2"; return MOE_CONFIG; }
+    if (c->top_k > c->num_experts) { why = "router: top_k exceeds num_experts"; return MOE_CONFIG; }
+    if (c->assignment_mode < 0 || c->assignment_mode > 2) { why = "make_assignment: unknown mode"; return MOE_CONFIG; }
+    return MOE_OK;
+}
+
+int capacity_of(int64_t tokens, const moe_router_cfg* c, int phase) {
+    // routing.cpp:43-49 — computed in double, independent of top_k
+    const double cf = phase == MOE_TRAIN ? c->capacity_factor_train : c->capacity_factor_eval;
+    const double v = cf * static_cast<double>(tokens) / static_cast<double>(c->num_experts);
+    return std::max<int>(1, static_cast<int>(std::ceil(v)));
+}
+
+}  // namespace
+
+struct moe_handle {
+    moe_router_cfg cfg{};
+    moe_layer_dims dims{};
+    cudaStream_t stream = nullptr;
+    std::string err;
+    int E = 0, K = 0, El = 0, ep = 1, rank = 0;
+    int64_t Tmax = 0, d = 0, f = 0;
+    int cap_pad_max = 0;
+    size_t esz = 4;  // activation element size
+    ncclComm_t comm = nullptr;
+
+    // workspace
+    DevMem logits, probs, choice, gate_prob, wts, slot, pos, row_src, kept, counts_r;
+    DevMem colsum_part, count_part, fcoef, fcount, aux_scratch, noise, ord, flags;
+    DevMem hist, base, gkept;
+    DevMem Xloc, Xr, H, Or, Oloc, dOloc, dOr, dH, dXr, dXloc;
+    DevMem dL, dxg, dwg_part;
+    AssignScratch as{};
+    std::vector<uint32_t> host_ord;
+    std::vector<float> host_noise;
+
+    // forward context
+    bool fwd_valid = false;
+    int64_t T = 0;
+    int cap = 0, dec_cap = 0, cap_pad = 0, phase = 0, mode = 0;
+    bool jitter_on = false, has_residual = false;
+    const void* x = nullptr;
+    const float* gate_w = nullptr;
+    const void* w1 = nullptr;
+    const void* w2 = nullptr;
+    double last_logical_traffic = 0.0, last_actual_sent = 0.0;
+
+    void* loc(DevMem& a, DevMem& b) { return ep == 1 ? a.p : b.p; }
+};
+
+namespace {
+
+template <class F>
+moe_status guarded(moe_handle* h, F&& fn) {
+    try {
+        fn();
+        if (h) h->err.clear();
+        return MOE_OK;
+    } catch (const Status& s) {
+        if (h) h->err = s.what();
+        return static_cast<moe_status>(s.code);
+    } catch (const std::exception& e) {
+        if (h) h->err = e.what();
+        return MOE_CUDA;
+    }
+}
+
+void require(bool ok, int code, const char* msg) {
+    if (!ok) throw Status(code, msg);
+}
+
+ncclDataType_t nccl_type(size_t esz) { return esz == 2 ? ncclBfloat16 : ncclFloat32; }
+
+// All-to-all of equal chunks: rank r sends chunk s of `send` to rank s and
+// receives rank s's chunk r into chunk s of `recv` (parallel.cpp:294-307,
+// fixed (sender, expert) order).
+void all_to_all(moe_handle* h, const void* send, void* recv, size_t chunk_elems,
+                ncclDataType_t ty, size_t esz) {
+    NCCL_CHECK(ncclGroupStart());
+    for (int s = 0; s < h->ep; ++s) {
+        NCCL_CHECK(ncclSend(static_cast<const char*>(send) + s * chunk_elems * esz, chunk_elems, ty,
+                            s, h->comm, h->stream));
+        NCCL_CHECK(ncclRecv(static_cast<char*>(recv) + s * chunk_elems * esz, chunk_elems, ty, s,
+                            h->comm, h->stream));
+    }
+    NCCL_CHECK(ncclGroupEnd());
+}
+
+template <class TIO>
+void row_gemm(moe_handle* h, const TIO* A, const TIO* W, TIO* C, const float* bias,
+              const TIO* mask, const int32_t* counts, int64_t N, int64_t K, bool w_nmajor,
+              int epi, int nseg_ep) {
+    RowGemmArgs a;
+    a.A = A;
+    a.W = W;
+    a.C = C;
+    a.bias = bias;
+    a.mask = mask;
+    a.counts = counts;
+    a.N = N;
+    a.K = K;
+    a.ep = nseg_ep;
+    a.El = h->El;
+    a.cap_pad = h->cap_pad;
+    a.w_nmajor = w_nmajor;
+    a.epi = epi;
+    if constexpr (std::is_same<TIO, __nv_bfloat16>::value) {
+        if (tc_row_gemm_supported(a)) {
+            launch_row_gemm_tc(a, h->stream);
+            return;
+        }
+    }
+    launch_row_gemm_simt<TIO>(a, h->stream);
+}
+
+template <class TIO>
+void wgrad_gemm(moe_handle* h, const TIO* A, const TIO* B, TIO* C, int64_t M, int64_t N,
+                const int32_t* counts, int nseg_ep) {
+    WgradGemmArgs a;
+    a.A = A;
+    a.B = B;
+    a.C = C;
+    a.counts = counts;
+    a.M = M;
+    a.N = N;
+    a.ep = nseg_ep;
+    a.El = h->El;
+    a.cap_pad = h->cap_pad;
+    if constexpr (std::is_same<TIO, __nv_bfloat16>::value) {
+        if (tc_wgrad_gemm_supported(a)) {
+            launch_wgrad_gemm_tc(a, h->stream);
+            return;
+        }
+    }
+    launch_wgrad_gemm_simt<TIO>(a, h->stream);
+}
+
+// ---------------------------------------------------------------------------
+// router: gate -> softmax/top-k -> balance loss -> assignment
+// ---------------------------------------------------------------------------
+template <class TIO>
+void route(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, int phase, uint64_t seed,
+           float* aux) {
+    const int E = h->E, K = h->K;
+    cudaStream_t st = h->stream;
+    const bool jitter = phase == MOE_TRAIN && h->cfg.jitter_eps > 0.0;
+    if (jitter) {
+        // routing.cpp:62-70: noise stream Rng(derive_seed(seed, "jitter")), row-major
+        const uint64_t js = derive_seed_tag(seed, "jitter");
+        const double eps = h->cfg.jitter_eps;
+        if (!launch_jitter_noise_device(js, T * h->d, eps, h->noise.as<float>(), st)) {
+            h->host_noise.resize(static_cast<size_t>(T * h->d));
+            uniform_f32(js, 1.0 - eps, 1.0 + eps, T * h->d, h->host_noise.data());
+            MOE_CUDA_CHECK(cudaMemcpyAsync(h->noise.p, h->host_noise.data(),
+                                           sizeof(float) * T * h->d, cudaMemcpyHostToDevice, st));
+        }
+    }
+    // logits = (x * noise) @ gate_w  (routing.cpp:71)
+    launch_gemm_dense<TIO>(x, h->d, 1, jitter ? h->noise.as<float>() : nullptr, gate_w, E, 1,
+                           h->logits.as<float>(), T, E, h->d, 1, st);
+    launch_softmax_topk(h->logits.as<float>(), T, E, K, h->probs.as<float>(),
+                        h->choice.as<int32_t>(), h->gate_prob.as<float>(),
+                        h->colsum_part.as<float>(), h->count_part.as<int32_t>(),
+                        h->flags.as<uint32_t>(), st);
+    launch_balance_finalize(h->colsum_part.as<float>(), h->count_part.as<int32_t>(),
+                            softmax_parts(T), T, E, h->cfg.balance_coeff,
+                            aux ? aux : h->aux_scratch.as<float>(), h->fcoef.as<float>(),
+                            h->fcount.as<int32_t>(), st);
+    h->jitter_on = jitter;
+}
+
+void assign(moe_handle* h, int64_t T, const int32_t* choice, int cap, int mode, uint64_t aseed,
+            int32_t* slot_out) {
+    const uint32_t* ord = nullptr;
+    if (mode == MOE_RTS) {
+        // routing.cpp:180-187: priority order = Rng(derive_seed(seed,"assign")).permutation(T)
+        h->host_ord.resize(static_cast<size_t>(T));
+        permutation(aseed, T, h->host_ord.data());
+        MOE_CUDA_CHECK(cudaMemcpyAsync(h->ord.p, h->host_ord.data(), sizeof(uint32_t) * T,
+                                       cudaMemcpyHostToDevice, h->stream));
+        ord = h->ord.as<uint32_t>();
+    }
+    if (mode == MOE_GROUPED && T % h->cfg.group_count != 0)
+        throw Status(MOE_CONFIG, "assign_grouped: group_count must divide the token count");
+    launch_assign(T, h->E, h->K, cap, mode, h->cfg.group_count, choice, ord, h->cap_pad, h->as,
+                  slot_out, h->pos.as<int32_t>(), h->row_src.as<int32_t>(),
+                  h->kept.as<int32_t>(), h->flags.as<uint32_t>(), h->stream);
+}
+
+void set_geometry(moe_handle* h, int64_t T, int phase, int& mode) {
+    h->cap = capacity_of(T, &h->cfg, phase);
+    mode = phase == MOE_EVAL ? MOE_PLAIN : h->cfg.assignment_mode;  // routing.cpp:194-196
+    const int G = h->cfg.group_count;
+    h->dec_cap = mode == MOE_GROUPED ? G * ((h->cap + G - 1) / G) : h->cap;
+    h->cap_pad = static_cast<int>(round_up(h->dec_cap, kRowAlign));
+    if (h->cap_pad > h->cap_pad_max) throw Status(MOE_SHAPE, "capacity exceeds workspace");
+}
+
+template <class TIO>
+void forward_impl(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, const TIO* w1,
+                  const float* b1, const TIO* w2, const float* b2, int phase, uint64_t seed,
+                  const TIO* residual, TIO* y, float* aux, int32_t* expert_id, int32_t* slot,
+                  float* gate_prob) {
+    require(T >= 1 && T <= h->Tmax, MOE_SHAPE, "moe_forward: token count outside [1, max_tokens]");
+    require(x && gate_w && w1 && b1 && w2 && b2 && y, MOE_SHAPE, "moe_forward: null tensor");
+    require(phase == MOE_TRAIN || phase == MOE_EVAL, MOE_CONFIG, "moe_forward: bad phase");
+    cudaStream_t st = h->stream;
+    const int E = h->E, K = h->K, El = h->El, ep = h->ep;
+    int mode;
+    set_geometry(h, T, phase, mode);
+    h->fwd_valid = false;
+    route<TIO>(h, T, x, gate_w, phase, seed, aux);
+    assign(h, T, h->choice.as<int32_t>(), h->cap, mode, derive_seed_tag(seed, "assign"),
+           h->slot.as<int32_t>());
+    launch_combine_weights(T, E, K, h->gate_prob.as<float>(), h->wts.as<float>(), st);
+    // dispatch (routing.cpp:396): un-jittered x into [E, cap_pad, d]
+    TIO* Xloc = static_cast<TIO*>(h->loc(h->Xr, h->Xloc));
+    launch_dispatch_gather<TIO>(x, h->d, E, K, h->cap_pad, h->row_src.as<int32_t>(),
+                                h->kept.as<int32_t>(), Xloc, h->flags.as<uint32_t>(), st);
+    const int32_t* counts = h->kept.as<int32_t>();
+    if (ep > 1) {
+        // forward all-to-all: counts then rows (fixed-shape [E_local, cap_pad, d] slices)
+        all_to_all(h, h->kept.p, h->counts_r.p, El, ncclInt32, 4);
+        all_to_all(h, Xloc, h->Xr.p, static_cast<size_t>(El) * h->cap_pad * h->d,
+                   nccl_type(h->esz), h->esz);
+        counts = h->counts_r.as<int32_t>();
+        const double slice = static_cast<double>(El) * h->cap * h->d;
+        h->last_logical_traffic = 2.0 * slice * 8.0 * (ep - 1);
+        h->last_actual_sent = 2.0 * static_cast<double>(El) * h->cap_pad * h->d * h->esz * (ep - 1);
+    }
+    // expert FFN on occupied rows only (routing.cpp:399-405)
+    row_gemm<TIO>(h, h->Xr.as<TIO>(), w1, h->H.as<TIO>(), b1, nullptr, counts, h->f, h->d, true,
+                  EPI_BIAS_RELU, ep);
+    row_gemm<TIO>(h, h->H.as<TIO>(), w2, h->Or.as<TIO>(), b2, nullptr, counts, h->d, h->f, true,
+                  EPI_BIAS, ep);
+    TIO* Oloc = h->Or.as<TIO>();
+    if (ep > 1) {
+        all_to_all(h, h->Or.p, h->Oloc.p, static_cast<size_t>(El) * h->cap_pad * h->d,
+                   nccl_type(h->esz), h->esz);
+        Oloc = h->Oloc.as<TIO>();
+    }
+    // combine (routing.cpp:421, 258-298)
+    launch_combine<TIO>(Oloc, T, h->d, E, K, h->cap_pad, h->choice.as<int32_t>(),
+                        h->pos.as<int32_t>(), h->wts.as<float>(), residual ? residual : x, y,
+                        h->flags.as<uint32_t>(), st);
+    const size_t nk = static_cast<size_t>(T * K);
+    if (expert_id)
+        MOE_CUDA_CHECK(cudaMemcpyAsync(expert_id, h->choice.p, 4 * nk, cudaMemcpyDeviceToDevice, st));
+    if (slot) MOE_CUDA_CHECK(cudaMemcpyAsync(slot, h->slot.p, 4 * nk, cudaMemcpyDeviceToDevice, st));
+    if (gate_prob)
+        MOE_CUDA_CHECK(cudaMemcpyAsync(gate_prob, h->gate_prob.p, 4 * nk, cudaMemcpyDeviceToDevice, st));
+    h->T = T;
+    h->phase = phase;
+    h->mode = mode;
+    h->has_residual = residual != nullptr;
+    h->x = x;
+    h->gate_w = gate_w;
+    h->w1 = w1;
+    h->w2 = w2;
+    h->fwd_valid = true;
+}
+
+template <class TIO>
+void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dgate_w, TIO* dw1,
+                   float* db1, TIO* dw2, float* db2, TIO* dres) {
+    require(h->fwd_valid, MOE_SHAPE, "moe_backward: no forward context on this handle");
+    require(dy && dx && dgate_w && dw1 && db1 && dw2 && db2, MOE_SHAPE, "moe_backward: null tensor");
+    require(!h->has_residual || dres, MOE_SHAPE, "moe_backward: dresidual required");
+    cudaStream_t st = h->stream;
+    const int64_t T = h->T, d = h->d, f = h->f;
+    const int E = h->E, K = h->K, El = h->El, ep = h->ep;
+    const TIO* x = static_cast<const TIO*>(h->x);
+    const TIO* w1 = static_cast<const TIO*>(h->w1);
+    const TIO* w2 = static_cast<const TIO*>(h->w2);
+    const TIO* Oloc = ep > 1 ? h->Oloc.as<TIO>() : h->Or.as<TIO>();
+    // routing weights / balance loss / softmax backward -> dL
+    launch_router_bwd<TIO>(T, static_cast<int>(d), E, K, dy, Oloc, h->cap_pad,
+                           h->choice.as<int32_t>(), h->pos.as<int32_t>(),
+                           h->gate_prob.as<float>(), h->probs.as<float>(), h->fcoef.as<float>(),
+                           daux, h->dL.as<float>(), st);
+    // combine backward: dO rows = w * dy[t]
+    TIO* dOloc = static_cast<TIO*>(h->loc(h->dOr, h->dOloc));
+    launch_combine_bwd_gather<TIO>(dy, d, E, K, h->cap_pad, h->row_src.as<int32_t>(),
+                                   h->kept.as<int32_t>(), h->wts.as<float>(), dOloc, st);
+    const int32_t* counts = h->kept.as<int32_t>();
+    if (ep > 1) {
+        all_to_all(h, dOloc, h->dOr.p, static_cast<size_t>(El) * h->cap_pad * d,
+                   nccl_type(h->esz), h->esz);
+        counts = h->counts_r.as<int32_t>();
+    }
+    // expert backward: dH = (dO W2^T) * [H > 0]; dW2 = H^T dO; dX = dH W1^T; dW1 = X^T dH
+    row_gemm<TIO>(h, h->dOr.as<TIO>(), w2, h->dH.as<TIO>(), nullptr, h->H.as<TIO>(), counts, f, d,
+                  false, EPI_RELU_MASK, ep);
+    wgrad_gemm<TIO>(h, h->H.as<TIO>(), h->dOr.as<TIO>(), dw2, f, d, counts, ep);
+    launch_colsum_groups<TIO>(h->dOr.as<TIO>(), d, ep, El, h->cap_pad, counts, db2, st);
+    row_gemm<TIO>(h, h->dH.as<TIO>(), w1, h->dXr.as<TIO>(), nullptr, nullptr, counts, d, f, false,
+                  EPI_NONE, ep);
+    wgrad_gemm<TIO>(h, h->Xr.as<TIO>(), h->dH.as<TIO>(), dw1, d, f, counts, ep);
+    launch_colsum_groups<TIO>(h->dH.as<TIO>(), f, ep, El, h->cap_pad, counts, db1, st);
+    TIO* dXloc = h->dXr.as<TIO>();
+    if (ep > 1) {
+        all_to_all(h, h->dXr.p, h->dXloc.p, static_cast<size_t>(El) * h->cap_pad * d,
+                   nccl_type(h->esz), h->esz);
+        dXloc = h->dXloc.as<TIO>();
+    }
+    // gate backward: dxg = dL Wg^T; dWg = (x*noise)^T dL (split-K, fixed order)
+    const float* noise = h->jitter_on ? h->noise.as<float>() : nullptr;
+    launch_gemm_dense<float>(h->dL.as<float>(), E, 1, nullptr, h->gate_w, 1, E,
+                             h->dxg.as<float>(), T, d, E, 1, st);
+    const int splits = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(1, T / 512)));
+    launch_gemm_dense<TIO>(x, 1, d, noise, h->dL.as<float>(), E, 1, h->dwg_part.as<float>(), d, E,
+                           T, splits, st);
+    launch_splitk_reduce(h->dwg_part.as<float>(), splits, d * E, dgate_w, st);
+    if (ep > 1)
+        NCCL_CHECK(ncclAllReduce(dgate_w, dgate_w, static_cast<size_t>(d * E), ncclFloat32, ncclSum,
+                                 h->comm, st));
+    launch_dx_assemble<TIO>(T, d, E, K, h->cap_pad, h->dxg.as<float>(), noise, dXloc,
+                            h->choice.as<int32_t>(), h->pos.as<int32_t>(), dy, !h->has_residual,
+                            dx, dres, st);
+}
+
+void alloc_workspace(moe_handle* h) {
+    const int E = h->E, K = h->K;
+    const int64_t T = h->Tmax, d = h->d, f = h->f;
+    // largest capacity over both phases, grouped rounding included
+    moe_router_cfg c = h->cfg;
+    int capmax = std::max(capacity_of(T, &c, MOE_TRAIN), capacity_of(T, &c, MOE_EVAL));
+    const int G = c.group_count;
+    capmax = std::max(capmax, G * ((capmax + G - 1) / G));
+    h->cap_pad_max = static_cast<int>(round_up(capmax, kRowAlign));
+    const int64_t R = static_cast<int64_t>(E) * h->cap_pad_max;
+    const size_t es = h->esz;
+    h->logits.alloc(4 * T * E);
+    h->probs.alloc(4 * T * E);
+    h->choice.alloc(4 * T * K);
+    h->gate_prob.alloc(4 * T * K);
+    h->wts.alloc(4 * T * K);
+    h->slot.alloc(4 * T * K);
+    h->pos.alloc(4 * T * K);
+    h->row_src.alloc(4 * R);
+    h->kept.alloc(4 * E);
+    h->counts_r.alloc(4 * E);
+    const int nparts = softmax_parts(T);
+    h->colsum_part.alloc(4 * static_cast<size_t>(nparts) * E);
+    h->count_part.alloc(4 * static_cast<size_t>(nparts) * E);
+    h->fcoef.alloc(4 * E);
+    h->fcount.alloc(4 * E);
+    h->aux_scratch.alloc(16);
+    h->noise.alloc(4 * T * d);
+    h->ord.alloc(4 * T);
+    h->flags.alloc(16);
+    MOE_CUDA_CHECK(cudaMemset(h->flags.p, 0, 16));
+    const size_t sints = assign_scratch_ints(T, E, K, G);
+    h->hist.alloc(4 * sints);
+    h->base.alloc(4 * sints);
+    h->gkept.alloc(4 * (2 * static_cast<size_t>(G) * E + 64));
+    h->as.hist = h->hist.as<int32_t>();
+    h->as.base = h->base.as<int32_t>();
+    h->as.gkept = h->gkept.as<int32_t>();
+    h->as.max_chunks = static_cast<int>(sints / (2 * static_cast<size_t>(K) * E));
+    h->as.max_groups = G;
+    h->Xr.alloc(es * R * d);
+    h->H.alloc(es * R * f);
+    h->Or.alloc(es * R * d);
+    h->dOr.alloc(es * R * d);
+    h->dH.alloc(es * R * f);
+    h->dXr.alloc(es * R * d);
+    if (h->ep > 1) {
+        h->Xloc.alloc(es * R * d);
+        h->Oloc.alloc(es * R * d);
+        h->dOloc.alloc(es * R * d);
+        h->dXloc.alloc(es * R * d);
+    }
+    // buffers start finite (zero) so padded tensor-core tiles never see NaN garbage
+    for (DevMem* m : {&h->Xr, &h->H, &h->Or, &h->dOr, &h->dH, &h->dXr})
+        MOE_CUDA_CHECK(cudaMemset(m->p, 0, m->bytes));
+    h->dL.alloc(4 * T * E);
+    h->dxg.alloc(4 * T * d);
+    h->dwg_part.alloc(4 * 16 * d * E);
+    MOE_CUDA_CHECK(cudaDeviceSynchronize());
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int moe_abi_version(void) { return MOE_B200_ABI_VERSION; }
+
+void moe_router_cfg_default(moe_router_cfg* c) {
+    c->num_experts = 8;
+    c->capacity_factor_train = 1.0;
+    c->capacity_factor_eval = 2.0;
+    c->jitter_eps = 0.01;
+    c->balance_coeff = 0.01;
+    c->assignment_mode = MOE_PLAIN;
+    c->group_count = 1;
+    c->top_k = 1;
+    c->rng_seed = 0;
+}
+
+moe_status moe_router_cfg_validate(const moe_router_cfg* cfg) {
+    std::string why;
+    return static_cast<moe_status>(validate_cfg(cfg, why));
+}
+
+moe_status moe_capacity(int64_t tokens, const moe_router_cfg* cfg, int phase, int* cap_out) {
+    if (tokens < 1) return MOE_CONFIG;  // routing.cpp:44
+    std::string why;
+    const int st = validate_cfg(cfg, why);
+    if (st) return static_cast<moe_status>(st);
+    *cap_out = capacity_of(tokens, cfg, phase);
+    return MOE_OK;
+}
+
+uint64_t moe_derive_seed_tag(uint64_t seed, const char* tag) { return derive_seed_tag(seed, tag); }
+uint64_t moe_derive_seed_u64(uint64_t seed, uint64_t salt) { return derive_seed_u64(seed, salt); }
+
+moe_status moe_create(const moe_router_cfg* cfg, const moe_layer_dims* dims, moe_handle** out) {
+    if (!cfg || !dims || !out) return MOE_SHAPE;
+    *out = nullptr;
+    std::unique_ptr<moe_handle> h(new moe_handle());
+    moe_status s = guarded(h.get(), [&] {
+        std::string why;
+        const int st = validate_cfg(cfg, why);
+        if (st) throw Status(st, why);
+        require(dims->max_tokens >= 1 && dims->d_model >= 1 && dims->d_ff >= 1, MOE_SHAPE,
+                "moe_create: dims must be positive");
+        require(dims->dtype == MOE_F32 || dims->dtype == MOE_BF16, MOE_CONFIG, "moe_create: dtype");
+        const int ep = std::max(1, dims->ep_size);
+        require(cfg->num_experts % ep == 0, MOE_CONFIG,
+                "simulate: expert_parallel must divide num_experts");
+        require(ep == 1 || cfg->top_k == 1, MOE_CONFIG, "simulate: only top-1 routing is simulated");
+        require(dims->ep_rank >= 0 && dims->ep_rank < ep, MOE_CONFIG, "moe_create: ep_rank");
+        h->cfg = *cfg;
+        h->dims = *dims;
+        h->E = cfg->num_experts;
+        h->K = cfg->top_k;
+        h->ep = ep;
+        h->rank = dims->ep_rank;
+        h->El = h->E / ep;
+        h->Tmax = dims->max_tokens;
+        h->d = dims->d_model;
+        h->f = dims->d_ff;
+        h->esz = dims->dtype == MOE_BF16 ? 2 : 4;
+        alloc_workspace(h.get());
+    });
+    if (s == MOE_OK) *out = h.release();
+    return s;
+}
+
+moe_status moe_destroy(moe_handle* h) {
+    if (!h) return MOE_OK;
+    if (h->comm) ncclCommDestroy(h->comm);
+    delete h;
+    return MOE_OK;
+}
+
+const char* moe_last_error(const moe_handle* h) { return h ? h->err.c_str() : ""; }
+
+moe_status moe_set_stream(moe_handle* h, void* s) {
+    if (!h) return MOE_SHAPE;
+    h->stream = static_cast<cudaStream_t>(s);
+    return MOE_OK;
+}
+
+moe_status moe_check(moe_handle* h, uint32_t* flags_out) {
+    if (!h) return MOE_SHAPE;
+    uint32_t fl = 0;
+    moe_status s = guarded(h, [&] {
+        MOE_CUDA_CHECK(cudaStreamSynchronize(h->stream));
+        MOE_CUDA_CHECK(cudaMemcpy(&fl, h->flags.p, 4, cudaMemcpyDeviceToHost));
+        MOE_CUDA_CHECK(cudaMemset(h->flags.p, 0, 4));
+    });
+    if (flags_out) *flags_out = fl;
+    if (s) return s;
+    if (fl & MOE_FLAG_NONFINITE) {
+        h->err = "non-finite value produced by the MoE layer";
+        return MOE_NONFINITE;
+    }
+    if (fl & MOE_FLAG_CHOICE_RANGE) {
+        h->err = "assignment: choice out of expert range";
+        return MOE_CONFIG;
+    }
+    if (fl & MOE_FLAG_PROB_ROWS) {
+        h->err = "balance_loss: probs rows must sum to 1";
+        return MOE_INVALID_ARG;
+    }
+    return MOE_OK;
+}
+
+moe_status moe_forward(moe_handle* h, int64_t T, const void* x, const float* gate_w,
+                       const void* w1, const float* b1, const void* w2, const float* b2,
+                       int phase, uint64_t seed, const void* residual, void* y, float* aux,
+                       int32_t* expert_id, int32_t* slot, float* gate_prob) {
+    if (!h) return MOE_SHAPE;
+    return guarded(h, [&] {
+        if (h->esz == 2) {
+            using B = __nv_bfloat16;
+            forward_impl<B>(h, T, static_cast<const B*>(x), gate_w, static_cast<const B*>(w1), b1,
+                            static_cast<const B*>(w2), b2, phase, seed,
+                            static_cast<const B*>(residual), static_cast<B*>(y), aux, expert_id,
+                            slot, gate_prob);
+        } else {
+            forward_impl<float>(h, T, static_cast<const float*>(x), gate_w,
+                                static_cast<const float*>(w1), b1, static_cast<const float*>(w2),
+                                b2, phase, seed, static_cast<const float*>(residual),
+                                static_cast<float*>(y), aux, expert_id, slot, gate_prob);
+        }
+    });
+}
+
+moe_status moe_backward(moe_handle* h, const void* dy, float daux, void* dx, float* dgate_w,
+                        void* dw1, float* db1, void* dw2, float* db2, void* dresidual) {
+    if (!h) return MOE_SHAPE;
+    return guarded(h, [&] {
+        if (h->esz == 2) {
+            using B = __nv_bfloat16;
+            backward_impl<B>(h, static_cast<const B*>(dy), daux, static_cast<B*>(dx), dgate_w,
+                             static_cast<B*>(dw1), db1, static_cast<B*>(dw2), db2,
+                             static_cast<B*>(dresidual));
+        } else {
+            backward_impl<float>(h, static_cast<const float*>(dy), daux, static_cast<float*>(dx),
+                                 dgate_w, static_cast<float*>(dw1), db1, static_cast<float*>(dw2),
+                                 db2, static_cast<float*>(dresidual));
+        }
+    });
+}
+
+moe_status moe_last_decision_stats(moe_handle* h, int* capacity, int64_t* drop_count,
+                                   int64_t* kept_per_expert) {
+    if (!h) return MOE_SHAPE;
+    return guarded(h, [&] {
+        require(h->fwd_valid, MOE_SHAPE, "no forward on this handle");
+        std::vector<int32_t> kept(static_cast<size_t>(h->E));
+        MOE_CUDA_CHECK(cudaStreamSynchronize(h->stream));
+        MOE_CUDA_CHECK(cudaMemcpy(kept.data(), h->kept.p, 4 * h->E, cudaMemcpyDeviceToHost));
+        int64_t total = 0;
+        for (int e = 0; e < h->E; ++e) {
+            total += kept[e];
+            if (kept_per_expert) kept_per_expert[e] = kept[e];
+        }
+        if (capacity) *capacity = h->dec_cap;
+        if (drop_count) *drop_count = h->T * h->K - total;
+    });
+}
+
+moe_status moe_gate(moe_handle* h, int64_t T, const void* x, const float* gate_w, int phase,
+                    uint64_t jitter_seed, float* probs, int32_t* choice, float* gate_prob) {
+    if (!h) return MOE_SHAPE;
+    return guarded(h, [&] {
+        require(T >= 1 && T <= h->Tmax, MOE_SHAPE, "gate_forward: x [T,d] and gate_w [d,E] required");
+        cudaStream_t st = h->stream;
+        const int E = h->E, K = h->K;
+        const bool jitter = phase == MOE_TRAIN && h->cfg.jitter_eps > 0.0;
+        if (jitter) {
+            const double eps = h->cfg.jitter_eps;
+            if (!launch_jitter_noise_device(jitter_seed, T * h->d, eps, h->noise.as<float>(), st)) {
+                h->host_noise.resize(static_cast<size_t>(T * h->d));
+                uniform_f32(jitter_seed, 1.0 - eps, 1.0 + eps, T * h->d, h->host_noise.data());
+                MOE_CUDA_CHECK(cudaMemcpyAsync(h->noise.p, h->host_noise.data(),
+                                               sizeof(float) * T * h->d, cudaMemcpyHostToDevice, st));
+            }
+        }
+        const float* nz = jitter ? h->noise.as<float>() : nullptr;
+        if (h->esz == 2)
+            launch_gemm_dense<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(x), h->d, 1, nz,
+                                             gate_w, E, 1, h->logits.as<float>(), T, E, h->d, 1, st);
+        else
+            launch_gemm_dense<float>(static_cast<const float*>(x), h->d, 1, nz, gate_w, E, 1,
+                                     h->logits.as<float>(), T, E, h->d, 1, st);
+        launch_softmax_topk(h->logits.as<float>(), T, E, K, probs, choice, gate_prob,
+                            h->colsum_part.as<float>(), h->count_part.as<int32_t>(),
+                            h->flags.as<uint32_t>(), st);
+    });
+}
+
+moe_status moe_assign_mode(moe_handle* h, int64_t T, const int32_t* choice, int cap, int mode,
+                           int group_count, uint64_t rts_seed, int32_t* slot, int* capacity_host) {
+    if (!h) return MOE_SHAPE;
+    moe_status s = guarded(h, [&] {
+        require(T >= 1 && T <= h->Tmax, MOE_SHAPE, "assign: token count");
+        require(mode >= 0 && mode <= 2, MOE_CONFIG, "make_assignment: unknown mode");
+        require(cap >= 1, MOE_CONFIG, "assign: capacity must be >= 1");
+        if (mode == MOE_GROUPED)
+            require(group_count >= 1 && T % group_count == 0, MOE_CONFIG,
+                    "assign_grouped: group_count must divide the token count");
+        const int G = mode == MOE_GROUPED ? group_count : 1;
+        require(G <= h->as.max_groups || G == 1, MOE_CONFIG, "assign: group_count exceeds handle");
+        const int dec_cap = mode == MOE_GROUPED ? G * ((cap + G - 1) / G) : cap;
+        require(round_up(dec_cap, kRowAlign) <= h->cap_pad_max, MOE_SHAPE, "assign: capacity exceeds workspace");
+        h->cap_pad = static_cast<int>(round_up(dec_cap, kRowAlign));
+        moe_router_cfg saved = h->cfg;
+        h->cfg.group_count = G;
+        MOE_CUDA_CHECK(cudaMemsetAsync(slot, 0xff, 4 * static_cast<size_t>(T * h->K), h->stream));
+        assign(h, T, choice, cap, mode, rts_seed, slot);
+        h->cfg = saved;
+        h->fwd_valid = false;
+        if (capacity_host) *capacity_host = dec_cap;
+    });
+    if (s) return s;
+    return moe_check(h, nullptr);
+}
+
+moe_status moe_assign(moe_handle* h, int64_t T, const int32_t* choice, int phase,
+                      uint64_t assign_seed, int32_t* slot, int* capacity_host) {
+    if (!h) return MOE_SHAPE;
+    const int cap = capacity_of(T, &h->cfg, phase);
+    const int mode = phase == MOE_EVAL ? MOE_PLAIN : h->cfg.assignment_mode;
+    return moe_assign_mode(h, T, choice, cap, mode, h->cfg.group_count, assign_seed, slot,
+                           capacity_host);
+}
+
+moe_status moe_dispatch(moe_handle* h, int64_t T, const void* x, const int32_t* expert_id,
+                        const int32_t* slot, int capacity, void* buf, uint8_t* occupancy) {
+    if (!h) return MOE_SHAPE;
+    return guarded(h, [&] {
+        if (h->esz == 2)
+            launch_dispatch_ref<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(x), T, h->d, h->E,
+                                               h->K, capacity, expert_id, slot,
+                                               static_cast<__nv_bfloat16*>(buf), occupancy, h->stream);
+        else
+            launch_dispatch_ref<float>(static_cast<const float*>(x), T, h->d, h->E, h->K, capacity,
+                                       expert_id, slot, static_cast<float*>(buf), occupancy,
+                                       h->stream);
+    });
+}
+
+moe_status moe_combine(moe_handle* h, int64_t T, const void* expert_out, const int32_t* expert_id,
+                       const int32_t* slot, int capacity, const void* residual,
+                       const float* weights, void* y) {
+    if (!h) return MOE_SHAPE;
+    return guarded(h, [&] {
+        if (h->esz == 2)
+            launch_combine_ref<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(expert_out), T, h->d,
+                                              h->E, h->K, capacity, expert_id, slot, weights,
+                                              static_cast<const __nv_bfloat16*>(residual),
+                                              static_cast<__nv_bfloat16*>(y), h->stream);
+        else
+            launch_combine_ref<float>(static_cast<const float*>(expert_out), T, h->d, h->E, h->K,
+                                      capacity, expert_id, slot, weights,
+                                      static_cast<const float*>(residual), static_cast<float*>(y),
+                                      h->stream);
+    });
+}
+
+moe_status moe_balance_loss(moe_handle* h, int64_t T, const float* probs,
+                            const int32_t* expert_id, double alpha, float* loss) {
+    if (!h) return MOE_SHAPE;
+    moe_status s = guarded(h, [&] {
+        require(T >= 1 && T <= h->Tmax, MOE_SHAPE, "balance_loss: probs must be [T, E]");
+        // reuse the softmax kernel's reductions: logits = log(probs) is not
+        // needed; compute partials directly from probs via a dedicated pass
+        launch_balance_from_probs(probs, T, h->E, h->K, expert_id, alpha, loss,
+                                  h->colsum_part.as<float>(), h->count_part.as<int32_t>(),
+                                  h->flags.as<uint32_t>(), h->stream);
+    });
+    if (s) return s;
+    return moe_check(h, nullptr);
+}
+
+size_t moe_ep_unique_id_size(void) { return sizeof(ncclUniqueId); }
+
+moe_status moe_ep_get_unique_id(void* id_out) {
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return MOE_NCCL;
+    std::memcpy(id_out, &id, sizeof(id));
+    return MOE_OK;
+}
+
+moe_status moe_ep_init(moe_handle* h, const void* unique_id) {
+    if (!h) return MOE_SHAPE;
+    return guarded(h, [&] {
+        require(h->ep > 1, MOE_CONFIG, "moe_ep_init: ep_size must be > 1");
+        ncclUniqueId id;
+        std::memcpy(&id, unique_id, sizeof(id));
+        NCCL_CHECK(ncclCommInitRank(&h->comm, h->ep, id, h->rank));
+    });
+}
+
+moe_status moe_ep_traffic(moe_handle* h, double* logical_bytes_host, double* actual_bytes_sent) {
+    if (!h) return MOE_SHAPE;
+    return guarded(h, [&] {
+        // A2ATrafficLog (parallel.hpp:83-91): fixed-shape f64 bytes per
+        // direction pair = forward slice + reverse slice of [E/ep, cap, d].
+        if (logical_bytes_host) {
+            const double pair = 2.0 * h->El * static_cast<double>(h->cap) * h->d * 8.0;
+            for (int i = 0; i < h->ep; ++i)
+                for (int j = 0; j < h->ep; ++j) logical_bytes_host[i * h->ep + j] = i == j ? 0.0 : pair;
+        }
+        if (actual_bytes_sent) *actual_bytes_sent = h->last_actual_sent;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,383 @@
+// permute.cu — dispatch / combine permutation kernels and their backwards.
+//
+// Reference semantics (relative to /root/reference/proj/core/src):
+//   dispatch  routing.cpp:208-256   buf[e*cap + slot] = x[t]; bwd dx[t] += dbuf[row]
+//   combine   routing.cpp:258-346   y[t] = sum_k w_k O[row_k] (or residual if none kept);
+//                                   bwd dO[row] += w dy[t]; dw = <dy, O[row]>
+//   weights   routing.cpp:408-417   top-1 w = E * p; top-2 w_k = p_k / (p_0 + p_1)
+//
+// Every kernel is a row gather with 16-byte vector loads/stores, one warp per
+// row, so each output row is written exactly once (no atomics, deterministic).
+// The fused layer uses a compact internal row index e*cap_pad + pos (pos ==
+// slot except in grouped mode) whose occupied rows are dense per expert.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace moe {
+
+constexpr int kRowWarps = 8;
+
+// buf row r of expert e: src = row_src[r] if pos < kept[e]; zero-filled for
+// pos in [kept[e], roundup(kept[e], 128)) so the tensor-core tiles never read
+// stale rows; rows beyond that are never read.
+template <class TIO, int V>
+__global__ void __launch_bounds__(kRowWarps * 32)
+dispatch_gather_kernel(const TIO* __restrict__ x, int64_t d, int E, int K, int cap_pad,
+                       const int32_t* __restrict__ row_src, const int32_t* __restrict__ kept,
+                       TIO* __restrict__ buf) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t r = (int64_t)blockIdx.x * kRowWarps + warp;
+    if (r >= (int64_t)E * cap_pad) return;
+    const int e = (int)(r / cap_pad);
+    const int p = (int)(r % cap_pad);
+    const int n = kept[e];
+    TIO* dst = buf + r * d;
+    if (p < n) {
+        const int64_t t = row_src[r] / K;
+        const TIO* src = x + t * d;
+        for (int64_t j = (int64_t)lane * V; j < d; j += 32 * V) copy_vec<TIO, V>(dst + j, src + j);
+    } else if (p < round_up_dev(n, kRowAlign)) {
+        for (int64_t j = (int64_t)lane * V; j < d; j += 32 * V) zero_vec<TIO, V>(dst + j);
+    }
+}
+
+template <class TIO>
+void launch_dispatch_gather(const TIO* x, int64_t d, int E, int K, int cap_pad,
+                            const int32_t* row_src, const int32_t* kept, TIO* buf,
+                            uint32_t* flags, cudaStream_t st) {
+    (void)flags;
+    const int64_t rows = (int64_t)E * cap_pad;
+    const unsigned grid = (unsigned)ceil_div(rows, kRowWarps);
+    if (vec_width<TIO>(d) > 1)
+        dispatch_gather_kernel<TIO, 16 / sizeof(TIO)><<<grid, kRowWarps * 32, 0, st>>>(
+            x, d, E, K, cap_pad, row_src, kept, buf);
+    else
+        dispatch_gather_kernel<TIO, 1><<<grid, kRowWarps * 32, 0, st>>>(x, d, E, K, cap_pad,
+                                                                         row_src, kept, buf);
+    MOE_LAUNCH_CHECK();
+}
+
+// y[t] = sum_{k kept} w[t*K+k] * O[row_k]  (accumulated from 0 in k order,
+// routing.cpp:279-292), else the residual row.
+template <class TIO, int V>
+__global__ void __launch_bounds__(kRowWarps * 32)
+combine_kernel(const TIO* __restrict__ O, int64_t T, int64_t d, int K, int cap_pad,
+               const int32_t* __restrict__ choice, const int32_t* __restrict__ pos,
+               const float* __restrict__ w, const TIO* __restrict__ residual, TIO* __restrict__ y,
+               uint32_t* __restrict__ flags) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t t = (int64_t)blockIdx.x * kRowWarps + warp;
+    if (t >= T) return;
+    int64_t rows[2] = {-1, -1};
+    float wk[2] = {0.f, 0.f};
+    bool any = false;
+    for (int k = 0; k < K; ++k) {
+        const int32_t p = pos[t * K + k];
+        if (p >= 0) {
+            rows[k] = (int64_t)choice[t * K + k] * cap_pad + p;
+            wk[k] = w[t * K + k];
+            any = true;
+        }
+    }
+    bool bad = false;
+    for (int64_t j = (int64_t)lane * V; j < d; j += 32 * V) {
+        float acc[V];
+        if (any) {
+#pragma unroll
+            for (int q = 0; q < V; ++q) acc[q] = 0.f;
+            for (int k = 0; k < K; ++k) {
+                if (rows[k] < 0) continue;
+                float o[V];
+                load_f<TIO, V>(O + rows[k] * d + j, o);
+#pragma unroll
+                for (int q = 0; q < V; ++q) acc[q] = fmaf(wk[k], o[q], acc[q]);
+            }
+        } else {
+            load_f<TIO, V>(residual + t * d + j, acc);
+        }
+#pragma unroll
+        for (int q = 0; q < V; ++q) bad |= !finite_f(acc[q]);
+        store_f<TIO, V>(y + t * d + j, acc);
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, MOE_FLAG_NONFINITE_DEV);
+}
+
+template <class TIO>
+void launch_combine(const TIO* O, int64_t T, int64_t d, int E, int K, int cap_pad,
+                    const int32_t* choice, const int32_t* pos, const float* w,
+                    const TIO* residual, TIO* y, uint32_t* flags, cudaStream_t st) {
+    (void)E;
+    const unsigned grid = (unsigned)ceil_div(T, kRowWarps);
+    if (vec_width<TIO>(d) > 1)
+        combine_kernel<TIO, 16 / sizeof(TIO)><<<grid, kRowWarps * 32, 0, st>>>(
+            O, T, d, K, cap_pad, choice, pos, w, residual, y, flags);
+    else
+        combine_kernel<TIO, 1><<<grid, kRowWarps * 32, 0, st>>>(O, T, d, K, cap_pad, choice, pos,
+                                                                w, residual, y, flags);
+    MOE_LAUNCH_CHECK();
+}
+
+// dO[r] = w[src] * dy[t(src)] for occupied rows; zero tail up to 128 rows.
+template <class TIO, int V>
+__global__ void __launch_bounds__(kRowWarps * 32)
+combine_bwd_gather_kernel(const TIO* __restrict__ dy, int64_t d, int K, int cap_pad,
+                          const int32_t* __restrict__ row_src, const int32_t* __restrict__ kept,
+                          const float* __restrict__ w, TIO* __restrict__ dO, int64_t rows) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t r = (int64_t)blockIdx.x * kRowWarps + warp;
+    if (r >= rows) return;
+    const int e = (int)(r / cap_pad);
+    const int p = (int)(r % cap_pad);
+    const int n = kept[e];
+    TIO* dst = dO + r * d;
+    if (p < n) {
+        const int32_t src = row_src[r];
+        const float wv = w[src];
+        const TIO* s = dy + (int64_t)(src / K) * d;
+        for (int64_t j = (int64_t)lane * V; j < d; j += 32 * V) {
+            float v[V];
+            load_f<TIO, V>(s + j, v);
+#pragma unroll
+            for (int q = 0; q < V; ++q) v[q] *= wv;
+            store_f<TIO, V>(dst + j, v);
+        }
+    } else if (p < round_up_dev(n, kRowAlign)) {
+        for (int64_t j = (int64_t)lane * V; j < d; j += 32 * V) zero_vec<TIO, V>(dst + j);
+    }
+}
+
+template <class TIO>
+void launch_combine_bwd_gather(const TIO* dy, int64_t d, int E, int K, int cap_pad,
+                               const int32_t* row_src, const int32_t* kept, const float* w,
+                               TIO* dO, cudaStream_t st) {
+    const int64_t rows = (int64_t)E * cap_pad;
+    const unsigned grid = (unsigned)ceil_div(rows, kRowWarps);
+    if (vec_width<TIO>(d) > 1)
+        combine_bwd_gather_kernel<TIO, 16 / sizeof(TIO)><<<grid, kRowWarps * 32, 0, st>>>(
+            dy, d, K, cap_pad, row_src, kept, w, dO, rows);
+    else
+        combine_bwd_gather_kernel<TIO, 1><<<grid, kRowWarps * 32, 0, st>>>(dy, d, K, cap_pad,
+                                                                           row_src, kept, w, dO, rows);
+    MOE_LAUNCH_CHECK();
+}
+
+// dx[t] = dxg[t] * noise[t] + sum_{k kept} dX[row_k] (+ dy[t] if no route kept
+// and the residual is x).  Mirrors the three tape contributions to dx:
+// jitter mul bwd (ops.cpp:223-228), dispatch bwd (routing.cpp:245-253) and
+// the combine residual branch (routing.cpp:337-342).
+template <class TIO, int V>
+__global__ void __launch_bounds__(kRowWarps * 32)
+dx_assemble_kernel(int64_t T, int64_t d, int K, int cap_pad, const float* __restrict__ dxg,
+                   const float* __restrict__ noise, const TIO* __restrict__ dX,
+                   const int32_t* __restrict__ choice, const int32_t* __restrict__ pos,
+                   const TIO* __restrict__ dy, bool residual_is_x, TIO* __restrict__ dx,
+                   TIO* __restrict__ dres) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t t = (int64_t)blockIdx.x * kRowWarps + warp;
+    if (t >= T) return;
+    int64_t rows[2] = {-1, -1};
+    bool any = false;
+    for (int k = 0; k < K; ++k) {
+        const int32_t p = pos[t * K + k];
+        if (p >= 0) {
+            rows[k] = (int64_t)choice[t * K + k] * cap_pad + p;
+            any = true;
+        }
+    }
+    for (int64_t j = (int64_t)lane * V; j < d; j += 32 * V) {
+        float acc[V];
+#pragma unroll
+        for (int q = 0; q < V; ++q) acc[q] = 0.f;
+        for (int k = 0; k < K; ++k) {
+            if (rows[k] < 0) continue;
+            float v[V];
+            load_f<TIO, V>(dX + rows[k] * d + j, v);
+#pragma unroll
+            for (int q = 0; q < V; ++q) acc[q] += v[q];
+        }
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+            const float nz = noise ? noise[t * d + j + q] : 1.f;
+            acc[q] = fmaf(dxg[t * d + j + q], nz, acc[q]);
+        }
+        if (!any) {
+            float g[V];
+            load_f<TIO, V>(dy + t * d + j, g);
+            if (residual_is_x) {
+#pragma unroll
+                for (int q = 0; q < V; ++q) acc[q] += g[q];
+            } else if (dres) {
+                store_f<TIO, V>(dres + t * d + j, g);
+            }
+        } else if (!residual_is_x && dres) {
+            zero_vec<TIO, V>(dres + t * d + j);
+        }
+        store_f<TIO, V>(dx + t * d + j, acc);
+    }
+}
+
+template <class TIO>
+void launch_dx_assemble(int64_t T, int64_t d, int E, int K, int cap_pad, const float* dxg,
+                        const float* noise, const TIO* dX, const int32_t* choice,
+                        const int32_t* pos, const TIO* dy, bool residual_is_x, TIO* dx,
+                        TIO* dres, cudaStream_t st) {
+    (void)E;
+    const unsigned grid = (unsigned)ceil_div(T, kRowWarps);
+    if (vec_width<TIO>(d) > 1)
+        dx_assemble_kernel<TIO, 16 / sizeof(TIO)><<<grid, kRowWarps * 32, 0, st>>>(
+            T, d, K, cap_pad, dxg, noise, dX, choice, pos, dy, residual_is_x, dx, dres);
+    else
+        dx_assemble_kernel<TIO, 1><<<grid, kRowWarps * 32, 0, st>>>(
+            T, d, K, cap_pad, dxg, noise, dX, choice, pos, dy, residual_is_x, dx, dres);
+    MOE_LAUNCH_CHECK();
+}
+
+__global__ void combine_weights_kernel(int64_t T, int E, int K, const float* __restrict__ gp,
+                                       float* __restrict__ w) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= T) return;
+    if (K == 1) {
+        w[t] = gp[t] * (float)E;  // scale(gate_prob, E), routing.cpp:408-411
+    } else {
+        const float p0 = gp[2 * t], p1 = gp[2 * t + 1];
+        const float s = p0 + p1;  // add + div_elem, routing.cpp:412-416
+        w[2 * t] = p0 / s;
+        w[2 * t + 1] = p1 / s;
+    }
+}
+
+void launch_combine_weights(int64_t T, int E, int K, const float* gate_prob, float* w,
+                            cudaStream_t st) {
+    combine_weights_kernel<<<(unsigned)ceil_div(T, 256), 256, 0, st>>>(T, E, K, gate_prob, w);
+    MOE_LAUNCH_CHECK();
+}
+
+// db[g][n] = sum_{r, i < count(r,g)} src[(r*El+g)*cap_pad + i][n], fixed order.
+template <class TIO>
+__global__ void colsum_groups_kernel(const TIO* __restrict__ src, int64_t N, int ep, int El,
+                                     int cap_pad, const int32_t* __restrict__ counts,
+                                     float* __restrict__ db) {
+    const int g = blockIdx.y;
+    const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    float acc = 0.f;
+    for (int r = 0; r < ep; ++r) {
+        const int seg = r * El + g;
+        const int cnt = counts[seg];
+        const TIO* base = src + (int64_t)seg * cap_pad * N + n;
+        for (int i = 0; i < cnt; ++i) acc += to_f(base[(int64_t)i * N]);
+    }
+    db[(int64_t)g * N + n] = acc;
+}
+
+template <class TIO>
+void launch_colsum_groups(const TIO* src, int64_t N, int ep, int El, int cap_pad,
+                          const int32_t* counts, float* db, cudaStream_t st) {
+    dim3 grid((unsigned)ceil_div(N, 128), El);
+    colsum_groups_kernel<TIO><<<grid, 128, 0, st>>>(src, N, ep, El, cap_pad, counts, db);
+    MOE_LAUNCH_CHECK();
+}
+
+// ---- reference-layout per-stage kernels ------------------------------------
+template <class TIO>
+__global__ void dispatch_ref_kernel(const TIO* __restrict__ x, int64_t T, int64_t d, int K,
+                                    int cap, const int32_t* __restrict__ eid,
+                                    const int32_t* __restrict__ slot, TIO* __restrict__ buf,
+                                    uint8_t* __restrict__ occ) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t i = (int64_t)blockIdx.x * kRowWarps + warp;  // route index
+    if (i >= T * K) return;
+    const int32_t s = slot[i];
+    if (s < 0) return;
+    const int64_t row = (int64_t)eid[i] * cap + s;
+    const int64_t t = i / K;
+    for (int64_t j = lane; j < d; j += 32) buf[row * d + j] = x[t * d + j];
+    if (lane == 0 && occ) occ[row] = 1;
+}
+
+template <class TIO>
+void launch_dispatch_ref(const TIO* x, int64_t T, int64_t d, int E, int K, int cap,
+                         const int32_t* expert_id, const int32_t* slot, TIO* buf, uint8_t* occ,
+                         cudaStream_t st) {
+    MOE_CUDA_CHECK(cudaMemsetAsync(buf, 0, sizeof(TIO) * (size_t)E * cap * d, st));
+    if (occ) MOE_CUDA_CHECK(cudaMemsetAsync(occ, 0, (size_t)E * cap, st));
+    if (T * K == 0) return;
+    dispatch_ref_kernel<TIO><<<(unsigned)ceil_div(T * K, kRowWarps), kRowWarps * 32, 0, st>>>(
+        x, T, d, K, cap, expert_id, slot, buf, occ);
+    MOE_LAUNCH_CHECK();
+}
+
+template <class TIO>
+__global__ void combine_ref_kernel(const TIO* __restrict__ O, int64_t T, int64_t d, int K,
+                                   int cap, const int32_t* __restrict__ eid,
+                                   const int32_t* __restrict__ slot, const float* __restrict__ w,
+                                   const TIO* __restrict__ residual, TIO* __restrict__ y) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t t = (int64_t)blockIdx.x * kRowWarps + warp;
+    if (t >= T) return;
+    bool any = false;
+    for (int k = 0; k < K; ++k) any |= slot[t * K + k] >= 0;
+    for (int64_t j = lane; j < d; j += 32) {
+        float acc = 0.f;
+        if (any) {
+            for (int k = 0; k < K; ++k) {
+                const int32_t s = slot[t * K + k];
+                if (s < 0) continue;
+                acc = fmaf(w[(int64_t)k * T + t], to_f(O[((int64_t)eid[t * K + k] * cap + s) * d + j]), acc);
+            }
+        } else {
+            acc = to_f(residual[t * d + j]);
+        }
+        y[t * d + j] = from_f<TIO>(acc);
+    }
+}
+
+template <class TIO>
+void launch_combine_ref(const TIO* O, int64_t T, int64_t d, int E, int K, int cap,
+                        const int32_t* expert_id, const int32_t* slot, const float* w,
+                        const TIO* residual, TIO* y, cudaStream_t st) {
+    (void)E;
+    combine_ref_kernel<TIO><<<(unsigned)ceil_div(T, kRowWarps), kRowWarps * 32, 0, st>>>(
+        O, T, d, K, cap, expert_id, slot, w, residual, y);
+    MOE_LAUNCH_CHECK();
+}
+
+__global__ void check_finite_kernel(const float* __restrict__ p, int64_t n, uint32_t* flags) {
+    bool bad = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        bad |= !finite_f(p[i]);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, MOE_FLAG_NONFINITE_DEV);
+}
+
+void launch_check_finite_f32(const float* p, int64_t n, uint32_t* flags, cudaStream_t st) {
+    if (n <= 0) return;
+    check_finite_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 4 * kNumSMs), 256, 0, st>>>(
+        p, n, flags);
+    MOE_LAUNCH_CHECK();
+}
+
+#define INST(T)                                                                                  \
+    template void launch_dispatch_gather<T>(const T*, int64_t, int, int, int, const int32_t*,   \
+                                            const int32_t*, T*, uint32_t*, cudaStream_t);       \
+    template void launch_combine<T>(const T*, int64_t, int64_t, int, int, int, const int32_t*,   \
+                                    const int32_t*, const float*, const T*, T*, uint32_t*,       \
+                                    cudaStream_t);                                               \
+    template void launch_combine_bwd_gather<T>(const T*, int64_t, int, int, int, const int32_t*, \
+                                               const int32_t*, const float*, T*, cudaStream_t);  \
+    template void launch_dx_assemble<T>(int64_t, int64_t, int, int, int, const float*,           \
+                                        const float*, const T*, const int32_t*, const int32_t*,  \
+                                        const T*, bool, T*, T*, cudaStream_t);                   \
+    template void launch_colsum_groups<T>(const T*, int64_t, int, int, int, const int32_t*,      \
+                                          float*, cudaStream_t);                                 \
+    template void launch_dispatch_ref<T>(const T*, int64_t, int64_t, int, int, int,              \
+                                         const int32_t*, const int32_t*, T*, uint8_t*,           \
+                                         cudaStream_t);                                          \
+    template void launch_combine_ref<T>(const T*, int64_t, int64_t, int, int, int,               \
+                                        const int32_t*, const int32_t*, const float*, const T*,  \
+                                        T*, cudaStream_t);
+INST(float)
+INST(__nv_bfloat16)
+#undef INST
+
+}  // namespace moe

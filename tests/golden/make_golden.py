@@ -75,7 +75,10 @@ def ep_case(ref, name, spec):
     ep, T, d, f, E, mode, phase, seed = spec
     cfg = O.make_cfg(num_experts=E, assignment_mode=mode)
     x, gw, w1, b1, w2, b2, _ = O.layer_inputs(T * ep, d, f, E, seed=seed)
-    xs = x.reshape(ep, T, d)
+    xs = x.reshape(ep, T, d).copy()
+    o = O.restatement()
+    for r in range(ep):  # per-rank layer seed derive_seed(seed, r), parallel.cpp:272
+        xs[r] = margin_guard(xs[r], gw, cfg, phase, o.derive_seed(seed, r))
     ys, eid, slot, gp, cap, traffic = ref.ep_forward(xs, gw, w1, b1, w2, b2, cfg, phase, seed)
     np.savez_compressed(os.path.join(HERE, f"ep_{name}.npz"), xs=xs, ys=ys, expert_id=eid, slot=slot, gate_prob=gp,
                         capacity=np.int64(cap), traffic=traffic,

@@ -1,0 +1,245 @@
+"""GPU parity: libmoe_b200.so (through its C ABI) vs the CPU oracle.
+
+Decisions (expert ids, capacity slots, drop masks, capacity) must be
+bit-exact.  fp32 path: every output and gradient within
+max|gpu - ref| / max(1, |ref|) <= 1e-5 (the normalisation of the reference's
+gradcheck.hpp:21-24).  bf16 path: see test_gpu_bf16.py.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from oracle.margin import margin_guard
+from tests.golden import load as G
+
+pytestmark = pytest.mark.gpu
+
+TOL_F32 = 1e-5
+
+
+def rel_err(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    if a.size == 0:
+        return 0.0
+    return float(np.max(np.abs(a - b) / np.maximum(1.0, np.abs(b))))
+
+
+def to_dev(a, dt=torch.float32):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dt)
+
+
+def cfg_of(c):
+    import paper_2109_10465_b200 as M
+    return M.RouterConfig(num_experts=c.num_experts, capacity_factor_train=c.capacity_factor_train,
+                          capacity_factor_eval=c.capacity_factor_eval, jitter_eps=c.jitter_eps,
+                          balance_coeff=c.balance_coeff,
+                          assignment_mode=M.AssignmentMode(c.assignment_mode),
+                          group_count=c.group_count, top_k=c.top_k)
+
+
+def run_gpu_layer(cfg, phase, seed, inp, daux, dtype=torch.float32):
+    import paper_2109_10465_b200 as M
+    x = to_dev(inp["x"], dtype)
+    T, d = x.shape
+    f = inp["w1"].shape[-1]
+    params = M.MoeLayerParams(to_dev(inp["gate_w"]), to_dev(inp["w1"], dtype), to_dev(inp["b1"]),
+                              to_dev(inp["w2"], dtype), to_dev(inp["b2"]))
+    layer = M.MoeLayer(cfg_of(cfg), T, d, f, dtype)
+    res = None if inp.get("residual") is None else to_dev(inp["residual"], dtype)
+    y, aux, dec = layer.forward(x, params, M.Phase(phase), seed, residual=res)
+    g = layer.backward(to_dev(inp["dy"], dtype), daux)
+    torch.cuda.synchronize()
+    out = dict(y=y, aux=aux[0], expert_id=dec.expert_id, slot=dec.slot, gate_prob=dec.gate_prob,
+               capacity=dec.capacity, **g)
+    cap, drops, kept = layer.handle.stats()
+    out["stats"] = (cap, drops, kept)
+    return {k: (v.float().cpu().numpy() if torch.is_tensor(v) else v) for k, v in out.items()}
+
+
+@pytest.mark.parametrize("name", G.layer_names())
+def test_layer_fp32_vs_reference_golden(name):
+    cfg, phase, seed, daux, inp, z = G.load_layer(name)
+    # the fp32 path sees fp32-rounded inputs; the golden was computed in f64
+    out = run_gpu_layer(cfg, phase, seed, inp, daux)
+    assert np.array_equal(out["expert_id"].astype(np.int32), z["expert_id"])
+    assert np.array_equal(out["slot"].astype(np.int32), z["slot"])
+    assert out["capacity"] == int(z["capacity"])
+    cap, drops, kept = out["stats"]
+    assert cap == int(z["capacity"]) and drops == int((z["slot"] < 0).sum())
+    assert rel_err(out["gate_prob"], z["gate_prob"]) <= TOL_F32
+    assert rel_err(out["y"], z["y"]) <= TOL_F32
+    assert rel_err(out["aux"], z["aux"]) <= TOL_F32
+    for k in ("dx", "dgate_w", "db1", "db2", "dw1", "dw2", "dresidual"):
+        if k in z:
+            assert rel_err(out[k], z[k]) <= TOL_F32, k
+    if "dw1_rowsum" in z:
+        assert rel_err(out["dw1"].sum(2), z["dw1_rowsum"]) <= 1e-4
+        assert rel_err(out["dw2"].sum(1), z["dw2_colsum"]) <= 1e-4
+
+
+def test_layer_fp32_c1_full_size():
+    """Config 1 at full size (T=4096, d=512, f=2048, E=8, top-1, C=1.0, plain,
+    train, jitter on) vs the reference's own output (tests/golden/c1_full.npz)."""
+    z = G.load_c1()
+    T, d, f, E = (int(v) for v in z["spec"][:4])
+    x, gw, w1, b1, w2, b2, dy = O.layer_inputs(T, d, f, E, seed=42)
+    cfg = O.make_cfg(num_experts=E)
+    x = margin_guard(x, gw, cfg, O.TRAIN, 42)
+    inp = dict(x=x, gate_w=gw, w1=w1, b1=b1, w2=w2, b2=b2, dy=dy)
+    out = run_gpu_layer(cfg, O.TRAIN, 42, inp, 1.0)
+    assert np.array_equal(out["expert_id"].astype(np.int8), z["expert_id"])
+    assert np.array_equal(out["slot"].astype(np.int16), z["slot"])
+    assert out["capacity"] == int(z["capacity"]) == 512
+    rows = z["sample_rows"]
+    assert rel_err(out["y"][rows], z["y_rows"]) <= TOL_F32
+    assert rel_err(out["dx"][rows], z["dx_rows"]) <= TOL_F32
+    assert rel_err(out["aux"], z["aux"]) <= TOL_F32
+    assert rel_err(out["dgate_w"], z["dgate_w"]) <= TOL_F32
+    assert rel_err(out["db1"], z["db1"]) <= TOL_F32 and rel_err(out["db2"], z["db2"]) <= TOL_F32
+    # size-independent checksums (row / column sums over d or f terms)
+    assert rel_err(out["y"].sum(1), z["y_rowsum"]) <= 1e-4
+    assert rel_err(out["dw1"].sum(1), z["dw1_colsum"]) <= 1e-4
+    assert rel_err(out["dw2"].sum(2), z["dw2_rowsum"]) <= 1e-4
+
+
+@pytest.mark.parametrize("name", G.ep_names())
+def test_ep_golden_single_gpu_composition(name):
+    """simulate_expert_parallel_step contract on one GPU: rank r's output equals
+    the single-rank layer on its tokens with seed derive_seed(seed, r)."""
+    cfg, phase, seed, inp, z = G.load_ep(name)
+    o = O.restatement()
+    for r in range(inp["xs"].shape[0]):
+        one = dict(x=inp["xs"][r], gate_w=inp["gate_w"], w1=inp["w1"], b1=inp["b1"],
+                   w2=inp["w2"], b2=inp["b2"], dy=np.zeros_like(inp["xs"][r]))
+        out = run_gpu_layer(cfg, phase, o.derive_seed(seed, r), one, 0.0)
+        assert np.array_equal(out["expert_id"].astype(np.int32), z["expert_id"][r])
+        assert np.array_equal(out["slot"].astype(np.int32), z["slot"][r])
+        assert rel_err(out["y"], z["ys"][r]) <= TOL_F32
+
+
+# --- per-stage operators -----------------------------------------------------
+def test_gate_forward_kats_gpu():
+    import paper_2109_10465_b200 as M
+    cfg = M.RouterConfig(num_experts=2)
+    g = M.gate_forward(torch.tensor([[0.3, -0.4]], device="cuda"), torch.zeros(2, 2, device="cuda"),
+                       cfg, M.Phase.EVAL, 0)
+    assert g.probs[0, 0].item() == 0.5 and int(g.choice[0]) == 0
+    x = torch.tensor([[-1.0 if t % 2 == 0 else 1.0] for t in range(9)], device="cuda")
+    g = M.gate_forward(x, torch.tensor([[1.0, -1.0]], device="cuda"), cfg, M.Phase.EVAL, 0)
+    assert g.choice.tolist() == [1 if t % 2 == 0 else 0 for t in range(9)]
+
+
+@pytest.mark.parametrize("top_k,mode", [(1, O.PLAIN), (2, O.PLAIN), (1, O.RTS), (2, O.RTS),
+                                        (1, O.GROUPED), (2, O.GROUPED)])
+def test_assign_matches_oracle_fuzz(top_k, mode):
+    import paper_2109_10465_b200 as M
+    o = O.restatement()
+    rng = np.random.default_rng(1000 + 10 * top_k + mode)
+    for trial in range(25):
+        E = int(rng.integers(max(2, top_k), 70))
+        G_ = int(rng.integers(1, 5)) if mode == O.GROUPED else 1
+        T = int(rng.integers(1, 3000)) // G_ * G_ + G_
+        cap = int(rng.integers(1, max(2, 3 * T // E)))
+        ch = rng.integers(0, E, size=(T, top_k)).astype(np.int32)
+        if top_k == 2:
+            ch[:, 1] = np.where(ch[:, 1] == ch[:, 0], (ch[:, 0] + 1) % E, ch[:, 1])
+        ch = ch.reshape(-1)
+        seed = int(rng.integers(1 << 62))
+        ref_slot, ref_cap = o.assign(ch, E, cap, top_k=top_k, mode=mode, group_count=G_,
+                                     rts_seed=seed)
+        dev = torch.from_numpy(ch).cuda()
+        if mode == O.PLAIN:
+            d = M.assign_plain(dev, E, cap, top_k)
+        elif mode == O.GROUPED:
+            d = M.assign_grouped(dev, E, cap, G_, top_k)
+        else:
+            d = M.assign_rts(dev, E, cap, seed, top_k)
+        assert d.capacity == ref_cap
+        assert np.array_equal(d.slot.cpu().numpy(), ref_slot), (trial, E, T, cap)
+
+
+def test_assign_kats_gpu():
+    import paper_2109_10465_b200 as M
+    c = lambda v: torch.tensor(v, dtype=torch.int32, device="cuda")  # noqa: E731
+    assert M.assign_plain(c([0, 0, 0, 0]), 1, 2).slot.tolist() == [0, 1, -1, -1]
+    assert M.assign_plain(c([0, 1, 0, 1, 0, 2]), 3, 2, 2).slot.tolist() == [0, 0, 1, 1, -1, 0]
+    d = M.assign_grouped(c([0] * 6), 1, 3, 2)
+    assert d.slot.tolist() == [0, 1, -1, 2, 3, -1] and d.capacity == 4
+    with pytest.raises(M.ConfigError):
+        M.assign_grouped(c([0, 0, 0]), 1, 2, 2)
+    with pytest.raises(M.ConfigError):
+        M.assign_plain(c([0, 3]), 2, 2)
+
+
+def test_dispatch_combine_roundtrip_gpu():
+    import paper_2109_10465_b200 as M
+    rng = np.random.default_rng(61)
+    for _ in range(30):
+        E, T, cap, d = (int(rng.integers(1, 6)), int(rng.integers(1, 25)), int(rng.integers(1, 5)),
+                        int(rng.integers(1, 9)))
+        x = torch.from_numpy(rng.uniform(-1, 1, (T, d)).astype(np.float32)).cuda()
+        ch = torch.from_numpy(rng.integers(0, E, T).astype(np.int32)).cuda()
+        dec = M.assign_rts(ch, E, cap, int(rng.integers(1 << 62)))
+        buf = M.dispatch(x, dec)
+        y = M.combine(buf.data, dec, x, [torch.ones(T, device="cuda")])
+        assert torch.equal(y, x)
+        assert bool((buf.data[buf.occupancy == 0] == 0).all())
+
+
+def test_combine_hand_built_gpu():
+    import paper_2109_10465_b200 as M
+    x = torch.tensor([[1.0, 2.0], [-1.0, 0.5], [3.0, 3.0]], device="cuda")
+    dec = M.assign_plain(torch.tensor([0, 1, 0], dtype=torch.int32, device="cuda"), 2, 1)
+    y = M.combine(torch.tensor([[2.0, 4.0], [1.0, -0.5]], device="cuda"), dec, x,
+                  [torch.tensor([0.5, 0.25, 0.9], device="cuda")])
+    assert y.flatten().tolist() == [1.0, 2.0, 0.25, -0.125, 3.0, 3.0]
+
+
+def test_balance_loss_gpu():
+    import paper_2109_10465_b200 as M
+    dec = M.RoutingDecision(4, 2, 1, torch.arange(8, dtype=torch.int32, device="cuda") % 4,
+                            torch.zeros(8, dtype=torch.int32, device="cuda"),
+                            torch.zeros(8, device="cuda"))
+    assert abs(M.balance_loss(torch.full((8, 4), 0.25, device="cuda"), dec, 0.01).item() - 0.01) < 1e-8
+    P = torch.zeros(6, 4, device="cuda")
+    P[:, 0] = 1
+    dec = M.RoutingDecision(4, 8, 1, torch.zeros(6, dtype=torch.int32, device="cuda"),
+                            torch.arange(6, dtype=torch.int32, device="cuda"), torch.ones(6, device="cuda"))
+    assert abs(M.balance_loss(P, dec, 0.01).item() - 0.04) < 1e-8
+    with pytest.raises(M.InvalidArgument):
+        M.balance_loss(torch.full((2, 2), 0.4, device="cuda"),
+                       M.RoutingDecision(2, 1, 1, torch.zeros(2, dtype=torch.int32, device="cuda"),
+                                         torch.zeros(2, dtype=torch.int32, device="cuda"),
+                                         torch.zeros(2, device="cuda")), 0.01)
+
+
+def test_nonfinite_raises():
+    import paper_2109_10465_b200 as M
+    T, d, f, E = 16, 8, 16, 4
+    x, gw, w1, b1, w2, b2, dy = O.layer_inputs(T, d, f, E, seed=3)
+    x[3, 2] = np.nan
+    layer = M.MoeLayer(M.RouterConfig(num_experts=E), T, d, f, torch.float32)
+    p = M.MoeLayerParams(to_dev(gw), to_dev(w1), to_dev(b1), to_dev(w2), to_dev(b2))
+    with pytest.raises(M.NonFiniteError):
+        layer.forward(to_dev(x), p, M.Phase.TRAIN, 1)
+
+
+def test_autograd_adapter_matches_explicit_backward():
+    import paper_2109_10465_b200 as M
+    cfg, phase, seed, daux, inp, z = G.load_layer("top2_rts_train")
+    dt = torch.float32
+    T, d = inp["x"].shape
+    f = inp["w1"].shape[-1]
+    x = to_dev(inp["x"]).requires_grad_()
+    leaves = [to_dev(inp[k]).requires_grad_() for k in ("gate_w", "w1", "b1", "w2", "b2")]
+    params = M.MoeLayerParams(*leaves)
+    res = M.moe_layer_forward(x, params, cfg_of(cfg), M.Phase(phase), seed)
+    loss = (res.y * to_dev(inp["dy"])).sum() + daux * res.aux_loss
+    loss.backward()
+    assert rel_err(x.grad.cpu().numpy(), z["dx"]) <= TOL_F32
+    assert rel_err(leaves[0].grad.cpu().numpy(), z["dgate_w"]) <= TOL_F32
+    assert rel_err(leaves[1].grad.cpu().numpy(), z["dw1"]) <= TOL_F32
+    assert res.decision.drop_count() == int((z["slot"] < 0).sum())
+    del dt, T, d, f
