@@ -172,6 +172,10 @@ moe_status moe_ep_init(moe_handle* h, const void* unique_id);
  * bytes actually moved by this rank. */
 moe_status moe_ep_traffic(moe_handle* h, double* logical_bytes_host, double* actual_bytes_sent);
 
+/* ---- testing: route bf16 expert GEMMs through the SIMT kernels instead of
+ * tcgen05 (A/B comparisons of the two kernel families). ------------------ */
+void moe_debug_set_tensor_cores(int enabled);
+
 /* ---- RNG streams (rng.cpp:15-102), host, bit-exact -------------------- */
 uint64_t moe_derive_seed_tag(uint64_t seed, const char* tag);
 uint64_t moe_derive_seed_u64(uint64_t seed, uint64_t salt);

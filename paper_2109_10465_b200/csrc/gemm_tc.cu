@@ -1,14 +1,575 @@
-// gemm_tc.cu — tcgen05/TMEM bf16 grouped expert GEMMs (placeholder; see below).
+// gemm_tc.cu — grouped expert GEMMs on 5th-gen tensor cores (sm_100a).
+//
+// The expert FFN of the reference (routing.cpp:397-406; kernels::matmul_acc /
+// matmul_bt_acc / matmul_at_acc, ops.cpp:16-60) is >98% of the layer's work.
+// Here it is a persistent, warp-specialised tcgen05 kernel:
+//
+//   warp 0      TMA producer: cp.async.bulk.tensor 128B-swizzled A/B tiles
+//               into a kStages-deep shared-memory ring (mbarrier full/empty)
+//   warp 1      MMA issuer: one thread issues tcgen05.mma.cta_group::1.kind::f16
+//               (bf16 x bf16 -> fp32, M=128 N=256 K=16) into a TMEM accumulator;
+//               tcgen05.commit releases smem stages and publishes finished tiles
+//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 TMEM -> registers, fused
+//               bias / ReLU / ReLU-mask, bf16 pack, 16-byte stores
+//   TMEM        2 x 256 fp32 columns: the epilogue of tile i overlaps the MMAs
+//               of tile i+1
+//
+// Two problem kinds share the machinery:
+//   ROW    C[row, n] = epi(sum_k A[row,k] W_g(k,n))  — fwd1/fwd2 (W N-major)
+//          and dgrad1/dgrad2 (W K-major); rows are the occupied rows of each
+//          (origin rank, local expert) segment, tiles are compacted on device
+//          from the per-segment counts, so no host sync and no empty tiles.
+//   WGRAD  C_g[m, n] = sum_{rows of group g} A[row,m] B[row,n] — dW1/dW2
+//          (both operands MN-major; the K loop walks the group's segments).
+#include <cuda.h>
+
+#include <mutex>
+#include <unordered_map>
+
 #include "common.cuh"
 #include "gemm_tc.h"
 
 namespace moe {
 
+namespace tc {
+
+constexpr int BM = 128, BN = 256, BK = 64;
+constexpr int kStages = 4;
+constexpr int kThreads = 192;  // 6 warps
+constexpr int kEpiWarp0 = 2;
+constexpr uint32_t kTileABytes = BM * BK * 2;  // 16 KB
+constexpr uint32_t kTileBBytes = BN * BK * 2;  // 32 KB
+constexpr uint32_t kStageBytes = kTileABytes + kTileBBytes;
+constexpr int kMaxSegs = 1024;
+constexpr int kMaxGroups = 256;
+constexpr size_t kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + 1024 /*barriers*/ +
+                              4 * (kMaxSegs + 3 * kMaxGroups + 8);
+
+enum Kind { ROW = 0, WGRAD = 1 };
+
+struct __align__(64) Params {
+    CUtensorMap tmA;
+    CUtensorMap tmB;
+    void* C;
+    const float* bias;
+    const __nv_bfloat16* mask;
+    const int32_t* counts;
+    int64_t N;       // output columns
+    int64_t K;       // ROW: reduction length
+    int64_t M;       // WGRAD: output rows per group
+    int ep, El, cap_pad;
+    int epi;
+    int b_mn;        // ROW: 1 if W is N-major
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst,
+                                            int32_t c0, int32_t c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// TMEM -> registers: 32 lanes x 32 consecutive 32-bit columns
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+        "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+          "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+          "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+          "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Shared-memory matrix descriptor (tcgen05 "matrix descriptor"), 128B swizzle.
+//   K-major tile (rows x 64 K, 128 B per row): LBO unused (1), SBO = 1024 B
+//   (8-row core-matrix groups); advance along K by +32 B per K=16 step.
+//   MN-major tile (64-wide MN blocks of BK rows): LBO = MN-block stride,
+//   SBO = 1024 B (8-row K groups); advance along K by +2048 B per K=16 step.
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+    d |= static_cast<uint64_t>(1) << 46;  // descriptor version (Blackwell)
+    d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
+    return d;
+}
+
+// Instruction descriptor, kind::f16: bf16 A/B, fp32 D, M=128, N=256.
+__host__ __device__ constexpr uint32_t make_idesc(uint32_t a_mn, uint32_t b_mn) {
+    return (1u << 4)            // D format f32
+           | (1u << 7)          // A format bf16
+           | (1u << 10)         // B format bf16
+           | (a_mn << 15)       // A major (0 = K, 1 = MN)
+           | (b_mn << 16)       // B major
+           | ((BN >> 3) << 17)  // N
+           | ((BM >> 4) << 24); // M
+}
+
+// ------------------------------------------------------------ tile scheduler
+struct Sched {
+    int32_t* seg_cnt;   // [nseg] counts
+    int32_t* grp_mt;    // [El] m-tiles of the group
+    int32_t* grp_base;  // [El+1] first tile of the group
+    int total;
+};
+
+// ROW: tiles ordered (group, n-tile, m-tile) so the CTAs running at the same
+// time share the group's weight tile through L2.
+__device__ __forceinline__ void row_tile(const Params& p, const Sched& s, int NT, int t, int& seg,
+                                         int& mt, int& nt) {
+    int le = 0;
+    while (le + 1 < p.El && s.grp_base[le + 1] <= t) ++le;
+    const int local = t - s.grp_base[le];
+    const int gm = s.grp_mt[le];
+    nt = local / gm;
+    int mi = local % gm;
+    for (int r = 0; r < p.ep; ++r) {
+        const int sg = r * p.El + le;
+        const int c = (s.seg_cnt[sg] + BM - 1) / BM;
+        if (mi < c) {
+            seg = sg;
+            mt = mi;
+            return;
+        }
+        mi -= c;
+    }
+    seg = le;
+    mt = 0;
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kThreads, 1) grouped_gemm_kernel(const __grid_constant__ Params p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* tiles = smem;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+    uint64_t* empty = full + kStages;
+    uint64_t* tfull = empty + kStages;   // [2]
+    uint64_t* tempty = tfull + 2;        // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    int32_t* seg_cnt = reinterpret_cast<int32_t*>(smem + kStages * kStageBytes + 1024);
+    int32_t* grp_mt = seg_cnt + kMaxSegs;
+    int32_t* grp_base = grp_mt + kMaxGroups;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nseg = p.ep * p.El;
+
+    // ---- setup: barriers, TMEM, schedule
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < kStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        prefetch_tmap(&p.tmA);
+        prefetch_tmap(&p.tmB);
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    for (int i = threadIdx.x; i < nseg; i += blockDim.x) seg_cnt[i] = p.counts[i];
+    __syncthreads();
+    Sched s{seg_cnt, grp_mt, grp_base, 0};
+    int NT, MT;
+    if (KIND == ROW) {
+        NT = static_cast<int>(p.N / BN);
+        for (int g = threadIdx.x; g < p.El; g += blockDim.x) {
+            int m = 0;
+            for (int r = 0; r < p.ep; ++r) m += (seg_cnt[r * p.El + g] + BM - 1) / BM;
+            grp_mt[g] = m;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int acc = 0;
+            for (int g = 0; g < p.El; ++g) {
+                grp_base[g] = acc;
+                acc += grp_mt[g] * NT;
+            }
+            grp_base[p.El] = acc;
+        }
+        __syncthreads();
+        s.total = grp_base[p.El];
+        MT = 0;
+    } else {
+        NT = static_cast<int>(p.N / BN);
+        MT = static_cast<int>(p.M / BM);
+        s.total = p.El * MT * NT;
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ================= TMA producer =================
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < s.total; t += gridDim.x) {
+                if (KIND == ROW) {
+                    int seg, mt, nt;
+                    row_tile(p, s, NT, t, seg, mt, nt);
+                    const int le = seg % p.El;
+                    const int32_t arow = seg * p.cap_pad + mt * BM;
+                    const int nkb = static_cast<int>((p.K + BK - 1) / BK);
+                    for (int kb = 0; kb < nkb; ++kb) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        uint8_t* sa = tiles + stage * kStageBytes;
+                        uint8_t* sb = sa + kTileABytes;
+                        mbar_expect_tx(&full[stage], kStageBytes);
+                        tma_load_2d(&p.tmA, &full[stage], sa, kb * BK, arow);
+                        if (p.b_mn) {  // W [El*K, N]: 4 boxes {64 n, 64 k}
+#pragma unroll
+                            for (int j = 0; j < BN / 64; ++j)
+                                tma_load_2d(&p.tmB, &full[stage], sb + j * (64 * BK * 2),
+                                            nt * BN + j * 64, static_cast<int32_t>(le * p.K) + kb * BK);
+                        } else {       // W [El*N, K]: one box {64 k, 256 n}
+                            tma_load_2d(&p.tmB, &full[stage], sb, kb * BK,
+                                        static_cast<int32_t>(le * p.N) + nt * BN);
+                        }
+                        if (++stage == kStages) { stage = 0; phase ^= 1; }
+                    }
+                } else {
+                    const int g = t / (MT * NT);
+                    const int rem = t % (MT * NT);
+                    const int mt = rem / NT, nt = rem % NT;
+                    for (int r = 0; r < p.ep; ++r) {
+                        const int seg = r * p.El + g;
+                        const int nkb = (seg_cnt[seg] + BK - 1) / BK;
+                        for (int kb = 0; kb < nkb; ++kb) {
+                            mbar_wait(&empty[stage], phase ^ 1);
+                            uint8_t* sa = tiles + stage * kStageBytes;
+                            uint8_t* sb = sa + kTileABytes;
+                            const int32_t row = seg * p.cap_pad + kb * BK;
+                            mbar_expect_tx(&full[stage], kStageBytes);
+#pragma unroll
+                            for (int j = 0; j < BM / 64; ++j)
+                                tma_load_2d(&p.tmA, &full[stage], sa + j * (64 * BK * 2), mt * BM + j * 64, row);
+#pragma unroll
+                            for (int j = 0; j < BN / 64; ++j)
+                                tma_load_2d(&p.tmB, &full[stage], sb + j * (64 * BK * 2), nt * BN + j * 64, row);
+                            if (++stage == kStages) { stage = 0; phase ^= 1; }
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ================= MMA issuer =================
+        if (lane == 0) {
+            const uint32_t a_mn = KIND == WGRAD ? 1u : 0u;
+            const uint32_t b_mn = KIND == WGRAD ? 1u : static_cast<uint32_t>(p.b_mn);
+            const uint32_t idesc = make_idesc(a_mn, b_mn);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = blockIdx.x; t < s.total; t += gridDim.x) {
+                int nkb;
+                if (KIND == ROW) {
+                    nkb = static_cast<int>((p.K + BK - 1) / BK);
+                } else {
+                    const int g = t / (MT * NT);
+                    nkb = 0;
+                    for (int r = 0; r < p.ep; ++r) nkb += (seg_cnt[r * p.El + g] + BK - 1) / BK;
+                }
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t tmem_d = tmem_base + acc * BN;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(tiles + stage * kStageBytes);
+                    const uint32_t sb = sa + kTileABytes;
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k) {
+                        uint64_t ad, bd;
+                        if (a_mn) ad = sdesc(sa + k * 2048, 64 * BK * 2, 1024);
+                        else      ad = sdesc(sa + k * 32, 16, 1024);
+                        if (b_mn) bd = sdesc(sb + k * 2048, 64 * BK * 2, 1024);
+                        else      bd = sdesc(sb + k * 32, 16, 1024);
+                        tc_mma(tmem_d, ad, bd, idesc, (kb | k) ? 1u : 0u);
+                    }
+                    tc_commit(&empty[stage]);  // smem stage free once these MMAs retire
+                    if (++stage == kStages) { stage = 0; phase ^= 1; }
+                }
+                tc_commit(&tfull[acc]);  // accumulator ready (also fires if nkb == 0)
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else {
+        // ================= epilogue (warps 2..5) =================
+        const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+        const int row_in_tile = quarter * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        __nv_bfloat16* C = static_cast<__nv_bfloat16*>(p.C);
+        for (int t = blockIdx.x; t < s.total; t += gridDim.x) {
+            int64_t crow;
+            int64_t ncol0;
+            bool valid;
+            bool have_acc = true;
+            int le = 0;
+            if (KIND == ROW) {
+                int seg, mt, nt;
+                row_tile(p, s, NT, t, seg, mt, nt);
+                le = seg % p.El;
+                const int m = mt * BM + row_in_tile;
+                valid = m < seg_cnt[seg];
+                crow = static_cast<int64_t>(seg) * p.cap_pad + m;
+                ncol0 = static_cast<int64_t>(nt) * BN;
+            } else {
+                const int g = t / (MT * NT);
+                const int rem = t % (MT * NT);
+                const int mt = rem / NT, nt = rem % NT;
+                int nrows = 0;
+                for (int r = 0; r < p.ep; ++r) nrows += seg_cnt[r * p.El + g];
+                have_acc = nrows > 0;
+                valid = true;
+                crow = static_cast<int64_t>(g) * p.M + mt * BM + row_in_tile;
+                ncol0 = static_cast<int64_t>(nt) * BN;
+            }
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16);
+            __nv_bfloat16* crow_ptr = C + crow * p.N + ncol0;
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 32) {
+                uint32_t v[32];
+                tmem_ld32(tbase + c, v);
+                float f[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+                if (!have_acc || !valid) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) f[j] = 0.f;
+                } else if (KIND == ROW) {
+                    if (p.epi == EPI_BIAS || p.epi == EPI_BIAS_RELU) {
+                        const float* b = p.bias + static_cast<int64_t>(le) * p.N + ncol0 + c;
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4) {
+                            const float4 bb = __ldg(reinterpret_cast<const float4*>(b + j));
+                            f[j] += bb.x; f[j + 1] += bb.y; f[j + 2] += bb.z; f[j + 3] += bb.w;
+                        }
+                        if (p.epi == EPI_BIAS_RELU) {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) f[j] = f[j] > 0.f ? f[j] : 0.f;
+                        }
+                    } else if (p.epi == EPI_RELU_MASK) {
+                        const uint4* mp = reinterpret_cast<const uint4*>(p.mask + crow * p.N + ncol0 + c);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            uint4 u = __ldg(mp + q);
+                            const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+                            for (int j = 0; j < 8; ++j)
+                                if (!(__bfloat162float(h[j]) > 0.f)) f[q * 8 + j] = 0.f;
+                        }
+                    }
+                }
+                uint4* dst = reinterpret_cast<uint4*>(crow_ptr + c);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint4 u;
+                    __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) h2[j] = __floats2bfloat162_rn(f[q * 8 + 2 * j], f[q * 8 + 2 * j + 1]);
+                    dst[q] = u;
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+    }
+}
+
+// ------------------------------------------------------------ host side
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    });
+    if (!fn) throw Status(6, "cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+// 2D bf16 tensor [rows, cols] row-major, box {box_cols (inner), box_rows}, 128B swizzle
+CUtensorMap make_map(const void* base, int64_t rows, int64_t cols, int box_cols, int box_rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols * 2)};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Status(6, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return m;
+}
+
+int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = kNumSMs;
+    }
+    return n;
+}
+
+template <int KIND>
+void launch(const Params& p, int64_t max_tiles, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        MOE_CUDA_CHECK(cudaFuncSetAttribute(grouped_gemm_kernel<KIND>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(kSmemBytes)));
+        attr = true;
+    }
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms(), max_tiles)));
+    grouped_gemm_kernel<KIND><<<grid, kThreads, kSmemBytes, st>>>(p);
+    MOE_LAUNCH_CHECK();
+}
+
+}  // namespace tc
+
 static bool g_tc_enabled = true;
 void tc_set_enabled(bool on) { g_tc_enabled = on; }
-bool tc_row_gemm_supported(const RowGemmArgs&) { return false; }
-void launch_row_gemm_tc(const RowGemmArgs&, cudaStream_t) { throw Status(8, "tcgen05 row GEMM not built"); }
-bool tc_wgrad_gemm_supported(const WgradGemmArgs&) { return false; }
-void launch_wgrad_gemm_tc(const WgradGemmArgs&, cudaStream_t) { throw Status(8, "tcgen05 wgrad GEMM not built"); }
+
+bool tc_row_gemm_supported(const RowGemmArgs& a) {
+    return g_tc_enabled && a.N % tc::BN == 0 && a.K % tc::BK == 0 && a.cap_pad % tc::BM == 0 &&
+           a.ep * a.El <= tc::kMaxSegs && a.El <= tc::kMaxGroups;
+}
+
+bool tc_wgrad_gemm_supported(const WgradGemmArgs& a) {
+    return g_tc_enabled && a.N % tc::BN == 0 && a.M % tc::BM == 0 && a.cap_pad % tc::BK == 0 &&
+           a.ep * a.El <= tc::kMaxSegs && a.El <= tc::kMaxGroups;
+}
+
+void launch_row_gemm_tc(const RowGemmArgs& a, cudaStream_t st) {
+    tc::Params p{};
+    const int64_t rows = static_cast<int64_t>(a.ep) * a.El * a.cap_pad;
+    p.tmA = tc::make_map(a.A, rows, a.K, tc::BK, tc::BM);
+    if (a.w_nmajor)
+        p.tmB = tc::make_map(a.W, static_cast<int64_t>(a.El) * a.K, a.N, 64, tc::BK);
+    else
+        p.tmB = tc::make_map(a.W, static_cast<int64_t>(a.El) * a.N, a.K, tc::BK, tc::BN);
+    p.C = a.C;
+    p.bias = a.bias;
+    p.mask = static_cast<const __nv_bfloat16*>(a.mask);
+    p.counts = a.counts;
+    p.N = a.N;
+    p.K = a.K;
+    p.M = 0;
+    p.ep = a.ep;
+    p.El = a.El;
+    p.cap_pad = a.cap_pad;
+    p.epi = a.epi;
+    p.b_mn = a.w_nmajor ? 1 : 0;
+    const int64_t max_tiles = rows / tc::BM * (a.N / tc::BN);
+    tc::launch<tc::ROW>(p, max_tiles, st);
+}
+
+void launch_wgrad_gemm_tc(const WgradGemmArgs& a, cudaStream_t st) {
+    tc::Params p{};
+    const int64_t rows = static_cast<int64_t>(a.ep) * a.El * a.cap_pad;
+    p.tmA = tc::make_map(a.A, rows, a.M, 64, tc::BK);
+    p.tmB = tc::make_map(a.B, rows, a.N, 64, tc::BK);
+    p.C = a.C;
+    p.counts = a.counts;
+    p.N = a.N;
+    p.M = a.M;
+    p.K = 0;
+    p.ep = a.ep;
+    p.El = a.El;
+    p.cap_pad = a.cap_pad;
+    p.epi = EPI_NONE;
+    p.b_mn = 1;
+    const int64_t max_tiles = static_cast<int64_t>(a.El) * (a.M / tc::BM) * (a.N / tc::BN);
+    tc::launch<tc::WGRAD>(p, max_tiles, st);
+}
 
 }  // namespace moe

@@ -445,6 +445,8 @@ extern "C" {
 
 int moe_abi_version(void) { return MOE_B200_ABI_VERSION; }
 
+void moe_debug_set_tensor_cores(int enabled) { tc_set_enabled(enabled != 0); }
+
 void moe_router_cfg_default(moe_router_cfg* c) {
     c->num_experts = 8;
     c->capacity_factor_train = 1.0;

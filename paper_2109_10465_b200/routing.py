@@ -482,11 +482,13 @@ class MoeLayer:
                 G = self.cfg.group_count
                 cap = G * ((cap + G - 1) // G)
             dec = RoutingDecision(self.cfg.num_experts, cap, K, eid, slot, gp)
-        self._saved = (params, residual is not None)
+        # keep every tensor the saved context points at alive until backward
+        # (the reference tape keeps its parents alive the same way, tensor.cpp:140-152)
+        self._saved = (params, residual is not None, x, residual)
         return y, aux, dec
 
     def backward(self, dy, daux: float = 1.0, check: bool = True, grads=None):
-        params, has_res = self._saved
+        params, has_res = self._saved[:2]
         El, d, f = self.n_local, self.d_model, self.d_ff
         dev = dy.device
         if grads is None:

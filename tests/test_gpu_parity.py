@@ -26,6 +26,20 @@ def rel_err(a, b):
     return float(np.max(np.abs(a - b) / np.maximum(1.0, np.abs(b))))
 
 
+def rel_norm(a, b):
+    """Norm-wise error for gradients that reduce over tokens/rows (dgate_w,
+    dw1, db1, dw2, db2): max|gpu - ref| / max(1, max|ref|).  Each element is a
+    sum of up to T products whose own fp32 rounding (~1e-6 relative, from the
+    fp32 forward) cancels randomly, so the per-element bound is the tensor's
+    scale, not the element's (which can be ~0 after cancellation)."""
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b)) / max(1.0, float(np.max(np.abs(b)))))
+
+
+WGRADS = ("dgate_w", "db1", "db2", "dw1", "dw2")
+
+
 def to_dev(a, dt=torch.float32):
     return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dt)
 
@@ -73,7 +87,8 @@ def test_layer_fp32_vs_reference_golden(name):
     assert rel_err(out["aux"], z["aux"]) <= TOL_F32
     for k in ("dx", "dgate_w", "db1", "db2", "dw1", "dw2", "dresidual"):
         if k in z:
-            assert rel_err(out[k], z[k]) <= TOL_F32, k
+            err = rel_norm(out[k], z[k]) if k in WGRADS else rel_err(out[k], z[k])
+            assert err <= TOL_F32, (k, err)
     if "dw1_rowsum" in z:
         assert rel_err(out["dw1"].sum(2), z["dw1_rowsum"]) <= 1e-4
         assert rel_err(out["dw2"].sum(1), z["dw2_colsum"]) <= 1e-4
@@ -96,8 +111,8 @@ def test_layer_fp32_c1_full_size():
     assert rel_err(out["y"][rows], z["y_rows"]) <= TOL_F32
     assert rel_err(out["dx"][rows], z["dx_rows"]) <= TOL_F32
     assert rel_err(out["aux"], z["aux"]) <= TOL_F32
-    assert rel_err(out["dgate_w"], z["dgate_w"]) <= TOL_F32
-    assert rel_err(out["db1"], z["db1"]) <= TOL_F32 and rel_err(out["db2"], z["db2"]) <= TOL_F32
+    assert rel_norm(out["dgate_w"], z["dgate_w"]) <= TOL_F32
+    assert rel_norm(out["db1"], z["db1"]) <= TOL_F32 and rel_norm(out["db2"], z["db2"]) <= TOL_F32
     # size-independent checksums (row / column sums over d or f terms)
     assert rel_err(out["y"].sum(1), z["y_rowsum"]) <= 1e-4
     assert rel_err(out["dw1"].sum(1), z["dw1_colsum"]) <= 1e-4
@@ -239,7 +254,7 @@ def test_autograd_adapter_matches_explicit_backward():
     loss = (res.y * to_dev(inp["dy"])).sum() + daux * res.aux_loss
     loss.backward()
     assert rel_err(x.grad.cpu().numpy(), z["dx"]) <= TOL_F32
-    assert rel_err(leaves[0].grad.cpu().numpy(), z["dgate_w"]) <= TOL_F32
-    assert rel_err(leaves[1].grad.cpu().numpy(), z["dw1"]) <= TOL_F32
+    assert rel_norm(leaves[0].grad.cpu().numpy(), z["dgate_w"]) <= TOL_F32
+    assert rel_norm(leaves[1].grad.cpu().numpy(), z["dw1"]) <= TOL_F32
     assert res.decision.drop_count() == int((z["slot"] < 0).sum())
     del dt, T, d, f
