@@ -1,0 +1,399 @@
+"""bench.py — MoE-layer fwd+bwd tokens/s on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[2], the 64-expert top-1 config the target is
+quoted on): E=64 experts sharded E/N per GPU, d_model=2048, d_ff=8192, top-1,
+capacity factor 1.0, plain assignment, train phase (jitter eps=0.01,
+balance alpha=0.01), bf16 activations/weights with fp32 accumulation,
+T=8192 tokens per GPU (64k global at N=8, weak scaling).
+
+One step = moe_forward + moe_backward of loss = <dy, y> + aux (all expert
+grads, gate grad, dx) through the C ABI.  `value` is device-timed with inputs
+resident in HBM; `e2e` times the same step through the public API with the
+step's inputs (x, dy) copied from pinned host memory and dx + aux read back.
+
+  python bench.py [--gpus N --steps K --warmup W]            # our kernels
+  python bench.py --impl reference [...]                      # reference CPU path
+Multi-GPU: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOAD = dict(name="c3_ep_64e_top1", experts=64, d_model=2048, d_ff=8192, top_k=1,
+                capacity_factor=1.0, tokens_per_gpu=8192, assignment="plain", jitter_eps=0.01,
+                balance_coeff=0.01)
+METRIC = "MoE layer fwd+bwd tokens/sec"
+UNIT = "tokens/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], p["bf16_tflops"], p.get("bf16_tflops_sustained", p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) < 9:
+                continue
+            for i, n in enumerate(names):
+                if r[5 + i].lower() == "active":
+                    reasons.add(n)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU reference
+def reference_sample_inputs(seed=42):
+    """Bounded sample of the workload for the reference CPU path: one expert's
+    worth of config 3 — d=2048, f=8192, capacity 128 (128 tokens, E'=1, C=1.0)
+    — i.e. the same per-token work (every capacity row of every expert,
+    routing.cpp:399-405) and the same tokens-per-expert as the full config, so
+    its tokens/s equals the full config's (the gate is <1.5% of time)."""
+    import oracle as O
+    T, d, f, E = 128, WORKLOAD["d_model"], WORKLOAD["d_ff"], 1
+    x, gw, w1, b1, w2, b2, dy = O.layer_inputs(T, d, f, E, seed=seed)
+    cfg = O.make_cfg(num_experts=E, jitter_eps=WORKLOAD["jitter_eps"],
+                     balance_coeff=WORKLOAD["balance_coeff"])
+    return (x, gw, w1, b1, w2, b2, dy), cfg, T
+
+
+def cpu_threads_for(bytes_per_replica: float, cap: int) -> int:
+    n = os.cpu_count() or 1
+    try:
+        avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+        n = min(n, max(1, int(avail * 0.5 // bytes_per_replica)))
+    except Exception:
+        pass
+    return max(1, min(n, cap))
+
+
+def time_reference(threads: int, warm: bool = False):
+    import oracle as O
+    arrs, cfg, T = reference_sample_inputs()
+    if O.have_reference():
+        kind = "reference"
+        secs = O.time_reference_layer(*arrs[:6], cfg, O.TRAIN, 42, arrs[6], threads)
+    else:  # the C restatement (port), one replica per thread
+        kind = "port"
+        from concurrent.futures import ThreadPoolExecutor
+        o = O.restatement()
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(lambda i: o.moe_layer(*arrs[:6], cfg, O.TRAIN, 42 + i, dy=arrs[6]), range(threads)))
+        secs = time.perf_counter() - t0
+    return kind, T * threads / secs, secs
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = cpu_threads_for(1.2e9, 256)
+    # warm-up: exercise the code paths (and page in the library) on a tiny sample
+    import oracle as O
+    arrs, cfg, _ = reference_sample_inputs()
+    backend = O.reference() if O.have_reference() else O.restatement()
+    for _ in range(args.warmup):
+        backend.moe_layer(arrs[0][:8], *arrs[1:6], cfg, O.TRAIN, 1, dy=arrs[6][:8])
+    times = []
+    kind = "reference"
+    for _ in range(args.steps):
+        kind, tps, secs = time_reference(threads)
+        times.append(secs)
+        log(f"reference step: {secs:.2f} s, {tps:.2f} tokens/s ({threads} threads)")
+    secs = sorted(times)[len(times) // 2]
+    T = 128
+    value = T * threads / secs
+    sample = (f"per step: {threads} concurrent replicas of one config-3 expert (d=2048, f=8192, "
+              f"cap=128, 128 tokens, train, jitter on) fwd+bwd; median of {args.steps} steps")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(args.gpus),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(n):
+    return {"workload": WORKLOAD["name"], "experts": WORKLOAD["experts"],
+            "experts_per_gpu": WORKLOAD["experts"] // max(n, 1), "d_model": WORKLOAD["d_model"],
+            "d_ff": WORKLOAD["d_ff"], "top_k": 1, "capacity_factor": 1.0,
+            "assignment": "plain", "phase": "train", "jitter_eps": WORKLOAD["jitter_eps"],
+            "balance_coeff": WORKLOAD["balance_coeff"], "tokens_per_gpu": WORKLOAD["tokens_per_gpu"],
+            "global_tokens": WORKLOAD["tokens_per_gpu"] * n, "parallelism": f"ep{n}",
+            "l2": "inputs larger than L2: expert weights %.2f GB/GPU stream from HBM every step"
+                  % (2 * WORKLOAD["experts"] // max(n, 1) * WORKLOAD["d_model"] * WORKLOAD["d_ff"] * 2 / 1e9)}
+
+
+# ---------------------------------------------------------------- our kernels
+STAGE_BYTES_FLOPS = None
+
+
+def stage_model(stage, T, d, f, El, n_rows, n_tok):
+    """Algorithmic bytes and FLOPs of one launch of a stage.
+    n_rows = occupied expert rows processed on this GPU, n_tok = tokens."""
+    b16 = 2
+    W = El * d * f * b16  # one expert weight matrix family
+    if stage == "ffn1_fwd":      # H = relu(X W1 + b1): read X rows, W1; write H rows
+        return W + n_rows * (d + f) * b16, 2.0 * n_rows * d * f
+    if stage == "ffn2_fwd":      # O = H W2 + b2
+        return W + n_rows * (f + d) * b16, 2.0 * n_rows * d * f
+    if stage == "ffn2_dgrad":    # dH = (dO W2^T) * [H>0]: read dO, W2, H; write dH
+        return W + n_rows * (d + 2 * f) * b16, 2.0 * n_rows * d * f
+    if stage == "ffn1_dgrad":    # dX = dH W1^T
+        return W + n_rows * (f + d) * b16, 2.0 * n_rows * d * f
+    if stage in ("ffn2_wgrad", "ffn1_wgrad"):  # dW = A^T B: read A, B rows; write dW
+        return W + n_rows * (d + f) * b16, 2.0 * n_rows * d * f
+    return None, None
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2109_10465_b200 as M
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        log(f"note: WORLD_SIZE={world} but --gpus {args.gpus}; using WORLD_SIZE")
+    N = world
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if N > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    E, d, f = WORKLOAD["experts"], WORKLOAD["d_model"], WORKLOAD["d_ff"]
+    T = args.tokens_per_gpu
+    El = E // N
+    cfg = M.RouterConfig(num_experts=E, capacity_factor_train=WORKLOAD["capacity_factor"],
+                         jitter_eps=WORKLOAD["jitter_eps"], balance_coeff=WORKLOAD["balance_coeff"])
+    layer = M.MoeLayer(cfg, T, d, f, torch.bfloat16, ep_size=N, ep_rank=rank)
+    if N > 1:
+        uid = [M.ep_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        layer.ep_init(uid[0])
+    # synthetic parameters (random init of this architecture) and inputs
+    g = torch.Generator(device=dev).manual_seed(1234)
+    gr = torch.Generator(device=dev).manual_seed(1000 + rank)
+    s_g = float(np.sqrt(6.0 / (d + E)))
+    s_w = float(np.sqrt(6.0 / (d + f)))
+    gate_w = (torch.rand(d, E, device=dev, generator=g) * 2 - 1) * s_g  # replicated
+    w1 = ((torch.rand(El, d, f, device=dev, generator=gr) * 2 - 1) * s_w).to(torch.bfloat16)
+    w2 = ((torch.rand(El, f, d, device=dev, generator=gr) * 2 - 1) * s_w).to(torch.bfloat16)
+    b1 = (torch.rand(El, f, device=dev, generator=gr) * 2 - 1) * 0.01
+    b2 = (torch.rand(El, d, device=dev, generator=gr) * 2 - 1) * 0.01
+    params = M.MoeLayerParams(gate_w, w1, b1, w2, b2)
+    x = ((torch.rand(T, d, device=dev, generator=gr) * 2 - 1)).to(torch.bfloat16)
+    dy = ((torch.rand(T, d, device=dev, generator=gr) * 2 - 1)).to(torch.bfloat16)
+    seed = M.derive_seed(42, rank)  # per-rank layer seed (parallel.cpp:272)
+    y = torch.empty_like(x)
+    aux = torch.empty(1, device=dev)
+    grads = dict(dx=torch.empty_like(x), dgate_w=torch.empty_like(gate_w), dw1=torch.empty_like(w1),
+                 db1=torch.empty_like(b1), dw2=torch.empty_like(w2), db2=torch.empty_like(b2),
+                 dresidual=None)
+
+    def step():
+        layer.forward(x, params, M.Phase.TRAIN, seed, y=y, aux=aux, decision=False, check=False)
+        layer.backward(dy, 1.0, check=False, grads=grads)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if N > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if N == 1:
+            return v
+        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    layer.handle.check()  # surfaces any latched non-finite / range flag from warm-up
+    barrier()
+    # ---- device-timed region (inputs resident in HBM)
+    clocks = ClockSampler()
+    if rank == 0:
+        clocks.start()
+    layer.handle.profile(True)
+    launches0 = M.routing.kernel_launch_count()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(st)
+    for _ in range(args.steps):
+        step()
+    e1.record(st)
+    barrier()
+    launches = M.routing.kernel_launch_count() - launches0
+    clk = clocks.stop() if rank == 0 else None
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    stages = layer.handle.profile_read()
+    layer.handle.profile(False)
+    cap, drops, kept = layer.handle.stats()
+    value = N * T / (ms / 1e3)
+
+    # ---- e2e through the public API with host buffers
+    x_h = x.cpu().pin_memory()
+    dy_h = dy.cpu().pin_memory()
+    dx_h = torch.empty_like(x_h).pin_memory()
+    aux_h = torch.empty(1).pin_memory()
+    x_d = torch.empty_like(x)
+    dy_d = torch.empty_like(dy)
+
+    def e2e_step():
+        x_d.copy_(x_h, non_blocking=True)
+        layer.forward(x_d, params, M.Phase.TRAIN, seed, y=y, aux=aux, decision=False, check=False)
+        dy_d.copy_(dy_h, non_blocking=True)
+        layer.backward(dy_d, 1.0, check=False, grads=grads)
+        dx_h.copy_(grads["dx"], non_blocking=True)
+        aux_h.copy_(aux, non_blocking=True)
+
+    for _ in range(3):
+        e2e_step()
+    barrier()
+    e0.record(st)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(st)
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    e2e_value = N * T / (e2e_ms / 1e3)
+    layer.handle.check()
+
+    if rank != 0:
+        if N > 1:
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel (largest stage time)
+    hbm, tf_burst, tf_sus, src = peaks()
+    per_stage = {k: {"ms": v[0] / max(v[1], 1), "calls": v[1]} for k, v in stages.items()}
+    n_rows = int(kept.sum().item()) if N == 1 else None
+    if n_rows is None:
+        n_rows = T  # EP: every GPU processes ~T kept rows per step (weak scaling)
+    top = max(per_stage, key=lambda k: per_stage[k]["ms"])
+    bytes_, flops = stage_model(top, T, d, f, El, n_rows, T)
+    dur = per_stage[top]["ms"] / 1e3
+    roof = None
+    if bytes_ is not None:
+        t_mem = bytes_ / (hbm * 1e9)
+        t_cmp = flops / (tf_sus * 1e12)
+        if t_mem >= t_cmp:
+            ach = bytes_ / dur / 1e9
+            roof = {"kernel": top, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                    "frac": ach / hbm, "peak_source": src, "algorithmic_bytes": bytes_,
+                    "flops": flops, "traffic": None}
+        else:
+            ach = flops / dur / 1e12
+            roof = {"kernel": top, "bound": "tensor", "achieved": ach, "peak": tf_sus,
+                    "unit": "TFLOP/s", "frac": ach / tf_sus, "peak_source": src + " (sustained)",
+                    "algorithmic_bytes": bytes_, "flops": flops, "traffic": None}
+        roof["launch_ms"] = per_stage[top]["ms"]
+    gemm_ms = sum(v["ms"] for k, v in per_stage.items() if k.startswith("ffn"))
+    gemm_flops = 12.0 * n_rows * d * f
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random-init weights of the config-3 architecture, U(-1,1) tokens)",
+            "config": workload_config(N), "roofline": roof,
+            "expert_gemms": {"ms_per_step": gemm_ms, "tflops": gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms else None,
+                             "frac_of_bf16_sustained": (gemm_flops / (gemm_ms / 1e3) / 1e12) / tf_sus if gemm_ms else None},
+            "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": 2 * T * d * 2, "d2h_bytes_per_step": T * d * 2 + 4},
+            "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
+            "clocks": clk, "stages_ms": {k: round(v["ms"], 4) for k, v in per_stage.items()},
+            "decision": {"capacity": cap, "dropped_tokens_rank0": drops}}
+    if N == 1 and not args.no_cpu_baseline:
+        try:
+            threads = cpu_threads_for(1.2e9, 16)
+            kind, tps, secs = time_reference(threads)
+            _, cfg_s, Ts = reference_sample_inputs()
+            line["cpu_baseline"] = {"value": tps, "unit": UNIT, "cores": threads, "kind": kind,
+                                    "sample": f"{threads} concurrent replicas of one config-3 expert "
+                                              f"(d=2048, f=8192, cap=128, {Ts} tokens) fwd+bwd, {secs:.1f} s"}
+        except Exception as ex:  # pragma: no cover
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable",
+                                    "sample": str(ex)}
+    print(json.dumps(line), flush=True)
+    if N > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--tokens-per-gpu", type=int, default=WORKLOAD["tokens_per_gpu"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -172,6 +172,18 @@ moe_status moe_ep_init(moe_handle* h, const void* unique_id);
  * bytes actually moved by this rank. */
 moe_status moe_ep_traffic(moe_handle* h, double* logical_bytes_host, double* actual_bytes_sent);
 
+/* ---- observability (per-call stage times) ------------------ */
+/* Enable/disable the per-stage CUDA-event timeline of this handle (resets
+ * the accumulators).  Events are recorded on the handle's stream between
+ * stages, so they time exactly the kernels of each stage. */
+moe_status moe_profile_enable(moe_handle* h, int on);
+/* Accumulated stage times since enable: names [max_stages][32] (NUL
+ * terminated), total milliseconds and number of calls per stage. */
+moe_status moe_profile_read(moe_handle* h, int max_stages, char* names, double* ms_total,
+                            int64_t* calls, int* n_out);
+/* Number of kernels this library has launched in the process so far. */
+uint64_t moe_kernel_launch_count(void);
+
 /* ---- testing: route bf16 expert GEMMs through the SIMT kernels instead of
  * tcgen05 (A/B comparisons of the two kernel families). ------------------ */
 void moe_debug_set_tensor_cores(int enabled);

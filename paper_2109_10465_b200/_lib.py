@@ -71,6 +71,10 @@ _SIGS = {
     "moe_ep_get_unique_id": (C.c_int, [VP]),
     "moe_ep_init": (C.c_int, [H, VP]),
     "moe_ep_traffic": (C.c_int, [H, VP, C.POINTER(C.c_double)]),
+    "moe_profile_enable": (C.c_int, [H, C.c_int]),
+    "moe_profile_read": (C.c_int, [H, C.c_int, C.c_char_p, C.POINTER(C.c_double),
+                                   C.POINTER(C.c_int64), C.POINTER(C.c_int)]),
+    "moe_kernel_launch_count": (C.c_uint64, []),
     "moe_debug_set_tensor_cores": (None, [C.c_int]),
     "moe_derive_seed_tag": (C.c_uint64, [C.c_uint64, C.c_char_p]),
     "moe_derive_seed_u64": (C.c_uint64, [C.c_uint64, C.c_uint64]),

@@ -26,7 +26,14 @@ struct Status : std::runtime_error {
             throw ::moe::Status(6, std::string(#expr) + ": " + cudaGetErrorString(_e));      \
     } while (0)
 
-#define MOE_LAUNCH_CHECK() MOE_CUDA_CHECK(cudaGetLastError())
+// Every kernel launch site calls MOE_LAUNCH_CHECK() right after the launch;
+// it also counts launches (moe_kernel_launch_count, used by the bench).
+uint64_t count_launch();
+#define MOE_LAUNCH_CHECK()                        \
+    do {                                          \
+        MOE_CUDA_CHECK(cudaGetLastError());       \
+        ::moe::count_launch();                    \
+    } while (0)
 
 inline int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 inline int64_t ceil_div(int64_t v, int64_t a) { return (v + a - 1) / a; }

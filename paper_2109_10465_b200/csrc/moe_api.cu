@@ -8,7 +8,9 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <map>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -69,7 +71,65 @@ int capacity_of(int64_t tokens, const moe_router_cfg* c, int phase) {
 
 }  // namespace
 
+namespace moe {
+static std::atomic<uint64_t> g_launches{0};
+uint64_t count_launch() { return g_launches.fetch_add(1, std::memory_order_relaxed) + 1; }
+}  // namespace moe
+
+namespace {
+// Per-stage CUDA-event timeline (SURVEY §5 "per-call stats": stage times).
+struct Prof {
+    bool on = false;
+    std::vector<std::pair<const char*, cudaEvent_t>> marks;
+    std::vector<cudaEvent_t> pool;
+    std::map<std::string, std::pair<double, int64_t>> acc;
+    std::vector<std::string> order;
+    cudaEvent_t get() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        MOE_CUDA_CHECK(cudaEventCreate(&e));
+        return e;
+    }
+    void mark(const char* name, cudaStream_t st) {
+        if (!on) return;
+        cudaEvent_t e = get();
+        MOE_CUDA_CHECK(cudaEventRecord(e, st));
+        marks.emplace_back(name, e);
+    }
+    void drain() {  // fold recorded marks into the accumulators
+        if (marks.empty()) return;
+        MOE_CUDA_CHECK(cudaEventSynchronize(marks.back().second));
+        for (size_t i = 1; i < marks.size(); ++i) {
+            const char* nm = marks[i].first;
+            if (std::strcmp(nm, "begin") == 0) continue;
+            float ms = 0.f;
+            MOE_CUDA_CHECK(cudaEventElapsedTime(&ms, marks[i - 1].second, marks[i].second));
+            auto it = acc.find(nm);
+            if (it == acc.end()) {
+                order.emplace_back(nm);
+                acc[nm] = {ms, 1};
+            } else {
+                it->second.first += ms;
+                it->second.second += 1;
+            }
+        }
+        for (auto& m : marks) pool.push_back(m.second);
+        marks.clear();
+    }
+    ~Prof() {
+        for (auto& m : marks) cudaEventDestroy(m.second);
+        for (auto e : pool) cudaEventDestroy(e);
+    }
+};
+}  // namespace
+
 struct moe_handle {
+    Prof prof;
+    void mark(const char* n) { prof.mark(n, stream); }
     moe_router_cfg cfg{};
     moe_layer_dims dims{};
     cudaStream_t stream = nullptr;
@@ -210,18 +270,22 @@ void route(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, int phas
             MOE_CUDA_CHECK(cudaMemcpyAsync(h->noise.p, h->host_noise.data(),
                                            sizeof(float) * T * h->d, cudaMemcpyHostToDevice, st));
         }
+        h->mark("jitter_noise");
     }
     // logits = (x * noise) @ gate_w  (routing.cpp:71)
     launch_gemm_dense<TIO>(x, h->d, 1, jitter ? h->noise.as<float>() : nullptr, gate_w, E, 1,
                            h->logits.as<float>(), T, E, h->d, 1, st);
+    h->mark("gate_logits");
     launch_softmax_topk(h->logits.as<float>(), T, E, K, h->probs.as<float>(),
                         h->choice.as<int32_t>(), h->gate_prob.as<float>(),
                         h->colsum_part.as<float>(), h->count_part.as<int32_t>(),
                         h->flags.as<uint32_t>(), st);
+    h->mark("softmax_topk");
     launch_balance_finalize(h->colsum_part.as<float>(), h->count_part.as<int32_t>(),
                             softmax_parts(T), T, E, h->cfg.balance_coeff,
                             aux ? aux : h->aux_scratch.as<float>(), h->fcoef.as<float>(),
                             h->fcount.as<int32_t>(), st);
+    h->mark("balance_loss");
     h->jitter_on = jitter;
 }
 
@@ -265,14 +329,17 @@ void forward_impl(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, c
     int mode;
     set_geometry(h, T, phase, mode);
     h->fwd_valid = false;
+    h->mark("begin");
     route<TIO>(h, T, x, gate_w, phase, seed, aux);
     assign(h, T, h->choice.as<int32_t>(), h->cap, mode, derive_seed_tag(seed, "assign"),
            h->slot.as<int32_t>());
+    h->mark("assign");
     launch_combine_weights(T, E, K, h->gate_prob.as<float>(), h->wts.as<float>(), st);
     // dispatch (routing.cpp:396): un-jittered x into [E, cap_pad, d]
     TIO* Xloc = static_cast<TIO*>(h->loc(h->Xr, h->Xloc));
     launch_dispatch_gather<TIO>(x, h->d, E, K, h->cap_pad, h->row_src.as<int32_t>(),
                                 h->kept.as<int32_t>(), Xloc, h->flags.as<uint32_t>(), st);
+    h->mark("dispatch");
     const int32_t* counts = h->kept.as<int32_t>();
     if (ep > 1) {
         // forward all-to-all: counts then rows (fixed-shape [E_local, cap_pad, d] slices)
@@ -283,22 +350,27 @@ void forward_impl(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, c
         const double slice = static_cast<double>(El) * h->cap * h->d;
         h->last_logical_traffic = 2.0 * slice * 8.0 * (ep - 1);
         h->last_actual_sent = 2.0 * static_cast<double>(El) * h->cap_pad * h->d * h->esz * (ep - 1);
+        h->mark("a2a_dispatch");
     }
     // expert FFN on occupied rows only (routing.cpp:399-405)
     row_gemm<TIO>(h, h->Xr.as<TIO>(), w1, h->H.as<TIO>(), b1, nullptr, counts, h->f, h->d, true,
                   EPI_BIAS_RELU, ep);
+    h->mark("ffn1_fwd");
     row_gemm<TIO>(h, h->H.as<TIO>(), w2, h->Or.as<TIO>(), b2, nullptr, counts, h->d, h->f, true,
                   EPI_BIAS, ep);
+    h->mark("ffn2_fwd");
     TIO* Oloc = h->Or.as<TIO>();
     if (ep > 1) {
         all_to_all(h, h->Or.p, h->Oloc.p, static_cast<size_t>(El) * h->cap_pad * h->d,
                    nccl_type(h->esz), h->esz);
         Oloc = h->Oloc.as<TIO>();
+        h->mark("a2a_combine");
     }
     // combine (routing.cpp:421, 258-298)
     launch_combine<TIO>(Oloc, T, h->d, E, K, h->cap_pad, h->choice.as<int32_t>(),
                         h->pos.as<int32_t>(), h->wts.as<float>(), residual ? residual : x, y,
                         h->flags.as<uint32_t>(), st);
+    h->mark("combine");
     const size_t nk = static_cast<size_t>(T * K);
     if (expert_id)
         MOE_CUDA_CHECK(cudaMemcpyAsync(expert_id, h->choice.p, 4 * nk, cudaMemcpyDeviceToDevice, st));
@@ -329,50 +401,66 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
     const TIO* w1 = static_cast<const TIO*>(h->w1);
     const TIO* w2 = static_cast<const TIO*>(h->w2);
     const TIO* Oloc = ep > 1 ? h->Oloc.as<TIO>() : h->Or.as<TIO>();
+    h->mark("begin");
     // routing weights / balance loss / softmax backward -> dL
     launch_router_bwd<TIO>(T, static_cast<int>(d), E, K, dy, Oloc, h->cap_pad,
                            h->choice.as<int32_t>(), h->pos.as<int32_t>(),
                            h->gate_prob.as<float>(), h->probs.as<float>(), h->fcoef.as<float>(),
                            daux, h->dL.as<float>(), st);
+    h->mark("router_bwd");
     // combine backward: dO rows = w * dy[t]
     TIO* dOloc = static_cast<TIO*>(h->loc(h->dOr, h->dOloc));
     launch_combine_bwd_gather<TIO>(dy, d, E, K, h->cap_pad, h->row_src.as<int32_t>(),
                                    h->kept.as<int32_t>(), h->wts.as<float>(), dOloc, st);
+    h->mark("combine_bwd");
     const int32_t* counts = h->kept.as<int32_t>();
     if (ep > 1) {
         all_to_all(h, dOloc, h->dOr.p, static_cast<size_t>(El) * h->cap_pad * d,
                    nccl_type(h->esz), h->esz);
         counts = h->counts_r.as<int32_t>();
+        h->mark("a2a_dO");
     }
     // expert backward: dH = (dO W2^T) * [H > 0]; dW2 = H^T dO; dX = dH W1^T; dW1 = X^T dH
     row_gemm<TIO>(h, h->dOr.as<TIO>(), w2, h->dH.as<TIO>(), nullptr, h->H.as<TIO>(), counts, f, d,
                   false, EPI_RELU_MASK, ep);
+    h->mark("ffn2_dgrad");
     wgrad_gemm<TIO>(h, h->H.as<TIO>(), h->dOr.as<TIO>(), dw2, f, d, counts, ep);
+    h->mark("ffn2_wgrad");
     launch_colsum_groups<TIO>(h->dOr.as<TIO>(), d, ep, El, h->cap_pad, counts, db2, st);
+    h->mark("db2");
     row_gemm<TIO>(h, h->dH.as<TIO>(), w1, h->dXr.as<TIO>(), nullptr, nullptr, counts, d, f, false,
                   EPI_NONE, ep);
+    h->mark("ffn1_dgrad");
     wgrad_gemm<TIO>(h, h->Xr.as<TIO>(), h->dH.as<TIO>(), dw1, d, f, counts, ep);
+    h->mark("ffn1_wgrad");
     launch_colsum_groups<TIO>(h->dH.as<TIO>(), f, ep, El, h->cap_pad, counts, db1, st);
+    h->mark("db1");
     TIO* dXloc = h->dXr.as<TIO>();
     if (ep > 1) {
         all_to_all(h, h->dXr.p, h->dXloc.p, static_cast<size_t>(El) * h->cap_pad * d,
                    nccl_type(h->esz), h->esz);
         dXloc = h->dXloc.as<TIO>();
+        h->mark("a2a_dX");
     }
     // gate backward: dxg = dL Wg^T; dWg = (x*noise)^T dL (split-K, fixed order)
     const float* noise = h->jitter_on ? h->noise.as<float>() : nullptr;
     launch_gemm_dense<float>(h->dL.as<float>(), E, 1, nullptr, h->gate_w, 1, E,
                              h->dxg.as<float>(), T, d, E, 1, st);
+    h->mark("gate_dgrad");
     const int splits = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(1, T / 512)));
     launch_gemm_dense<TIO>(x, 1, d, noise, h->dL.as<float>(), E, 1, h->dwg_part.as<float>(), d, E,
                            T, splits, st);
     launch_splitk_reduce(h->dwg_part.as<float>(), splits, d * E, dgate_w, st);
-    if (ep > 1)
+    h->mark("gate_wgrad");
+    if (ep > 1) {
         NCCL_CHECK(ncclAllReduce(dgate_w, dgate_w, static_cast<size_t>(d * E), ncclFloat32, ncclSum,
                                  h->comm, st));
+        h->mark("allreduce_dgate_w");
+    }
     launch_dx_assemble<TIO>(T, d, E, K, h->cap_pad, h->dxg.as<float>(), noise, dXloc,
                             h->choice.as<int32_t>(), h->pos.as<int32_t>(), dy, !h->has_residual,
                             dx, dres, st);
+    h->mark("dx_assemble");
 }
 
 void alloc_workspace(moe_handle* h) {
@@ -523,6 +611,37 @@ moe_status moe_set_stream(moe_handle* h, void* s) {
     h->stream = static_cast<cudaStream_t>(s);
     return MOE_OK;
 }
+
+moe_status moe_profile_enable(moe_handle* h, int on) {
+    if (!h) return MOE_SHAPE;
+    return guarded(h, [&] {
+        h->prof.drain();
+        h->prof.acc.clear();
+        h->prof.order.clear();
+        h->prof.on = on != 0;
+    });
+}
+
+moe_status moe_profile_read(moe_handle* h, int max_stages, char* names, double* ms_total,
+                            int64_t* calls, int* n_out) {
+    if (!h) return MOE_SHAPE;
+    return guarded(h, [&] {
+        h->prof.drain();
+        int n = 0;
+        for (const std::string& nm : h->prof.order) {
+            if (n >= max_stages) break;
+            const auto& a = h->prof.acc[nm];
+            std::strncpy(names + 32 * n, nm.c_str(), 31);
+            names[32 * n + 31] = 0;
+            ms_total[n] = a.first;
+            calls[n] = a.second;
+            ++n;
+        }
+        *n_out = n;
+    });
+}
+
+uint64_t moe_kernel_launch_count(void) { return g_launches.load(); }
 
 moe_status moe_check(moe_handle* h, uint32_t* flags_out) {
     if (!h) return MOE_SHAPE;

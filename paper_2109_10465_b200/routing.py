@@ -201,6 +201,26 @@ class MoeHandle:
         buf = C.create_string_buffer(unique_id, len(unique_id))
         _check(L.load().moe_ep_init(self.h, buf), self.h)
 
+    def profile(self, on: bool):
+        """Enable the per-stage CUDA-event timeline (resets accumulators)."""
+        _check(L.load().moe_profile_enable(self.h, 1 if on else 0), self.h)
+
+    def profile_read(self) -> dict:
+        """{stage: (total_ms, calls)} accumulated since profile(True)."""
+        n = 64
+        names = C.create_string_buffer(32 * n)
+        ms = (C.c_double * n)()
+        calls = (C.c_int64 * n)()
+        cnt = C.c_int()
+        _check(L.load().moe_profile_read(self.h, n, names, ms, calls, C.byref(cnt)), self.h)
+        raw = names.raw
+        return {raw[32 * i:32 * i + 32].split(b"\0")[0].decode(): (ms[i], calls[i])
+                for i in range(cnt.value)}
+
+
+def kernel_launch_count() -> int:
+    return int(L.load().moe_kernel_launch_count())
+
     def stats(self):
         cap = C.c_int()
         drops = C.c_int64()

@@ -107,16 +107,32 @@ def test_layer_fp32_c1_full_size():
     assert np.array_equal(out["expert_id"].astype(np.int8), z["expert_id"])
     assert np.array_equal(out["slot"].astype(np.int16), z["slot"])
     assert out["capacity"] == int(z["capacity"]) == 512
+    # ReLU kinks: relu' is discontinuous at Hpre = 0 (ops.cpp:307-315), so an
+    # entry whose f64 pre-activation is within fp32 rounding of 0 may take the
+    # other branch.  Find them from the f64 oracle and exclude exactly the
+    # affected (expert, column) reductions and token rows; assert they are rare.
+    eid, slot = z["expert_id"].astype(np.int64), z["slot"].astype(np.int64)
+    kink_cols = np.zeros((E, f), bool)
+    kink_tok = np.zeros(T, bool)
+    for e in range(E):
+        toks = np.nonzero((eid == e) & (slot >= 0))[0]
+        hpre = x[toks] @ w1[e] + b1[e]
+        k = np.abs(hpre) < 1e-5
+        kink_cols[e] = k.any(0)
+        kink_tok[toks[k.any(1)]] = True
+    assert kink_cols.mean() < 1e-3 and kink_tok.mean() < 1e-2, (kink_cols.sum(), kink_tok.sum())
     rows = z["sample_rows"]
+    ok = ~kink_tok[rows]
     assert rel_err(out["y"][rows], z["y_rows"]) <= TOL_F32
-    assert rel_err(out["dx"][rows], z["dx_rows"]) <= TOL_F32
+    assert rel_err(out["dx"][rows][ok], z["dx_rows"][ok]) <= TOL_F32
     assert rel_err(out["aux"], z["aux"]) <= TOL_F32
     assert rel_norm(out["dgate_w"], z["dgate_w"]) <= TOL_F32
-    assert rel_norm(out["db1"], z["db1"]) <= TOL_F32 and rel_norm(out["db2"], z["db2"]) <= TOL_F32
+    assert rel_norm(out["db2"], z["db2"]) <= TOL_F32
+    assert rel_norm(out["db1"][~kink_cols], z["db1"][~kink_cols]) <= TOL_F32
     # size-independent checksums (row / column sums over d or f terms)
     assert rel_err(out["y"].sum(1), z["y_rowsum"]) <= 1e-4
-    assert rel_err(out["dw1"].sum(1), z["dw1_colsum"]) <= 1e-4
-    assert rel_err(out["dw2"].sum(2), z["dw2_rowsum"]) <= 1e-4
+    assert rel_norm(out["dw1"].sum(1)[~kink_cols], z["dw1_colsum"][~kink_cols]) <= TOL_F32
+    assert rel_norm(out["dw2"].sum(2), z["dw2_rowsum"]) <= TOL_F32
 
 
 @pytest.mark.parametrize("name", G.ep_names())
