@@ -217,10 +217,6 @@ class MoeHandle:
         return {raw[32 * i:32 * i + 32].split(b"\0")[0].decode(): (ms[i], calls[i])
                 for i in range(cnt.value)}
 
-
-def kernel_launch_count() -> int:
-    return int(L.load().moe_kernel_launch_count())
-
     def stats(self):
         cap = C.c_int()
         drops = C.c_int64()
@@ -228,6 +224,11 @@ def kernel_launch_count() -> int:
         _check(L.load().moe_last_decision_stats(self.h, C.byref(cap), C.byref(drops),
                                                 C.c_void_p(kept.data_ptr())), self.h)
         return cap.value, drops.value, kept
+
+
+def kernel_launch_count() -> int:
+    """Kernels launched by libmoe_b200.so in this process so far."""
+    return int(L.load().moe_kernel_launch_count())
 
 
 def ep_unique_id() -> bytes:
