@@ -187,6 +187,12 @@ uint64_t moe_kernel_launch_count(void);
 /* ---- testing: route bf16 expert GEMMs through the SIMT kernels instead of
  * tcgen05 (A/B comparisons of the two kernel families). ------------------ */
 void moe_debug_set_tensor_cores(int enabled);
+/* testing: raw mt19937_64 outputs [c*J, c*J + n) of Rng(seed) reconstructed
+ * on the host through the jump-ahead polynomial the device generator uses. */
+moe_status moe_debug_mt64_chunk_host(uint64_t seed, int64_t J, int c, int64_t n, uint64_t* out);
+/* testing: the first `count` raw outputs of Rng(seed) from the device
+ * generator into device memory out_dev. */
+moe_status moe_debug_mt64_device(uint64_t seed, int64_t count, uint64_t* out_dev);
 
 /* ---- RNG streams (rng.cpp:15-102), host, bit-exact -------------------- */
 uint64_t moe_derive_seed_tag(uint64_t seed, const char* tag);

@@ -76,6 +76,8 @@ _SIGS = {
                                    C.POINTER(C.c_int64), C.POINTER(C.c_int)]),
     "moe_kernel_launch_count": (C.c_uint64, []),
     "moe_debug_set_tensor_cores": (None, [C.c_int]),
+    "moe_debug_mt64_chunk_host": (C.c_int, [C.c_uint64, C.c_int64, C.c_int, C.c_int64, VP]),
+    "moe_debug_mt64_device": (C.c_int, [C.c_uint64, C.c_int64, VP]),
     "moe_derive_seed_tag": (C.c_uint64, [C.c_uint64, C.c_char_p]),
     "moe_derive_seed_u64": (C.c_uint64, [C.c_uint64, C.c_uint64]),
 }

@@ -148,3 +148,18 @@ void launch_balance_from_probs(const float* probs, int64_t T, int E, int K,
                                float* colsum_part, int32_t* count_part, uint32_t* flags,
                                cudaStream_t st);
 }  // namespace moe
+
+namespace moe {
+// gate.cu: register-tiled gate GEMMs (require gate_fast_ok(d, E))
+bool gate_fast_ok(int d, int E);
+template <class TX>
+void launch_gate_logits(const TX* x, const float* noise, const float* wg, float* logits,
+                        int64_t T, int d, int E, cudaStream_t st);
+template <class TIO>
+void launch_gate_dx(int64_t T, int d, int E, int K, int cap_pad, const float* dL, const float* wg,
+                    const float* noise, const TIO* dX, const int32_t* choice, const int32_t* pos,
+                    const TIO* dy, bool residual_is_x, TIO* dx, TIO* dres, cudaStream_t st);
+template <class TX>
+void launch_gate_dw(const TX* x, const float* noise, const float* dL, float* part, int64_t T,
+                    int d, int E, int splits, cudaStream_t st);
+}  // namespace moe

@@ -148,7 +148,6 @@ struct moe_handle {
     DevMem dL, dxg, dwg_part;
     AssignScratch as{};
     std::vector<uint32_t> host_ord;
-    std::vector<float> host_noise;
 
     // forward context
     bool fwd_valid = false;
@@ -262,19 +261,18 @@ void route(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, int phas
     const bool jitter = phase == MOE_TRAIN && h->cfg.jitter_eps > 0.0;
     if (jitter) {
         // routing.cpp:62-70: noise stream Rng(derive_seed(seed, "jitter")), row-major
+        // generated on the device by jump-ahead (rng.cu)
         const uint64_t js = derive_seed_tag(seed, "jitter");
-        const double eps = h->cfg.jitter_eps;
-        if (!launch_jitter_noise_device(js, T * h->d, eps, h->noise.as<float>(), st)) {
-            h->host_noise.resize(static_cast<size_t>(T * h->d));
-            uniform_f32(js, 1.0 - eps, 1.0 + eps, T * h->d, h->host_noise.data());
-            MOE_CUDA_CHECK(cudaMemcpyAsync(h->noise.p, h->host_noise.data(),
-                                           sizeof(float) * T * h->d, cudaMemcpyHostToDevice, st));
-        }
+        launch_jitter_noise_device(js, T * h->d, h->cfg.jitter_eps, h->noise.as<float>(), st);
         h->mark("jitter_noise");
     }
     // logits = (x * noise) @ gate_w  (routing.cpp:71)
-    launch_gemm_dense<TIO>(x, h->d, 1, jitter ? h->noise.as<float>() : nullptr, gate_w, E, 1,
-                           h->logits.as<float>(), T, E, h->d, 1, st);
+    if (gate_fast_ok(static_cast<int>(h->d), E))
+        launch_gate_logits<TIO>(x, jitter ? h->noise.as<float>() : nullptr, gate_w,
+                                h->logits.as<float>(), T, static_cast<int>(h->d), E, st);
+    else
+        launch_gemm_dense<TIO>(x, h->d, 1, jitter ? h->noise.as<float>() : nullptr, gate_w, E, 1,
+                               h->logits.as<float>(), T, E, h->d, 1, st);
     h->mark("gate_logits");
     launch_softmax_topk(h->logits.as<float>(), T, E, K, h->probs.as<float>(),
                         h->choice.as<int32_t>(), h->gate_prob.as<float>(),
@@ -444,12 +442,15 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
     }
     // gate backward: dxg = dL Wg^T; dWg = (x*noise)^T dL (split-K, fixed order)
     const float* noise = h->jitter_on ? h->noise.as<float>() : nullptr;
-    launch_gemm_dense<float>(h->dL.as<float>(), E, 1, nullptr, h->gate_w, 1, E,
-                             h->dxg.as<float>(), T, d, E, 1, st);
-    h->mark("gate_dgrad");
+    const bool fast = gate_fast_ok(static_cast<int>(d), E);
     const int splits = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(1, T / 512)));
-    launch_gemm_dense<TIO>(x, 1, d, noise, h->dL.as<float>(), E, 1, h->dwg_part.as<float>(), d, E,
-                           T, splits, st);
+    if (fast) {
+        launch_gate_dw<TIO>(x, noise, h->dL.as<float>(), h->dwg_part.as<float>(), T,
+                            static_cast<int>(d), E, splits, st);
+    } else {
+        launch_gemm_dense<TIO>(x, 1, d, noise, h->dL.as<float>(), E, 1, h->dwg_part.as<float>(), d,
+                               E, T, splits, st);
+    }
     launch_splitk_reduce(h->dwg_part.as<float>(), splits, d * E, dgate_w, st);
     h->mark("gate_wgrad");
     if (ep > 1) {
@@ -457,10 +458,18 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
                                  h->comm, st));
         h->mark("allreduce_dgate_w");
     }
-    launch_dx_assemble<TIO>(T, d, E, K, h->cap_pad, h->dxg.as<float>(), noise, dXloc,
-                            h->choice.as<int32_t>(), h->pos.as<int32_t>(), dy, !h->has_residual,
-                            dx, dres, st);
-    h->mark("dx_assemble");
+    if (fast) {  // dx = (dL Wg^T) * noise + dispatch bwd + residual, one kernel
+        launch_gate_dx<TIO>(T, static_cast<int>(d), E, K, h->cap_pad, h->dL.as<float>(), h->gate_w,
+                            noise, dXloc, h->choice.as<int32_t>(), h->pos.as<int32_t>(), dy,
+                            !h->has_residual, dx, dres, st);
+    } else {
+        launch_gemm_dense<float>(h->dL.as<float>(), E, 1, nullptr, h->gate_w, 1, E,
+                                 h->dxg.as<float>(), T, d, E, 1, st);
+        launch_dx_assemble<TIO>(T, d, E, K, h->cap_pad, h->dxg.as<float>(), noise, dXloc,
+                                h->choice.as<int32_t>(), h->pos.as<int32_t>(), dy,
+                                !h->has_residual, dx, dres, st);
+    }
+    h->mark("gate_dx");
 }
 
 void alloc_workspace(moe_handle* h) {
@@ -732,15 +741,9 @@ moe_status moe_gate(moe_handle* h, int64_t T, const void* x, const float* gate_w
         cudaStream_t st = h->stream;
         const int E = h->E, K = h->K;
         const bool jitter = phase == MOE_TRAIN && h->cfg.jitter_eps > 0.0;
-        if (jitter) {
-            const double eps = h->cfg.jitter_eps;
-            if (!launch_jitter_noise_device(jitter_seed, T * h->d, eps, h->noise.as<float>(), st)) {
-                h->host_noise.resize(static_cast<size_t>(T * h->d));
-                uniform_f32(jitter_seed, 1.0 - eps, 1.0 + eps, T * h->d, h->host_noise.data());
-                MOE_CUDA_CHECK(cudaMemcpyAsync(h->noise.p, h->host_noise.data(),
-                                               sizeof(float) * T * h->d, cudaMemcpyHostToDevice, st));
-            }
-        }
+        if (jitter)
+            launch_jitter_noise_device(jitter_seed, T * h->d, h->cfg.jitter_eps,
+                                       h->noise.as<float>(), st);
         const float* nz = jitter ? h->noise.as<float>() : nullptr;
         if (h->esz == 2)
             launch_gemm_dense<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(x), h->d, 1, nz,
@@ -872,3 +875,21 @@ moe_status moe_ep_traffic(moe_handle* h, double* logical_bytes_host, double* act
 }
 
 }  // extern "C"
+
+// ---- debug entry points for the device mt19937_64 generator (tests) ------
+namespace moe {
+void host_mt64_chunk(uint64_t seed, int64_t J, int P, int c, int64_t n, uint64_t* out);
+void launch_mt64_raw_device(uint64_t seed, int64_t count, uint64_t* out, cudaStream_t st);
+}  // namespace moe
+
+extern "C" {
+moe_status moe_debug_mt64_chunk_host(uint64_t seed, int64_t J, int c, int64_t n, uint64_t* out) {
+    return guarded(nullptr, [&] { moe::host_mt64_chunk(seed, J, 1, c, n, out); });
+}
+moe_status moe_debug_mt64_device(uint64_t seed, int64_t count, uint64_t* out_dev) {
+    return guarded(nullptr, [&] {
+        moe::launch_mt64_raw_device(seed, count, out_dev, nullptr);
+        MOE_CUDA_CHECK(cudaDeviceSynchronize());
+    });
+}
+}

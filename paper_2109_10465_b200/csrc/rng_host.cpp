@@ -39,12 +39,4 @@ void permutation(uint64_t seed, int64_t n, uint32_t* out) {
     }
 }
 
-void uniform_f32(uint64_t seed, double lo, double hi, int64_t n, float* out) {
-    std::mt19937_64 eng(seed);
-    for (int64_t i = 0; i < n; ++i) {
-        const double u = static_cast<double>(eng() >> 11) * 0x1.0p-53;
-        out[i] = static_cast<float>(lo + (hi - lo) * u);
-    }
-}
-
 }  // namespace moe

@@ -15,7 +15,5 @@ uint64_t derive_seed_tag(uint64_t seed, const char* tag);  // rng.cpp:24-30
 uint64_t derive_seed_u64(uint64_t seed, uint64_t salt);    // rng.cpp:32-34
 // Rng(seed).permutation(n), rng.cpp:94-102 (Fisher-Yates, rejection uniform_int)
 void permutation(uint64_t seed, int64_t n, uint32_t* out);
-// n draws of Rng(seed).uniform(lo, hi) rounded to float (routing.cpp:64-68)
-void uniform_f32(uint64_t seed, double lo, double hi, int64_t n, float* out);
 
 }  // namespace moe
