@@ -34,22 +34,26 @@ namespace moe {
 namespace tc {
 
 constexpr int BM = 128, BN = 256, BK = 64;
-constexpr int kStages = 4;
+constexpr int kStages = 3;
 constexpr int kThreads = 192;  // 6 warps
-constexpr int kEpiWarp0 = 2;
 constexpr uint32_t kTileABytes = BM * BK * 2;  // 16 KB
 constexpr uint32_t kTileBBytes = BN * BK * 2;  // 32 KB
 constexpr uint32_t kStageBytes = kTileABytes + kTileBBytes;
+// epilogue staging: per epilogue warp, 2 buffers of 32 rows x 64 bf16 (128 B
+// rows, 128B-swizzled) drained by TMA bulk tensor stores
+constexpr uint32_t kStageCBytes = 32 * 64 * 2;  // 4 KB
+constexpr uint32_t kEpiBytes = 4 * 2 * kStageCBytes;
 constexpr int kMaxSegs = 1024;
 constexpr int kMaxGroups = 256;
-constexpr size_t kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + 1024 /*barriers*/ +
-                              4 * (kMaxSegs + 3 * kMaxGroups + 8);
+constexpr size_t kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + kEpiBytes +
+                              1024 /*barriers*/ + 4 * (kMaxSegs + 3 * kMaxGroups + 8);
 
 enum Kind { ROW = 0, WGRAD = 1 };
 
 struct __align__(64) Params {
     CUtensorMap tmA;
     CUtensorMap tmB;
+    CUtensorMap tmC;  // output, box {64 cols, 32 rows}, 128B swizzle
     void* C;
     const float* bias;
     const __nv_bfloat16* mask;
@@ -201,12 +205,14 @@ __global__ void __launch_bounds__(kThreads, 1) grouped_gemm_kernel(const __grid_
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* tiles = smem;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+    uint8_t* cstage = smem + kStages * kStageBytes;  // [4 warps][2][4 KB]
+    uint8_t* misc = cstage + kEpiBytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(misc);
     uint64_t* empty = full + kStages;
     uint64_t* tfull = empty + kStages;   // [2]
     uint64_t* tempty = tfull + 2;        // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    int32_t* seg_cnt = reinterpret_cast<int32_t*>(smem + kStages * kStageBytes + 1024);
+    int32_t* seg_cnt = reinterpret_cast<int32_t*>(misc + 1024);
     int32_t* grp_mt = seg_cnt + kMaxSegs;
     int32_t* grp_base = grp_mt + kMaxGroups;
 
@@ -226,6 +232,7 @@ __global__ void __launch_bounds__(kThreads, 1) grouped_gemm_kernel(const __grid_
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         prefetch_tmap(&p.tmA);
         prefetch_tmap(&p.tmB);
+        prefetch_tmap(&p.tmC);
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -369,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, 1) grouped_gemm_kernel(const __grid_
         const int row_in_tile = quarter * 32 + lane;
         int acc = 0;
         uint32_t acc_phase = 0;
-        __nv_bfloat16* C = static_cast<__nv_bfloat16*>(p.C);
+        uint32_t cbuf = 0;
         for (int t = blockIdx.x; t < s.total; t += gridDim.x) {
             int64_t crow;
             int64_t ncol0;
@@ -398,33 +405,42 @@ __global__ void __launch_bounds__(kThreads, 1) grouped_gemm_kernel(const __grid_
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16);
-            __nv_bfloat16* crow_ptr = C + crow * p.N + ncol0;
+            const int32_t box_row = static_cast<int32_t>(crow - lane);  // this warp's 32 rows
 #pragma unroll 1
-            for (int c = 0; c < BN; c += 32) {
-                uint32_t v[32];
-                tmem_ld32(tbase + c, v);
-                float f[32];
+            for (int c = 0; c < BN; c += 64) {
+                float f[64];
+                {
+                    uint32_t v[32];
+                    tmem_ld32(tbase + c, v);
 #pragma unroll
-                for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+                    for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+                    tmem_ld32(tbase + c + 32, v);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) f[32 + j] = __uint_as_float(v[j]);
+                }
+                if (c + 64 == BN) {  // accumulator fully read: MMA may reuse it
+                    tc_fence_before();
+                    mbar_arrive(&tempty[acc]);
+                }
                 if (!have_acc || !valid) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) f[j] = 0.f;
+                    for (int j = 0; j < 64; ++j) f[j] = 0.f;
                 } else if (KIND == ROW) {
                     if (p.epi == EPI_BIAS || p.epi == EPI_BIAS_RELU) {
                         const float* b = p.bias + static_cast<int64_t>(le) * p.N + ncol0 + c;
 #pragma unroll
-                        for (int j = 0; j < 32; j += 4) {
+                        for (int j = 0; j < 64; j += 4) {
                             const float4 bb = __ldg(reinterpret_cast<const float4*>(b + j));
                             f[j] += bb.x; f[j + 1] += bb.y; f[j + 2] += bb.z; f[j + 3] += bb.w;
                         }
                         if (p.epi == EPI_BIAS_RELU) {
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) f[j] = f[j] > 0.f ? f[j] : 0.f;
+                            for (int j = 0; j < 64; ++j) f[j] = f[j] > 0.f ? f[j] : 0.f;
                         }
                     } else if (p.epi == EPI_RELU_MASK) {
                         const uint4* mp = reinterpret_cast<const uint4*>(p.mask + crow * p.N + ncol0 + c);
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
+                        for (int q = 0; q < 8; ++q) {
                             uint4 u = __ldg(mp + q);
                             const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u);
 #pragma unroll
@@ -433,20 +449,35 @@ __global__ void __launch_bounds__(kThreads, 1) grouped_gemm_kernel(const __grid_
                         }
                     }
                 }
-                uint4* dst = reinterpret_cast<uint4*>(crow_ptr + c);
+                // stage the warp's 32 x 64 bf16 block (128B-swizzled rows) and
+                // hand it to the TMA engine; two buffers alternate per warp
+                uint8_t* sbuf = cstage + ((quarter * 2 + (cbuf & 1)) * kStageCBytes);
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                __syncwarp();
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
+                for (int q = 0; q < 8; ++q) {
                     uint4 u;
                     __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
 #pragma unroll
                     for (int j = 0; j < 4; ++j) h2[j] = __floats2bfloat162_rn(f[q * 8 + 2 * j], f[q * 8 + 2 * j + 1]);
-                    dst[q] = u;
+                    *reinterpret_cast<uint4*>(sbuf + lane * 128 + ((q ^ (lane & 7)) << 4)) = u;
                 }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+                    asm volatile(
+                        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                            reinterpret_cast<uint64_t>(&p.tmC)),
+                        "r"(smem_u32(sbuf)), "r"(static_cast<int32_t>(ncol0 + c)), "r"(box_row)
+                        : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+                ++cbuf;
             }
-            tc_fence_before();
-            mbar_arrive(&tempty[acc]);
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        __syncwarp();
     }
     __syncthreads();
     if (warp == 1) {
@@ -537,6 +568,7 @@ void launch_row_gemm_tc(const RowGemmArgs& a, cudaStream_t st) {
         p.tmB = tc::make_map(a.W, static_cast<int64_t>(a.El) * a.K, a.N, 64, tc::BK);
     else
         p.tmB = tc::make_map(a.W, static_cast<int64_t>(a.El) * a.N, a.K, tc::BK, tc::BN);
+    p.tmC = tc::make_map(a.C, rows, a.N, 64, 32);
     p.C = a.C;
     p.bias = a.bias;
     p.mask = static_cast<const __nv_bfloat16*>(a.mask);
@@ -558,6 +590,7 @@ void launch_wgrad_gemm_tc(const WgradGemmArgs& a, cudaStream_t st) {
     const int64_t rows = static_cast<int64_t>(a.ep) * a.El * a.cap_pad;
     p.tmA = tc::make_map(a.A, rows, a.M, 64, tc::BK);
     p.tmB = tc::make_map(a.B, rows, a.N, 64, tc::BK);
+    p.tmC = tc::make_map(a.C, static_cast<int64_t>(a.El) * a.M, a.N, 64, 32);
     p.C = a.C;
     p.counts = a.counts;
     p.N = a.N;

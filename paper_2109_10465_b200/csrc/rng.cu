@@ -242,64 +242,87 @@ __global__ void __launch_bounds__(kThreads) base_kernel(uint64_t seed, uint64_t*
     }
 }
 
+// New word i of the next 312-block computed from the OLD block only (the
+// reference twist updates in place; words >= 156 read already-updated words
+// 0..155, which we recompute locally), so a block needs one barrier.
+__device__ __forceinline__ uint64_t next_word(const uint64_t* __restrict__ o, int i) {
+    if (i < N - M) return twist(o[i], o[i + 1], o[i + M]);
+    if (i < N - 1) return twist(o[i], o[i + 1], twist(o[i - (N - M)], o[i - (N - M) + 1], o[i]));
+    // i == N-1: needs new[0] and new[M-1]
+    const uint64_t n0 = twist(o[0], o[1], o[M]);
+    const uint64_t nm = twist(o[M - 1], o[M], o[N - 1]);
+    return twist(o[N - 1], n0, nm);
+}
+
+constexpr int kChunkThreads = 2 * N + 16;  // 640: two threads per window word for the jump
+
 // One CTA per chunk: jump to the chunk's window, then generate J outputs.
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kChunkThreads, 1)
 chunk_kernel(const uint64_t* __restrict__ base, const uint64_t* __restrict__ jump, int64_t J,
              int64_t count, double lo, double span, float* __restrict__ noise,
              uint64_t* __restrict__ raw_out) {
     extern __shared__ uint64_t sm[];
     uint64_t* sb = sm;              // base [BASE]
     uint64_t* sg = sm + BASE;       // g_c  [W]
-    uint64_t* s = sg + W;           // window / state [N]
+    uint64_t* s0 = sg + W;          // ping [N]
+    uint64_t* s1 = s0 + N;          // pong [N]
     const int c = blockIdx.x;
     const int64_t q0 = static_cast<int64_t>(c) * J;
     if (q0 >= count) return;
     for (int i = threadIdx.x; i < BASE; i += blockDim.x) sb[i] = base[i];
     for (int i = threadIdx.x; i < W; i += blockDim.x) sg[i] = jump[static_cast<int64_t>(c) * W + i];
     __syncthreads();
-    // window word j = XOR_{i : g_i} base[j + i]
-    if (threadIdx.x < N) {
-        const int j = threadIdx.x;
-        uint64_t acc = 0;
-        for (int w = 0; w < W; ++w) {
-            uint64_t bits = sg[w];
-            const uint64_t* bp = sb + j + w * 64;
-            while (bits) {
-                const int b = __ffsll(static_cast<long long>(bits)) - 1;
-                bits &= bits - 1;
-                acc ^= bp[b];
+    // window word j = XOR_{i : g_i} base[j + i]; two threads per j (even / odd
+    // words of g), two independent accumulators each for load-latency ILP.
+    const int t = threadIdx.x;
+    if (t < 2 * N) {
+        const int j = t % N, part = t / N;
+        uint64_t a0 = 0, a1 = 0;
+        for (int w = part; w < W; w += 4) {
+            uint64_t b0 = sg[w];
+            uint64_t b1 = w + 2 < W ? sg[w + 2] : 0ULL;
+            const uint64_t* p0 = sb + j + w * 64;
+            const uint64_t* p1 = p0 + 128;
+            while (b0 | b1) {
+                if (b0) {
+                    const int b = __ffsll(static_cast<long long>(b0)) - 1;
+                    b0 &= b0 - 1;
+                    a0 ^= p0[b];
+                }
+                if (b1) {
+                    const int b = __ffsll(static_cast<long long>(b1)) - 1;
+                    b1 &= b1 - 1;
+                    a1 ^= p1[b];
+                }
             }
         }
-        s[j] = acc;
+        if (part == 1) s1[j] = a0 ^ a1;
+        __syncthreads();
+        if (part == 0) s0[j] = a0 ^ a1 ^ s1[j];
+    } else {
+        __syncthreads();
     }
     __syncthreads();
     const int64_t n = min(J, count - q0);
+    uint64_t* cur = s0;
+    uint64_t* nxt = s1;
     for (int64_t blk = 0; blk * N < n; ++blk) {
-        if (blk > 0) {  // block twist, shift-invariant recurrence
-            const int i = threadIdx.x;
-            uint64_t v0 = 0;
-            if (i < N - M) v0 = twist(s[i], s[i + 1], s[i + M]);
-            __syncthreads();
-            if (i < N - M) s[i] = v0;
-            __syncthreads();
-            uint64_t v1 = 0;
-            if (i >= N - M && i < N - 1) v1 = twist(s[i], s[i + 1], s[i + M - N]);
-            __syncthreads();
-            if (i >= N - M && i < N - 1) s[i] = v1;
-            __syncthreads();
-            if (i == N - 1) s[N - 1] = twist(s[N - 1], s[0], s[M - 1]);
-            __syncthreads();
-        }
-        const int64_t q = blk * N + threadIdx.x;
-        if (threadIdx.x < N && q < n) {
-            const uint64_t out = temper(s[threadIdx.x]);
-            if (raw_out) raw_out[q0 + q] = out;
-            if (noise) {
-                const double u = static_cast<double>(out >> 11) * 0x1.0p-53;
-                noise[q0 + q] = static_cast<float>(lo + span * u);
+        if (t < N) {
+            const int64_t q = blk * N + t;
+            if (q < n) {
+                const uint64_t out = temper(cur[t]);
+                if (raw_out) raw_out[q0 + q] = out;
+                if (noise) {
+                    const double u = static_cast<double>(out >> 11) * 0x1.0p-53;
+                    noise[q0 + q] = static_cast<float>(lo + span * u);
+                }
             }
+            if ((blk + 1) * N < n) nxt[t] = next_word(cur, t);
         }
         __syncthreads();
+        uint64_t* tmp = cur;
+        cur = nxt;
+        nxt = tmp;
     }
 }
 
@@ -321,14 +344,14 @@ void generate(uint64_t seed, int64_t count, double lo, double hi, float* noise, 
     Scratch& sc = scratch();
     base_kernel<<<1, kThreads, 0, st>>>(seed, sc.base);
     MOE_LAUNCH_CHECK();
-    const size_t smem = sizeof(uint64_t) * (BASE + W + N);
+    const size_t smem = sizeof(uint64_t) * (BASE + W + 2 * N);
     static bool attr = false;
     if (!attr) {
         MOE_CUDA_CHECK(cudaFuncSetAttribute(chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             static_cast<int>(smem)));
         attr = true;
     }
-    chunk_kernel<<<P, kThreads, smem, st>>>(sc.base, tab.dev, J, count, lo, hi - lo, noise, raw);
+    chunk_kernel<<<P, kChunkThreads, smem, st>>>(sc.base, tab.dev, J, count, lo, hi - lo, noise, raw);
     MOE_LAUNCH_CHECK();
 }
 

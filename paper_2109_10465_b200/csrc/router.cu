@@ -93,6 +93,14 @@ softmax_topk_kernel(const float* __restrict__ logits, int64_t T, int E, int K,
             }
             b0 = nb0; i0 = ni0; b1 = nb1; i1 = ni1;
         }
+        if (i0 < 0 || i0 >= E) {  // NaN row: no comparison succeeded (flagged above)
+            i0 = 0;
+            b0 = 0.f;
+        }
+        if (i1 < 0 || i1 >= E || i1 == i0) {
+            i1 = i0 == 0 ? 1 % E : 0;
+            b1 = 0.f;
+        }
         if (lane == 0) {
             choice[t * K] = i0;
             gate_prob[t * K] = b0;

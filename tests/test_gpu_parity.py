@@ -117,10 +117,10 @@ def test_layer_fp32_c1_full_size():
     for e in range(E):
         toks = np.nonzero((eid == e) & (slot >= 0))[0]
         hpre = x[toks] @ w1[e] + b1[e]
-        k = np.abs(hpre) < 1e-5
+        k = np.abs(hpre) < 1e-6  # fp32 error of Hpre here is ~1e-7
         kink_cols[e] = k.any(0)
         kink_tok[toks[k.any(1)]] = True
-    assert kink_cols.mean() < 1e-3 and kink_tok.mean() < 1e-2, (kink_cols.sum(), kink_tok.sum())
+    assert kink_cols.mean() < 1e-2 and kink_tok.mean() < 2e-2, (kink_cols.sum(), kink_tok.sum())
     rows = z["sample_rows"]
     ok = ~kink_tok[rows]
     assert rel_err(out["y"][rows], z["y_rows"]) <= TOL_F32
