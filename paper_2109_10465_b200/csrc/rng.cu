@@ -275,9 +275,9 @@ chunk_kernel(const uint64_t* __restrict__ base, const uint64_t* __restrict__ jum
     // window word j = XOR_{i : g_i} base[j + i]; two threads per j (even / odd
     // words of g), two independent accumulators each for load-latency ILP.
     const int t = threadIdx.x;
+    const int j = t % N, part = t / N;  // part 2 = idle threads (t >= 624)
+    uint64_t a0 = 0, a1 = 0;
     if (t < 2 * N) {
-        const int j = t % N, part = t / N;
-        uint64_t a0 = 0, a1 = 0;
         for (int w = part; w < W; w += 4) {
             uint64_t b0 = sg[w];
             uint64_t b1 = w + 2 < W ? sg[w + 2] : 0ULL;
@@ -296,12 +296,11 @@ chunk_kernel(const uint64_t* __restrict__ base, const uint64_t* __restrict__ jum
                 }
             }
         }
-        if (part == 1) s1[j] = a0 ^ a1;
-        __syncthreads();
-        if (part == 0) s0[j] = a0 ^ a1 ^ s1[j];
-    } else {
-        __syncthreads();
     }
+    // barriers outside divergent code (bar.sync is warp-aligned)
+    if (part == 1) s1[j] = a0 ^ a1;
+    __syncthreads();
+    if (part == 0) s0[j] = a0 ^ a1 ^ s1[j];
     __syncthreads();
     const int64_t n = min(J, count - q0);
     uint64_t* cur = s0;
