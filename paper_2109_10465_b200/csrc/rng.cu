@@ -34,7 +34,10 @@ namespace mt {
 constexpr int N = 312, M = 156, DEG = 19937;
 constexpr uint64_t A = 0xB5026F5AA96619E9ULL, UM = 0xFFFFFFFF80000000ULL, LM = 0x7FFFFFFFULL;
 constexpr int W = (DEG + 63) / 64 + 1;  // words of a polynomial of degree < DEG (+1 spare)
-constexpr int BASE = DEG + N;           // base words needed: x[1 .. DEG + N]
+constexpr int kJumpR = 10;              // window words per lane in the jump
+// base words x[1 .. BASE]: DEG + N are needed by the jump; the sliding
+// window of the last lane reads up to 32*kJumpR + 2*kJumpR words past DEG.
+constexpr int BASE = DEG + 32 * kJumpR + 2 * kJumpR + 8;
 constexpr int kThreads = 320;
 
 __host__ __device__ __forceinline__ uint64_t temper(uint64_t z) {
@@ -272,35 +275,42 @@ chunk_kernel(const uint64_t* __restrict__ base, const uint64_t* __restrict__ jum
     for (int i = threadIdx.x; i < BASE; i += blockDim.x) sb[i] = base[i];
     for (int i = threadIdx.x; i < W; i += blockDim.x) sg[i] = jump[static_cast<int64_t>(c) * W + i];
     __syncthreads();
-    // window word j = XOR_{i : g_i} base[j + i]; two threads per j (even / odd
-    // words of g), two independent accumulators each for load-latency ILP.
+    // window word j = XOR_{i : g_i} base[j + i].  Warp w takes bit range
+    // [w*L, (w+1)*L) of g; lane l owns R consecutive words j = l*R + r in
+    // registers and slides a register window over base, so each bit costs one
+    // shared load plus R predicated XORs (g's bit is warp-uniform: no
+    // divergence).  Partial windows meet in shared memory via atomic XOR.
     const int t = threadIdx.x;
-    const int j = t % N, part = t / N;  // part 2 = idle threads (t >= 624)
-    uint64_t a0 = 0, a1 = 0;
-    if (t < 2 * N) {
-        for (int w = part; w < W; w += 4) {
-            uint64_t b0 = sg[w];
-            uint64_t b1 = w + 2 < W ? sg[w + 2] : 0ULL;
-            const uint64_t* p0 = sb + j + w * 64;
-            const uint64_t* p1 = p0 + 128;
-            while (b0 | b1) {
-                if (b0) {
-                    const int b = __ffsll(static_cast<long long>(b0)) - 1;
-                    b0 &= b0 - 1;
-                    a0 ^= p0[b];
+    const int warp = t >> 5, lane = t & 31;
+    for (int i = t; i < N; i += blockDim.x) s0[i] = 0;
+    __syncthreads();
+    {
+        constexpr int R = kJumpR;
+        const int nwarps = blockDim.x >> 5;
+        const int L = (DEG + nwarps - 1) / nwarps;
+        const int i0 = warp * L, i1 = min(DEG, i0 + L);
+        const int j0 = lane * R;
+        uint64_t acc[R], win[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            acc[r] = 0;
+            win[r] = sb[i0 + j0 + r];
+        }
+        for (int i = i0; i < i1; i += R) {
+#pragma unroll
+            for (int s = 0; s < R; ++s) {
+                const int ii = i + s;
+                if (ii < i1 && ((sg[ii >> 6] >> (ii & 63)) & 1ULL)) {
+#pragma unroll
+                    for (int r = 0; r < R; ++r) acc[r] ^= win[(s + r) % R];
                 }
-                if (b1) {
-                    const int b = __ffsll(static_cast<long long>(b1)) - 1;
-                    b1 &= b1 - 1;
-                    a1 ^= p1[b];
-                }
+                win[s] = sb[i + j0 + R + s];
             }
         }
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+            if (j0 + r < N) atomicXor(reinterpret_cast<unsigned long long*>(&s0[j0 + r]), acc[r]);
     }
-    // barriers outside divergent code (bar.sync is warp-aligned)
-    if (part == 1) s1[j] = a0 ^ a1;
-    __syncthreads();
-    if (part == 0) s0[j] = a0 ^ a1 ^ s1[j];
     __syncthreads();
     const int64_t n = min(J, count - q0);
     uint64_t* cur = s0;
