@@ -1,0 +1,96 @@
+"""Multi-GPU expert-parallel parity check (run under torchrun, one rank per GPU).
+
+Contract (parallel.hpp:100-109, test_parallel.cpp:194-265): rank r gates its own
+tokens with seed derive_seed(seed, r); its output equals the single-rank layer
+on x_r with that seed.  The reference's EP step is forward-only; the backward
+is pinned by composition: dx_r is rank-local, dWg is the sum over ranks, and an
+owned expert's grads are the sum over origin ranks of the single-rank grads.
+
+  torchrun --nproc-per-node N tests/ep_check.py [fp32|bf16]
+Prints 'EP_OK <max errors>' on rank 0 and exits non-zero on mismatch.
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle as O  # noqa: E402
+import paper_2109_10465_b200 as M  # noqa: E402
+from oracle.margin import margin_guard  # noqa: E402
+
+
+def main():
+    mode = sys.argv[1] if len(sys.argv) > 1 else "fp32"
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+    dev = torch.device("cuda")
+    dist.init_process_group("nccl", device_id=dev)
+    E, El = 4 * world, 4
+    T, d, f = 256, 256, 512
+    seed = 77
+    dt = torch.float32 if mode == "fp32" else torch.bfloat16
+    o = O.restatement()
+    x_all, gw, w1, b1, w2, b2, dy_all = O.layer_inputs(T * world, d, f, E, seed=5)
+    cfg_o = O.make_cfg(num_experts=E, capacity_factor_train=1.0)
+    rnd = (lambda a: a.astype(np.float32).astype(np.float64)) if mode == "fp32" else \
+        (lambda a: torch.from_numpy(np.asarray(a, np.float32)).to(torch.bfloat16).float().numpy().astype(np.float64))
+    xs, dys = [], []
+    for r in range(world):
+        xr = rnd(x_all[r * T:(r + 1) * T])
+        xr = margin_guard(xr, gw, cfg_o, O.TRAIN, o.derive_seed(seed, r), round_fn=rnd)
+        xs.append(xr)
+        dys.append(rnd(dy_all[r * T:(r + 1) * T]))
+    w1r, w2r = rnd(w1), rnd(w2)
+    gwr, b1r, b2r = [a.astype(np.float32).astype(np.float64) for a in (gw, b1, b2)]
+    refs = [o.moe_layer(xs[r], gwr, w1r, b1r, w2r, b2r, cfg_o, O.TRAIN, o.derive_seed(seed, r),
+                        dy=dys[r], daux=1.0) for r in range(world)]
+
+    to = lambda a, t=torch.float32: torch.from_numpy(np.ascontiguousarray(a)).to(dev, t)  # noqa
+    lo, hi = rank * El, (rank + 1) * El
+    params = M.MoeLayerParams(to(gwr), to(w1r[lo:hi], dt), to(b1r[lo:hi]), to(w2r[lo:hi], dt),
+                              to(b2r[lo:hi]))
+    layer = M.MoeLayer(M.RouterConfig(num_experts=E), T, d, f, dt, ep_size=world, ep_rank=rank)
+    uid = [M.ep_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    layer.ep_init(uid[0])
+    y, aux, dec = layer.forward(to(xs[rank], dt), params, M.Phase.TRAIN, M.derive_seed(seed, rank))
+    g = layer.backward(to(dys[rank], dt), 1.0)
+    torch.cuda.synchronize()
+
+    def rel(a, b):  # element-wise, max(1,|ref|) normalisation
+        a = a.float().cpu().numpy().astype(np.float64)
+        return float(np.max(np.abs(a - b) / np.maximum(1.0, np.abs(b))))
+
+    def reln(a, b):  # norm-wise for token-reduced gradients
+        a = a.float().cpu().numpy().astype(np.float64)
+        return float(np.max(np.abs(a - b)) / max(1.0, float(np.max(np.abs(b)))))
+
+    ref = refs[rank]
+    ok = np.array_equal(dec.expert_id.cpu().numpy(), ref.expert_id) and \
+        np.array_equal(dec.slot.cpu().numpy(), ref.slot)
+    dwg = sum(rr.dgate_w for rr in refs)
+    dw1 = sum(rr.dw1 for rr in refs)[lo:hi]
+    dw2 = sum(rr.dw2 for rr in refs)[lo:hi]
+    db1 = sum(rr.db1 for rr in refs)[lo:hi]
+    db2 = sum(rr.db2 for rr in refs)[lo:hi]
+    errs = dict(y=rel(y, ref.y), dx=rel(g["dx"], ref.dx), aux=abs(aux.item() - ref.aux),
+                dgate_w=reln(g["dgate_w"], dwg), dw1=reln(g["dw1"], dw1), dw2=reln(g["dw2"], dw2),
+                db1=reln(g["db1"], db1), db2=reln(g["db2"], db2))
+    tol = 1e-5 if mode == "fp32" else 2e-2
+    bad = torch.tensor([0 if ok and all(v <= tol for v in errs.values()) else 1], device=dev)
+    dist.all_reduce(bad)
+    print(f"rank {rank} decisions_ok={ok} errs={ {k: f'{v:.2e}' for k, v in errs.items()} }",
+          flush=True)
+    if rank == 0:
+        print("EP_OK" if bad.item() == 0 else "EP_FAIL", world, mode, flush=True)
+    dist.destroy_process_group()
+    sys.exit(0 if bad.item() == 0 else 1)
+
+
+if __name__ == "__main__":
+    main()
