@@ -27,8 +27,9 @@ from oracle.margin import margin_guard  # noqa: E402
 def main():
     mode = sys.argv[1] if len(sys.argv) > 1 else "fp32"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
-    dev = torch.device("cuda")
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
     E, El = 4 * world, 4
     T, d, f = 256, 256, 512
