@@ -50,6 +50,10 @@ def peaks():
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
+    """nvidia-smi sampled every 50 ms from before warm-up to after the timed
+    loops; samples are tagged with host time so the timed window can be cut
+    out (falls back to the whole busy period if the window is shorter than
+    the sampling interval)."""
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -57,11 +61,12 @@ class ClockSampler:
     def __init__(self):
         self.rows = []
         self.proc = None
+        self.windows = []
 
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -70,29 +75,34 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
+            self.rows.append((time.time(), [c.strip() for c in line.split(",")]))
+
+    def mark(self, t0, t1):
+        self.windows.append((t0, t1))
 
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        time.sleep(0.12)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        rows = [r for r in self.rows if len(r[1]) >= 9 and r[1][1].replace(".", "").isdigit()]
+        inside = [r for r in rows if any(a - 0.06 <= r[0] <= b + 0.06 for a, b in self.windows)]
+        use = inside if len(inside) >= 2 else rows
+        sm = sorted(float(r[1][1]) for r in use)
+        mx = [float(r[1][2]) for r in use]
         reasons = set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
-            if len(r) < 9:
-                continue
+        for _, r in use:
             for i, n in enumerate(names):
                 if r[5 + i].lower() == "active":
                     reasons.add(n)
-        sm.sort()
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(use),
+                "window": "timed region" if use is inside else "whole run (timed region shorter than sampling)"}
 
 
 # ---------------------------------------------------------------- CPU reference
@@ -203,6 +213,7 @@ def stage_model(stage, T, d, f, El, n_rows, n_tok):
 
 
 def run_ours(args):
+    os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep NCCL's banner off stdout
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -266,15 +277,16 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    clocks = ClockSampler()
+    if rank == 0:
+        clocks.start()
     for _ in range(max(args.warmup, 3)):
         step()
     layer.handle.check()  # surfaces any latched non-finite / range flag from warm-up
     barrier()
     # ---- device-timed region (inputs resident in HBM)
-    clocks = ClockSampler()
-    if rank == 0:
-        clocks.start()
     layer.handle.profile(True)
+    w0 = time.time()
     launches0 = M.routing.kernel_launch_count()
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -285,7 +297,7 @@ def run_ours(args):
     e1.record(st)
     barrier()
     launches = M.routing.kernel_launch_count() - launches0
-    clk = clocks.stop() if rank == 0 else None
+    clocks.mark(w0, time.time())
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     stages = layer.handle.profile_read()
     layer.handle.profile(False)
@@ -336,12 +348,15 @@ def run_ours(args):
         e2e_step(i)
     torch.cuda.synchronize()
     barrier()
+    w0 = time.time()
     e0.record(st)
     for i in range(args.steps):
         e2e_step(i)
     e1.record(s_out)
     torch.cuda.synchronize()
     barrier()
+    clocks.mark(w0, time.time())
+    clk = clocks.stop() if rank == 0 else None
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     assert torch.equal(dx_h[(args.steps - 1) % 2].view(torch.int16), gb[(args.steps - 1) % 2]["dx"].cpu().view(torch.int16))
     e2e_value = N * T / (e2e_ms / 1e3)
