@@ -47,17 +47,20 @@ __device__ __forceinline__ void load8f(const float* p, float (&v)[8]) {
 template <class TX>
 __global__ void __launch_bounds__(NT)
 logits_kernel(const TX* __restrict__ x, const float* __restrict__ noise,
-              const float* __restrict__ wg, float* __restrict__ logits, int64_t T, int d, int E) {
+              const float* __restrict__ wg, float* __restrict__ logits, int64_t T, int d, int E,
+              int k_per_split) {
     __shared__ __align__(16) float Xs[BK][BT + 4];
     __shared__ __align__(16) float Ws[BK][BE + 4];
     const int tid = threadIdx.x;
     const int tx = tid % 16, ty = tid / 16;
     const int64_t t0 = (int64_t)blockIdx.x * BT;
     const int e0 = blockIdx.y * BE;
+    const int kb = blockIdx.z * k_per_split, ke = min(d, kb + k_per_split);
+    logits += (int64_t)blockIdx.z * T * E;  // split-K partials, summed in fixed order by softmax
     float acc[4][4] = {};
     // staging roles: x: 64 rows x 4 groups of 8 k; W: 32 rows x 16 float4
     const int xr = tid / 4, xq = tid % 4;
-    for (int k0 = 0; k0 < d; k0 += BK) {
+    for (int k0 = kb; k0 < ke; k0 += BK) {
         {
             float v[8];
             const int64_t t = t0 + xr;
@@ -278,11 +281,18 @@ dw_kernel(const TX* __restrict__ x, const float* __restrict__ noise,
 
 bool gate_fast_ok(int d, int E) { return d % 64 == 0 && E % 4 == 0 && E <= gate::MAXE; }
 
+int gate_logit_splits(int64_t T, int d, int E) {
+    const int64_t ctas = ceil_div(T, gate::BT) * ceil_div(E, gate::BE);
+    int s = 1;
+    while (s < kMaxGateSplits && ctas * s < 2 * kNumSMs && (d / (2 * s)) % gate::BK == 0) s *= 2;
+    return s;
+}
+
 template <class TX>
 void launch_gate_logits(const TX* x, const float* noise, const float* wg, float* logits,
-                        int64_t T, int d, int E, cudaStream_t st) {
-    dim3 grid((unsigned)ceil_div(T, gate::BT), (unsigned)ceil_div(E, gate::BE));
-    gate::logits_kernel<TX><<<grid, gate::NT, 0, st>>>(x, noise, wg, logits, T, d, E);
+                        int64_t T, int d, int E, int splits, cudaStream_t st) {
+    dim3 grid((unsigned)ceil_div(T, gate::BT), (unsigned)ceil_div(E, gate::BE), (unsigned)splits);
+    gate::logits_kernel<TX><<<grid, gate::NT, 0, st>>>(x, noise, wg, logits, T, d, E, d / splits);
     MOE_LAUNCH_CHECK();
 }
 
@@ -307,7 +317,7 @@ void launch_gate_dw(const TX* x, const float* noise, const float* dL, float* par
 
 #define INST(T)                                                                                  \
     template void launch_gate_logits<T>(const T*, const float*, const float*, float*, int64_t,  \
-                                        int, int, cudaStream_t);                                 \
+                                        int, int, int, cudaStream_t);                            \
     template void launch_gate_dx<T>(int64_t, int, int, int, int, const float*, const float*,     \
                                     const float*, const T*, const int32_t*, const int32_t*,      \
                                     const T*, bool, T*, T*, cudaStream_t);                       \

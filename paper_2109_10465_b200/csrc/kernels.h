@@ -17,9 +17,13 @@ constexpr float kProbRowTol = 1e-4f;
 
 // ---- router.cu ------------------------------------------------------------
 int softmax_parts(int64_t T);
-void launch_softmax_topk(const float* logits, int64_t T, int E, int K, float* probs,
+// logits may be `nsplit` split-K partial arrays [nsplit][T][E], summed in
+// fixed order before the softmax.
+void launch_softmax_topk(const float* logits, int nsplit, int64_t T, int E, int K, float* probs,
                          int32_t* choice, float* gate_prob, float* colsum_part,
                          int32_t* count_part, uint32_t* flags, cudaStream_t st);
+constexpr int kMaxGateSplits = 8;
+int gate_logit_splits(int64_t T, int d, int E);
 void launch_balance_finalize(const float* colsum_part, const int32_t* count_part, int nparts,
                              int64_t T, int E, double alpha, float* aux, float* fcoef,
                              int32_t* counts, cudaStream_t st);
@@ -154,7 +158,7 @@ namespace moe {
 bool gate_fast_ok(int d, int E);
 template <class TX>
 void launch_gate_logits(const TX* x, const float* noise, const float* wg, float* logits,
-                        int64_t T, int d, int E, cudaStream_t st);
+                        int64_t T, int d, int E, int splits, cudaStream_t st);
 template <class TIO>
 void launch_gate_dx(int64_t T, int d, int E, int K, int cap_pad, const float* dL, const float* wg,
                     const float* noise, const TIO* dX, const int32_t* choice, const int32_t* pos,

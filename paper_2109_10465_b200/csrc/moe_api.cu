@@ -139,6 +139,16 @@ struct moe_handle {
     int cap_pad_max = 0;
     size_t esz = 4;  // activation element size
     ncclComm_t comm = nullptr;
+    // side stream for backward work independent of the expert GEMMs, and a
+    // comm stream for the dX all-to-all (owned by the handle)
+    cudaStream_t side = nullptr, comm_stream = nullptr;
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr, ev_side = nullptr, ev_comm = nullptr;
+    ~moe_handle() {
+        for (cudaEvent_t e : {ev_a, ev_b, ev_c, ev_side, ev_comm})
+            if (e) cudaEventDestroy(e);
+        if (side) cudaStreamDestroy(side);
+        if (comm_stream) cudaStreamDestroy(comm_stream);
+    }
 
     // workspace
     DevMem logits, probs, choice, gate_prob, wts, slot, pos, row_src, kept, counts_r;
@@ -267,14 +277,17 @@ void route(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, int phas
         h->mark("jitter_noise");
     }
     // logits = (x * noise) @ gate_w  (routing.cpp:71)
-    if (gate_fast_ok(static_cast<int>(h->d), E))
+    int nsplit = 1;
+    if (gate_fast_ok(static_cast<int>(h->d), E)) {
+        nsplit = gate_logit_splits(T, static_cast<int>(h->d), E);
         launch_gate_logits<TIO>(x, jitter ? h->noise.as<float>() : nullptr, gate_w,
-                                h->logits.as<float>(), T, static_cast<int>(h->d), E, st);
-    else
+                                h->logits.as<float>(), T, static_cast<int>(h->d), E, nsplit, st);
+    } else {
         launch_gemm_dense<TIO>(x, h->d, 1, jitter ? h->noise.as<float>() : nullptr, gate_w, E, 1,
                                h->logits.as<float>(), T, E, h->d, 1, st);
+    }
     h->mark("gate_logits");
-    launch_softmax_topk(h->logits.as<float>(), T, E, K, h->probs.as<float>(),
+    launch_softmax_topk(h->logits.as<float>(), nsplit, T, E, K, h->probs.as<float>(),
                         h->choice.as<int32_t>(), h->gate_prob.as<float>(),
                         h->colsum_part.as<float>(), h->count_part.as<int32_t>(),
                         h->flags.as<uint32_t>(), st);
@@ -418,41 +431,55 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
         counts = h->counts_r.as<int32_t>();
         h->mark("a2a_dO");
     }
-    // expert backward: dH = (dO W2^T) * [H > 0]; dW2 = H^T dO; dX = dH W1^T; dW1 = X^T dH
-    row_gemm<TIO>(h, h->dOr.as<TIO>(), w2, h->dH.as<TIO>(), nullptr, h->H.as<TIO>(), counts, f, d,
-                  false, EPI_RELU_MASK, ep);
-    h->mark("ffn2_dgrad");
-    wgrad_gemm<TIO>(h, h->H.as<TIO>(), h->dOr.as<TIO>(), dw2, f, d, counts, ep);
-    h->mark("ffn2_wgrad");
-    launch_colsum_groups<TIO>(h->dOr.as<TIO>(), d, ep, El, h->cap_pad, counts, db2, st);
-    h->mark("db2");
-    row_gemm<TIO>(h, h->dH.as<TIO>(), w1, h->dXr.as<TIO>(), nullptr, nullptr, counts, d, f, false,
-                  EPI_NONE, ep);
-    h->mark("ffn1_dgrad");
-    wgrad_gemm<TIO>(h, h->Xr.as<TIO>(), h->dH.as<TIO>(), dw1, d, f, counts, ep);
-    h->mark("ffn1_wgrad");
-    launch_colsum_groups<TIO>(h->dH.as<TIO>(), f, ep, El, h->cap_pad, counts, db1, st);
-    h->mark("db1");
-    TIO* dXloc = h->dXr.as<TIO>();
-    if (ep > 1) {
-        all_to_all(h, h->dXr.p, h->dXloc.p, static_cast<size_t>(El) * h->cap_pad * d,
-                   nccl_type(h->esz), h->esz);
-        dXloc = h->dXloc.as<TIO>();
-        h->mark("a2a_dX");
-    }
-    // gate backward: dxg = dL Wg^T; dWg = (x*noise)^T dL (split-K, fixed order)
+    // Side stream: work that only needs dL / dO / dH runs next to the expert
+    // GEMMs (those are HBM- or tensor-bound persistent kernels that leave
+    // shared memory and registers for these FMA/HBM-light kernels):
+    //   dWg = (x*noise)^T dL (split-K, fixed order), db2 = colsum(dO), db1 = colsum(dH)
     const float* noise = h->jitter_on ? h->noise.as<float>() : nullptr;
     const bool fast = gate_fast_ok(static_cast<int>(d), E);
     const int splits = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(1, T / 512)));
+    cudaStream_t side = h->side;
+    MOE_CUDA_CHECK(cudaEventRecord(h->ev_a, st));
+    MOE_CUDA_CHECK(cudaStreamWaitEvent(side, h->ev_a, 0));
     if (fast) {
         launch_gate_dw<TIO>(x, noise, h->dL.as<float>(), h->dwg_part.as<float>(), T,
-                            static_cast<int>(d), E, splits, st);
+                            static_cast<int>(d), E, splits, side);
     } else {
         launch_gemm_dense<TIO>(x, 1, d, noise, h->dL.as<float>(), E, 1, h->dwg_part.as<float>(), d,
-                               E, T, splits, st);
+                               E, T, splits, side);
     }
-    launch_splitk_reduce(h->dwg_part.as<float>(), splits, d * E, dgate_w, st);
-    h->mark("gate_wgrad");
+    launch_splitk_reduce(h->dwg_part.as<float>(), splits, d * E, dgate_w, side);
+    launch_colsum_groups<TIO>(h->dOr.as<TIO>(), d, ep, El, h->cap_pad, counts, db2, side);
+    // expert backward: dH = (dO W2^T) * [H > 0]; dX = dH W1^T; dW2 = H^T dO; dW1 = X^T dH
+    row_gemm<TIO>(h, h->dOr.as<TIO>(), w2, h->dH.as<TIO>(), nullptr, h->H.as<TIO>(), counts, f, d,
+                  false, EPI_RELU_MASK, ep);
+    h->mark("ffn2_dgrad");
+    MOE_CUDA_CHECK(cudaEventRecord(h->ev_b, st));
+    MOE_CUDA_CHECK(cudaStreamWaitEvent(side, h->ev_b, 0));
+    launch_colsum_groups<TIO>(h->dH.as<TIO>(), f, ep, El, h->cap_pad, counts, db1, side);
+    MOE_CUDA_CHECK(cudaEventRecord(h->ev_side, side));
+    row_gemm<TIO>(h, h->dH.as<TIO>(), w1, h->dXr.as<TIO>(), nullptr, nullptr, counts, d, f, false,
+                  EPI_NONE, ep);
+    h->mark("ffn1_dgrad");
+    TIO* dXloc = h->dXr.as<TIO>();
+    if (ep > 1) {  // return dX to its origin ranks while the weight gradients compute
+        MOE_CUDA_CHECK(cudaEventRecord(h->ev_c, st));
+        MOE_CUDA_CHECK(cudaStreamWaitEvent(h->comm_stream, h->ev_c, 0));
+        cudaStream_t saved = h->stream;
+        h->stream = h->comm_stream;
+        all_to_all(h, h->dXr.p, h->dXloc.p, static_cast<size_t>(El) * h->cap_pad * d,
+                   nccl_type(h->esz), h->esz);
+        h->stream = saved;
+        MOE_CUDA_CHECK(cudaEventRecord(h->ev_comm, h->comm_stream));
+        dXloc = h->dXloc.as<TIO>();
+    }
+    wgrad_gemm<TIO>(h, h->H.as<TIO>(), h->dOr.as<TIO>(), dw2, f, d, counts, ep);
+    h->mark("ffn2_wgrad");
+    wgrad_gemm<TIO>(h, h->Xr.as<TIO>(), h->dH.as<TIO>(), dw1, d, f, counts, ep);
+    h->mark("ffn1_wgrad");
+    MOE_CUDA_CHECK(cudaStreamWaitEvent(st, h->ev_side, 0));
+    if (ep > 1) MOE_CUDA_CHECK(cudaStreamWaitEvent(st, h->ev_comm, 0));
+    h->mark("bwd_join");
     if (ep > 1) {
         NCCL_CHECK(ncclAllReduce(dgate_w, dgate_w, static_cast<size_t>(d * E), ncclFloat32, ncclSum,
                                  h->comm, st));
@@ -483,7 +510,7 @@ void alloc_workspace(moe_handle* h) {
     h->cap_pad_max = static_cast<int>(round_up(capmax, kRowAlign));
     const int64_t R = static_cast<int64_t>(E) * h->cap_pad_max;
     const size_t es = h->esz;
-    h->logits.alloc(4 * T * E);
+    h->logits.alloc(4 * T * E * kMaxGateSplits);  // split-K partials
     h->probs.alloc(4 * T * E);
     h->choice.alloc(4 * T * K);
     h->gate_prob.alloc(4 * T * K);
@@ -601,6 +628,10 @@ moe_status moe_create(const moe_router_cfg* cfg, const moe_layer_dims* dims, moe
         h->f = dims->d_ff;
         h->esz = dims->dtype == MOE_BF16 ? 2 : 4;
         alloc_workspace(h.get());
+        MOE_CUDA_CHECK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+        MOE_CUDA_CHECK(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
+        for (cudaEvent_t* e : {&h->ev_a, &h->ev_b, &h->ev_c, &h->ev_side, &h->ev_comm})
+            MOE_CUDA_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     });
     if (s == MOE_OK) *out = h.release();
     return s;
@@ -751,7 +782,7 @@ moe_status moe_gate(moe_handle* h, int64_t T, const void* x, const float* gate_w
         else
             launch_gemm_dense<float>(static_cast<const float*>(x), h->d, 1, nz, gate_w, E, 1,
                                      h->logits.as<float>(), T, E, h->d, 1, st);
-        launch_softmax_topk(h->logits.as<float>(), T, E, K, probs, choice, gate_prob,
+        launch_softmax_topk(h->logits.as<float>(), 1, T, E, K, probs, choice, gate_prob,
                             h->colsum_part.as<float>(), h->count_part.as<int32_t>(),
                             h->flags.as<uint32_t>(), st);
     });

@@ -25,10 +25,11 @@ namespace moe {
 constexpr int kSoftmaxWarps = 8;
 
 __global__ void __launch_bounds__(kSoftmaxWarps * 32)
-softmax_topk_kernel(const float* __restrict__ logits, int64_t T, int E, int K,
+softmax_topk_kernel(const float* __restrict__ logits, int nsplit, int64_t T, int E, int K,
                     float* __restrict__ probs, int32_t* __restrict__ choice,
                     float* __restrict__ gate_prob, float* __restrict__ colsum_part,
                     int32_t* __restrict__ count_part, uint32_t* __restrict__ flags) {
+    const int64_t TE = T * E;
     extern __shared__ float sm[];
     float* s_col = sm;                                   // [warps][E]
     int32_t* s_cnt = reinterpret_cast<int32_t*>(sm + kSoftmaxWarps * E);  // [E]
@@ -40,25 +41,34 @@ softmax_topk_kernel(const float* __restrict__ logits, int64_t T, int E, int K,
     const int64_t rows_per_cta = (int64_t)kSoftmaxWarps * 8;
     const int64_t t0 = (int64_t)blockIdx.x * rows_per_cta;
     for (int64_t t = t0 + warp; t < min(T, t0 + rows_per_cta); t += kSoftmaxWarps) {
-        const float* L = logits + t * E;
+        const float* Lp = logits + t * E;
+        auto lg = [&](int e) {  // split-K partials summed in fixed order
+            float v = Lp[e];
+            for (int s = 1; s < nsplit; ++s) v += Lp[s * TE + e];
+            return v;
+        };
+        float L[8];  // E <= 256: at most 8 logits per lane
+        const int nl = (E + 31) / 32;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (q < nl && lane + 32 * q < E) L[q] = lg(lane + 32 * q);
         float mx = -INFINITY;
-        for (int e = lane; e < E; e += 32) mx = fmaxf(mx, L[e]);
+        for (int e = lane, q = 0; e < E; e += 32, ++q) mx = fmaxf(mx, L[q]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         float s = 0.f;
-        for (int e = lane; e < E; e += 32) s += expf(L[e] - mx);
+        for (int e = lane, q = 0; e < E; e += 32, ++q) s += expf(L[q] - mx);
         s = warp_sum(s);
-        const float inv = 1.0f / s;
         // best / second best over P with the reference's tie rules
         float b0 = -1.f, b1 = -1.f;
         int i0 = 0x7fffffff, i1 = 0x7fffffff;
         float psum = 0.f;
-        for (int e = lane; e < E; e += 32) {
-            const float p = expf(L[e] - mx) / s;
+        for (int e = lane, q = 0; e < E; e += 32, ++q) {
+            const float p = expf(L[q] - mx) / s;
             probs[t * E + e] = p;
             s_col[warp * E + e] += p;
             psum += p;
-            if (!finite_f(p) || !finite_f(L[e])) flag |= MOE_FLAG_NONFINITE_DEV;
+            if (!finite_f(p) || !finite_f(L[q])) flag |= MOE_FLAG_NONFINITE_DEV;
             // keep the two best (value desc, index asc) seen by this lane
             if (p > b0 || (p == b0 && e < i0)) {
                 b1 = b0; i1 = i0; b0 = p; i0 = e;
@@ -66,7 +76,6 @@ softmax_topk_kernel(const float* __restrict__ logits, int64_t T, int E, int K,
                 b1 = p; i1 = e;
             }
         }
-        (void)inv;
         psum = warp_sum(psum);
         // warp merge of (b0,i0,b1,i1)
 #pragma unroll
@@ -152,13 +161,14 @@ __global__ void balance_finalize_kernel(const float* __restrict__ colsum_part,
     if (threadIdx.x == 0) *aux = (float)s_acc[0];
 }
 
-void launch_softmax_topk(const float* logits, int64_t T, int E, int K, float* probs,
+void launch_softmax_topk(const float* logits, int nsplit, int64_t T, int E, int K, float* probs,
                          int32_t* choice, float* gate_prob, float* colsum_part,
                          int32_t* count_part, uint32_t* flags, cudaStream_t st) {
+    if (E > 256) throw Status(2, "gate: num_experts > 256 not supported on this path");
     const int nparts = softmax_parts(T);
     const size_t smem = sizeof(float) * kSoftmaxWarps * E + sizeof(int32_t) * E;
     softmax_topk_kernel<<<nparts, kSoftmaxWarps * 32, smem, st>>>(
-        logits, T, E, K, probs, choice, gate_prob, colsum_part, count_part, flags);
+        logits, nsplit, T, E, K, probs, choice, gate_prob, colsum_part, count_part, flags);
     MOE_LAUNCH_CHECK();
 }
 
