@@ -63,9 +63,10 @@ class ClockSampler:
         self.proc = None
         self.windows = []
 
-    def start(self):
+    def start(self, ngpus: int = 1):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}",
+            ids = ",".join(str(i) for i in range(ngpus))  # the GPUs this job runs on
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", ids, f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
@@ -279,7 +280,7 @@ def run_ours(args):
 
     clocks = ClockSampler()
     if rank == 0:
-        clocks.start()
+        clocks.start(N)
     for _ in range(max(args.warmup, 3)):
         step()
     layer.handle.check()  # surfaces any latched non-finite / range flag from warm-up
