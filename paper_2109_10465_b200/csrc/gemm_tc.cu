@@ -34,7 +34,10 @@ namespace moe {
 namespace tc {
 
 constexpr int BM = 128, BN = 256, BK = 64;
-constexpr int kStages = 3;
+// 4 x 48 KB stages keep ~3 stages (144 KB) in flight: enough to cover TMA
+// latency at the MMA's ~94 B/clk consumption (3 stages starved the MMA).
+constexpr int kStages = 4;
+constexpr int kEpiBufs = 1;  // epilogue staging buffers per warp
 constexpr int kThreads = 192;  // 6 warps
 constexpr uint32_t kTileABytes = BM * BK * 2;  // 16 KB
 constexpr uint32_t kTileBBytes = BN * BK * 2;  // 32 KB
@@ -42,7 +45,7 @@ constexpr uint32_t kStageBytes = kTileABytes + kTileBBytes;
 // epilogue staging: per epilogue warp, 2 buffers of 32 rows x 64 bf16 (128 B
 // rows, 128B-swizzled) drained by TMA bulk tensor stores
 constexpr uint32_t kStageCBytes = 32 * 64 * 2;  // 4 KB
-constexpr uint32_t kEpiBytes = 4 * 2 * kStageCBytes;
+constexpr uint32_t kEpiBytes = 4 * kEpiBufs * kStageCBytes;
 constexpr int kMaxSegs = 1024;
 constexpr int kMaxGroups = 256;
 constexpr size_t kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + kEpiBytes +
@@ -451,8 +454,13 @@ __global__ void __launch_bounds__(kThreads, 1) grouped_gemm_kernel(const __grid_
                 }
                 // stage the warp's 32 x 64 bf16 block (128B-swizzled rows) and
                 // hand it to the TMA engine; two buffers alternate per warp
-                uint8_t* sbuf = cstage + ((quarter * 2 + (cbuf & 1)) * kStageCBytes);
-                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                uint8_t* sbuf = cstage + ((quarter * kEpiBufs + (cbuf % kEpiBufs)) * kStageCBytes);
+                if (lane == 0) {
+                    if constexpr (kEpiBufs == 1)
+                        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    else
+                        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                }
                 __syncwarp();
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
