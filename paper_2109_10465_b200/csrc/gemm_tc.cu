@@ -34,24 +34,30 @@ namespace moe {
 namespace tc {
 
 constexpr int BM = 128, BN = 256, BK = 64;
-// 4 x 48 KB stages keep ~3 stages (144 KB) in flight: enough to cover TMA
-// latency at the MMA's ~94 B/clk consumption (3 stages starved the MMA).
-constexpr int kStages = 4;
-constexpr int kEpiBufs = 1;  // epilogue staging buffers per warp
 constexpr int kThreads = 192;  // 6 warps
 constexpr uint32_t kTileABytes = BM * BK * 2;  // 16 KB
 constexpr uint32_t kTileBBytes = BN * BK * 2;  // 32 KB
 constexpr uint32_t kStageBytes = kTileABytes + kTileBBytes;
-// epilogue staging: per epilogue warp, 2 buffers of 32 rows x 64 bf16 (128 B
+// epilogue staging: per epilogue warp, 1-2 buffers of 32 rows x 64 bf16 (128 B
 // rows, 128B-swizzled) drained by TMA bulk tensor stores
 constexpr uint32_t kStageCBytes = 32 * 64 * 2;  // 4 KB
-constexpr uint32_t kEpiBytes = 4 * kEpiBufs * kStageCBytes;
 constexpr int kMaxSegs = 1024;
 constexpr int kMaxGroups = 256;
-constexpr size_t kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + kEpiBytes +
-                              1024 /*barriers*/ + 4 * (kMaxSegs + 3 * kMaxGroups + 8);
 
 enum Kind { ROW = 0, WGRAD = 1 };
+
+// Pipeline shape per kind.  ROW (fwd/dgrad, K = d or f) is MMA/HBM-streaming:
+// 4 x 48 KB stages keep ~3 stages in flight, enough to cover TMA latency at
+// the MMA's ~94 B/clk consumption (3 stages starved the MMA).  WGRAD (K = the
+// expert's rows, ~128 on one GPU) is bound by its dW stores: 3 stages and a
+// double-buffered epilogue.
+template <int KIND> struct KCfg {
+    static constexpr int stages = KIND == ROW ? 4 : 3;
+    static constexpr int epi_bufs = KIND == ROW ? 1 : 2;
+    static constexpr uint32_t epi_bytes = 4 * epi_bufs * kStageCBytes;
+    static constexpr size_t smem = 1024 /*align slack*/ + stages * kStageBytes + epi_bytes +
+                                   1024 /*barriers*/ + 4 * (kMaxSegs + 3 * kMaxGroups + 8);
+};
 
 struct __align__(64) Params {
     CUtensorMap tmA;
@@ -205,6 +211,9 @@ __device__ __forceinline__ void row_tile(const Params& p, const Sched& s, int NT
 
 template <int KIND>
 __global__ void __launch_bounds__(kThreads, 1) grouped_gemm_kernel(const __grid_constant__ Params p) {
+    constexpr int kStages = KCfg<KIND>::stages;
+    constexpr int kEpiBufs = KCfg<KIND>::epi_bufs;
+    constexpr uint32_t kEpiBytes = KCfg<KIND>::epi_bytes;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* tiles = smem;
@@ -545,11 +554,11 @@ void launch(const Params& p, int64_t max_tiles, cudaStream_t st) {
     if (!attr) {
         MOE_CUDA_CHECK(cudaFuncSetAttribute(grouped_gemm_kernel<KIND>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            static_cast<int>(kSmemBytes)));
+                                            static_cast<int>(KCfg<KIND>::smem)));
         attr = true;
     }
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms(), max_tiles)));
-    grouped_gemm_kernel<KIND><<<grid, kThreads, kSmemBytes, st>>>(p);
+    grouped_gemm_kernel<KIND><<<grid, kThreads, KCfg<KIND>::smem, st>>>(p);
     MOE_LAUNCH_CHECK();
 }
 
