@@ -23,6 +23,7 @@
 //          (both operands MN-major; the K loop walks the group's segments).
 #include <cuda.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 
@@ -503,6 +504,396 @@ __global__ void __launch_bounds__(kThreads, 1) grouped_gemm_kernel(const __grid_
     }
 }
 
+// ===================================================================== 2-CTA
+// cta_group::2 variant for the compute-bound regime (experts with >= 2 row
+// tiles, i.e. expert parallelism or large T).  A CTA pair (cluster of 2) owns a
+// 256 x 256 output tile: each CTA stages its own 128 rows of A and HALF of B
+// (128 of the 256 columns), so a stage is 32 KB per CTA and 6 stages fit; the
+// leader issues tcgen05.mma.cta_group::2 (M=256, N=256) reading both CTAs'
+// shared memory and writing each CTA's TMEM half.  Both CTAs' TMA loads
+// complete on the leader's full barrier; MMA completion is multicast to both
+// CTAs' empty / tmem-full barriers; both epilogues arrive on the leader's
+// tmem-empty barrier.
+namespace pair {
+
+constexpr int kStages = 6;
+constexpr uint32_t kHalfB = 128 * BK * 2;             // 16 KB
+constexpr uint32_t kStage = kTileABytes + kHalfB;     // 32 KB
+constexpr uint32_t kEpi = 4 * kStageCBytes;           // one staging buffer per epilogue warp
+constexpr size_t kSmem = 1024 + kStages * kStage + kEpi + 1024 + 4 * (kMaxSegs + 3 * kMaxGroups + 8);
+
+__device__ __forceinline__ uint32_t cta_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.aligned;\nbarrier.cluster.wait.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t leader_addr(const void* p) {  // same offset in CTA 0
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(0));
+    return r;
+}
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_t leader_bar,
+                                                 void* dst, int32_t c0, int32_t c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void mma2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                     uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void commit2(uint64_t* bar) {  // arrive on bar in both CTAs
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(smem_u32(bar)),
+        "h"(static_cast<uint16_t>(3))
+        : "memory");
+}
+__device__ __forceinline__ void arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+__host__ __device__ constexpr uint32_t idesc2(uint32_t a_mn, uint32_t b_mn) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (a_mn << 15) | (b_mn << 16) | ((BN >> 3) << 17) |
+           ((256 >> 4) << 24);
+}
+
+// ROW: pair-tile t -> (group, n-tile, m-pair); this CTA takes m-tile 2*mp+rank
+// of the group's m-tile list (segment-major).  valid = that m-tile exists.
+__device__ __forceinline__ void row_pair_tile(const Params& p, const Sched& s, int NT, int t,
+                                              uint32_t rank, int& seg, int& mt, int& nt,
+                                              bool& valid) {
+    int le = 0;
+    while (le + 1 < p.El && s.grp_base[le + 1] <= t) ++le;
+    const int local = t - s.grp_base[le];
+    const int gmp = (s.grp_mt[le] + 1) / 2;
+    nt = local / gmp;
+    const int mp = local % gmp;
+    int want = 2 * mp + static_cast<int>(rank);
+    valid = want < s.grp_mt[le];
+    if (!valid) want = 2 * mp;  // stage the partner's rows; results are masked
+    for (int r = 0; r < p.ep; ++r) {
+        const int sg = r * p.El + le;
+        const int c = (s.seg_cnt[sg] + BM - 1) / BM;
+        if (want < c) {
+            seg = sg;
+            mt = want;
+            return;
+        }
+        want -= c;
+    }
+    seg = le;
+    mt = 0;
+    valid = false;
+}
+
+template <int KIND>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+gemm2_kernel(const __grid_constant__ Params p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* tiles = smem;
+    uint8_t* cstage = smem + kStages * kStage;
+    uint8_t* misc = cstage + kEpi;
+    uint64_t* full = reinterpret_cast<uint64_t*>(misc);
+    uint64_t* empty = full + kStages;
+    uint64_t* tfull = empty + kStages;   // [2]
+    uint64_t* tempty = tfull + 2;        // [2] (leader's are used)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    int32_t* seg_cnt = reinterpret_cast<int32_t*>(misc + 1024);
+    int32_t* grp_mt = seg_cnt + kMaxSegs;
+    int32_t* grp_base = grp_mt + kMaxGroups;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cta_rank();
+    const bool leader = rank == 0;
+    const int pair_id = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const int nseg = p.ep * p.El;
+
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < kStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 256);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        prefetch_tmap(&p.tmA);
+        prefetch_tmap(&p.tmB);
+        prefetch_tmap(&p.tmC);
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    for (int i = threadIdx.x; i < nseg; i += blockDim.x) seg_cnt[i] = p.counts[i];
+    __syncthreads();
+    Sched s{seg_cnt, grp_mt, grp_base, 0};
+    const int NT = static_cast<int>(p.N / BN);
+    int MTP = 0;
+    if (KIND == ROW) {
+        for (int g = threadIdx.x; g < p.El; g += blockDim.x) {
+            int m = 0;
+            for (int r = 0; r < p.ep; ++r) m += (seg_cnt[r * p.El + g] + BM - 1) / BM;
+            grp_mt[g] = m;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int acc = 0;
+            for (int g = 0; g < p.El; ++g) {
+                grp_base[g] = acc;
+                acc += ((grp_mt[g] + 1) / 2) * NT;
+            }
+            grp_base[p.El] = acc;
+        }
+        __syncthreads();
+        s.total = grp_base[p.El];
+    } else {
+        MTP = static_cast<int>(p.M / (2 * BM));
+        s.total = p.El * MTP * NT;
+    }
+    tc_fence_before();
+    cluster_sync();  // barriers of both CTAs initialised before any remote arrive
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ================= TMA producer (both CTAs) =================
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = pair_id; t < s.total; t += npairs) {
+                int nkb_total = 0;
+                int seg = 0, mt = 0, nt = 0, g = 0;
+                bool valid = true;
+                if (KIND == ROW) {
+                    row_pair_tile(p, s, NT, t, rank, seg, mt, nt, valid);
+                    nkb_total = static_cast<int>((p.K + BK - 1) / BK);
+                } else {
+                    g = t / (MTP * NT);
+                    const int rem = t % (MTP * NT);
+                    mt = 2 * (rem / NT) + static_cast<int>(rank);
+                    nt = rem % NT;
+                }
+                const int le = seg % p.El;
+                auto load_stage = [&](int32_t a_c0, int32_t a_c1, int32_t kcoord, int32_t rowk) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* sa = tiles + stage * kStage;
+                    uint8_t* sb = sa + kTileABytes;
+                    const uint32_t lbar = leader_addr(&full[stage]);
+                    if (leader) mbar_expect_tx(&full[stage], 2 * kStage);
+                    if (KIND == ROW) {
+                        tma_load_2d_pair(&p.tmA, lbar, sa, a_c0, a_c1);
+                        const int n_half = nt * BN + static_cast<int>(rank) * 128;
+                        if (p.b_mn) {
+#pragma unroll
+                            for (int j = 0; j < 2; ++j)
+                                tma_load_2d_pair(&p.tmB, lbar, sb + j * (64 * BK * 2), n_half + j * 64, kcoord);
+                        } else {
+                            tma_load_2d_pair(&p.tmB, lbar, sb, rowk, static_cast<int32_t>(le * p.N) + n_half);
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < BM / 64; ++j)
+                            tma_load_2d_pair(&p.tmA, lbar, sa + j * (64 * BK * 2), mt * BM + j * 64, a_c1);
+                        const int n_half = nt * BN + static_cast<int>(rank) * 128;
+#pragma unroll
+                        for (int j = 0; j < 2; ++j)
+                            tma_load_2d_pair(&p.tmB, lbar, sb + j * (64 * BK * 2), n_half + j * 64, a_c1);
+                    }
+                    if (++stage == kStages) { stage = 0; phase ^= 1; }
+                };
+                if (KIND == ROW) {
+                    const int32_t arow = seg * p.cap_pad + mt * BM;
+                    for (int kb = 0; kb < nkb_total; ++kb)
+                        load_stage(kb * BK, arow, static_cast<int32_t>(le * p.K) + kb * BK, kb * BK);
+                } else {
+                    for (int r = 0; r < p.ep; ++r) {
+                        const int sg = r * p.El + g;
+                        const int nkb = (seg_cnt[sg] + BK - 1) / BK;
+                        for (int kb = 0; kb < nkb; ++kb) load_stage(0, sg * p.cap_pad + kb * BK, 0, 0);
+                    }
+                }
+                (void)valid;
+            }
+        }
+    } else if (warp == 1) {
+        // ================= MMA issuer (leader only) =================
+        if (leader && lane == 0) {
+            const uint32_t a_mn = KIND == WGRAD ? 1u : 0u;
+            const uint32_t b_mn = KIND == WGRAD ? 1u : static_cast<uint32_t>(p.b_mn);
+            const uint32_t idesc = idesc2(a_mn, b_mn);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = pair_id; t < s.total; t += npairs) {
+                int nkb;
+                if (KIND == ROW) {
+                    nkb = static_cast<int>((p.K + BK - 1) / BK);
+                } else {
+                    const int g = t / (MTP * NT);
+                    nkb = 0;
+                    for (int r = 0; r < p.ep; ++r) nkb += (seg_cnt[r * p.El + g] + BK - 1) / BK;
+                }
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t tmem_d = tmem_base + acc * BN;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(tiles + stage * kStage);
+                    const uint32_t sb = sa + kTileABytes;
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k) {
+                        uint64_t ad, bd;
+                        if (a_mn) ad = sdesc(sa + k * 2048, 64 * BK * 2, 1024);
+                        else      ad = sdesc(sa + k * 32, 16, 1024);
+                        if (b_mn) bd = sdesc(sb + k * 2048, 64 * BK * 2, 1024);
+                        else      bd = sdesc(sb + k * 32, 16, 1024);
+                        mma2(tmem_d, ad, bd, idesc, (kb | k) ? 1u : 0u);
+                    }
+                    commit2(&empty[stage]);
+                    if (++stage == kStages) { stage = 0; phase ^= 1; }
+                }
+                commit2(&tfull[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else {
+        // ================= epilogue (warps 2..5, both CTAs) =================
+        const int quarter = warp & 3;
+        const int row_in_tile = quarter * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = pair_id; t < s.total; t += npairs) {
+            int64_t crow, ncol0;
+            bool valid;
+            bool have_acc = true;
+            int le = 0;
+            if (KIND == ROW) {
+                int seg, mt, nt;
+                bool tvalid;
+                row_pair_tile(p, s, NT, t, rank, seg, mt, nt, tvalid);
+                le = seg % p.El;
+                const int m = mt * BM + row_in_tile;
+                valid = tvalid && m < seg_cnt[seg];
+                crow = static_cast<int64_t>(seg) * p.cap_pad + m;
+                ncol0 = static_cast<int64_t>(nt) * BN;
+                if (!tvalid) crow = -1;  // nothing of this CTA's half is stored
+            } else {
+                const int g = t / (MTP * NT);
+                const int rem = t % (MTP * NT);
+                const int mt = 2 * (rem / NT) + static_cast<int>(rank), nt = rem % NT;
+                int nrows = 0;
+                for (int r = 0; r < p.ep; ++r) nrows += seg_cnt[r * p.El + g];
+                have_acc = nrows > 0;
+                valid = true;
+                crow = static_cast<int64_t>(g) * p.M + mt * BM + row_in_tile;
+                ncol0 = static_cast<int64_t>(nt) * BN;
+            }
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16);
+            const bool store = crow >= 0;
+            const int32_t box_row = static_cast<int32_t>(crow - lane);
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 64) {
+                float f[64];
+                {
+                    uint32_t v[32];
+                    tmem_ld32(tbase + c, v);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+                    tmem_ld32(tbase + c + 32, v);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) f[32 + j] = __uint_as_float(v[j]);
+                }
+                if (c + 64 == BN) {  // both CTAs arrive on the leader's tmem-empty barrier
+                    tc_fence_before();
+                    arrive_remote(leader_addr(&tempty[acc]));
+                }
+                if (!store) continue;
+                if (!have_acc || !valid) {
+#pragma unroll
+                    for (int j = 0; j < 64; ++j) f[j] = 0.f;
+                } else if (KIND == ROW) {
+                    if (p.epi == EPI_BIAS || p.epi == EPI_BIAS_RELU) {
+                        const float* b = p.bias + static_cast<int64_t>(le) * p.N + ncol0 + c;
+#pragma unroll
+                        for (int j = 0; j < 64; j += 4) {
+                            const float4 bb = __ldg(reinterpret_cast<const float4*>(b + j));
+                            f[j] += bb.x; f[j + 1] += bb.y; f[j + 2] += bb.z; f[j + 3] += bb.w;
+                        }
+                        if (p.epi == EPI_BIAS_RELU) {
+#pragma unroll
+                            for (int j = 0; j < 64; ++j) f[j] = f[j] > 0.f ? f[j] : 0.f;
+                        }
+                    } else if (p.epi == EPI_RELU_MASK) {
+                        const uint4* mp = reinterpret_cast<const uint4*>(p.mask + crow * p.N + ncol0 + c);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            uint4 u = __ldg(mp + q);
+                            const __nv_bfloat16* hh = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+                            for (int j = 0; j < 8; ++j)
+                                if (!(__bfloat162float(hh[j]) > 0.f)) f[q * 8 + j] = 0.f;
+                        }
+                    }
+                }
+                uint8_t* sbuf = cstage + quarter * kStageCBytes;
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                __syncwarp();
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    uint4 u;
+                    __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) h2[j] = __floats2bfloat162_rn(f[q * 8 + 2 * j], f[q * 8 + 2 * j + 1]);
+                    *reinterpret_cast<uint4*>(sbuf + lane * 128 + ((q ^ (lane & 7)) << 4)) = u;
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+                    asm volatile(
+                        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                            reinterpret_cast<uint64_t>(&p.tmC)),
+                        "r"(smem_u32(sbuf)), "r"(static_cast<int32_t>(ncol0 + c)), "r"(box_row)
+                        : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+            }
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        __syncwarp();
+    }
+    __syncthreads();
+    cluster_sync();  // the partner's MMAs may still read this CTA's smem / TMEM
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+    }
+}
+
+}  // namespace pair
+
 // ------------------------------------------------------------ host side
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -562,6 +953,31 @@ void launch(const Params& p, int64_t max_tiles, cudaStream_t st) {
     MOE_LAUNCH_CHECK();
 }
 
+
+template <int KIND>
+void launch_pair(const Params& p, int64_t max_pair_tiles, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        MOE_CUDA_CHECK(cudaFuncSetAttribute(pair::gemm2_kernel<KIND>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(pair::kSmem)));
+        attr = true;
+    }
+    const int npairs = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms() / 2, max_pair_tiles)));
+    pair::gemm2_kernel<KIND><<<2 * npairs, kThreads, pair::kSmem, st>>>(p);
+    MOE_LAUNCH_CHECK();
+}
+
+// 2-CTA pairs pay off when the MMA is the bottleneck: every expert has >= 2
+// row tiles (ROW) / K spans >= 256 rows (WGRAD).  MOE_B200_PAIR=0/1 forces.
+static int pair_override() {
+    static int v = [] {
+        const char* e = std::getenv("MOE_B200_PAIR");
+        return e ? std::atoi(e) : -1;
+    }();
+    return v;
+}
+
 }  // namespace tc
 
 static bool g_tc_enabled = true;
@@ -599,7 +1015,15 @@ void launch_row_gemm_tc(const RowGemmArgs& a, cudaStream_t st) {
     p.epi = a.epi;
     p.b_mn = a.w_nmajor ? 1 : 0;
     const int64_t max_tiles = rows / tc::BM * (a.N / tc::BN);
-    tc::launch<tc::ROW>(p, max_tiles, st);
+    const int ov = tc::pair_override();
+    const bool use_pair = ov >= 0 ? ov == 1 : static_cast<int64_t>(a.ep) * a.cap_pad >= 2 * tc::BM;
+    if (use_pair) {
+        if (!a.w_nmajor)  // each CTA stages 128 of the 256 weight rows
+            p.tmB = tc::make_map(a.W, static_cast<int64_t>(a.El) * a.N, a.K, tc::BK, 128);
+        tc::launch_pair<tc::ROW>(p, (max_tiles + 1) / 2, st);
+    } else {
+        tc::launch<tc::ROW>(p, max_tiles, st);
+    }
 }
 
 void launch_wgrad_gemm_tc(const WgradGemmArgs& a, cudaStream_t st) {
@@ -619,7 +1043,13 @@ void launch_wgrad_gemm_tc(const WgradGemmArgs& a, cudaStream_t st) {
     p.epi = EPI_NONE;
     p.b_mn = 1;
     const int64_t max_tiles = static_cast<int64_t>(a.El) * (a.M / tc::BM) * (a.N / tc::BN);
-    tc::launch<tc::WGRAD>(p, max_tiles, st);
+    const int ov = tc::pair_override();
+    const bool use_pair = (a.M / tc::BM) % 2 == 0 &&
+                          (ov >= 0 ? ov == 1 : static_cast<int64_t>(a.ep) * a.cap_pad >= 4 * tc::BK);
+    if (use_pair)
+        tc::launch_pair<tc::WGRAD>(p, max_tiles / 2, st);
+    else
+        tc::launch<tc::WGRAD>(p, max_tiles, st);
 }
 
 }  // namespace moe
