@@ -201,8 +201,13 @@ ncclDataType_t nccl_type(size_t esz) { return esz == 2 ? ncclBfloat16 : ncclFloa
 // fixed (sender, expert) order).
 void all_to_all(moe_handle* h, const void* send, void* recv, size_t chunk_elems,
                 ncclDataType_t ty, size_t esz) {
+    // own chunk: device-local copy; peers: one NCCL group of send/recv pairs
+    MOE_CUDA_CHECK(cudaMemcpyAsync(static_cast<char*>(recv) + h->rank * chunk_elems * esz,
+                                   static_cast<const char*>(send) + h->rank * chunk_elems * esz,
+                                   chunk_elems * esz, cudaMemcpyDeviceToDevice, h->stream));
     NCCL_CHECK(ncclGroupStart());
     for (int s = 0; s < h->ep; ++s) {
+        if (s == h->rank) continue;
         NCCL_CHECK(ncclSend(static_cast<const char*>(send) + s * chunk_elems * esz, chunk_elems, ty,
                             s, h->comm, h->stream));
         NCCL_CHECK(ncclRecv(static_cast<char*>(recv) + s * chunk_elems * esz, chunk_elems, ty, s,
@@ -354,9 +359,11 @@ void forward_impl(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, c
     const int32_t* counts = h->kept.as<int32_t>();
     if (ep > 1) {
         // forward all-to-all: counts then rows (fixed-shape [E_local, cap_pad, d] slices)
+        NCCL_CHECK(ncclGroupStart());  // counts and rows in one NCCL group
         all_to_all(h, h->kept.p, h->counts_r.p, El, ncclInt32, 4);
         all_to_all(h, Xloc, h->Xr.p, static_cast<size_t>(El) * h->cap_pad * h->d,
                    nccl_type(h->esz), h->esz);
+        NCCL_CHECK(ncclGroupEnd());
         counts = h->counts_r.as<int32_t>();
         const double slice = static_cast<double>(El) * h->cap * h->d;
         h->last_logical_traffic = 2.0 * slice * 8.0 * (ep - 1);
