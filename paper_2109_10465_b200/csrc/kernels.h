@@ -167,3 +167,14 @@ template <class TX>
 void launch_gate_dw(const TX* x, const float* noise, const float* dL, float* part, int64_t T,
                     int d, int E, int splits, cudaStream_t st);
 }  // namespace moe
+
+namespace moe {
+constexpr int kMaxCopies = 16;
+struct PeerCopyJobs {
+    const void* src[kMaxCopies];
+    void* dst[kMaxCopies];
+    int64_t bytes[kMaxCopies];
+    int n;
+};
+void launch_peer_copy(const PeerCopyJobs& jobs, cudaStream_t st);
+}  // namespace moe

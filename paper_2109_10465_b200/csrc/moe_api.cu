@@ -11,6 +11,7 @@
 #include <atomic>
 #include <cmath>
 #include <map>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -143,7 +144,15 @@ struct moe_handle {
     // comm stream for the dX all-to-all (owned by the handle)
     cudaStream_t side = nullptr, comm_stream = nullptr;
     cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr, ev_side = nullptr, ev_comm = nullptr;
+    // NVLink peer map (CUDA IPC) of the receive buffers: [buffer][rank]
+    enum { P_X = 0, P_O, P_DO, P_DX, P_CNT, P_NBUF };
+    bool ipc = false;
+    void* peer[P_NBUF][8] = {};
+    DevMem bar;  // 1-int NCCL all-reduce used as the exchange barrier
     ~moe_handle() {
+        for (int b = 0; b < P_NBUF; ++b)
+            for (int r = 0; r < 8; ++r)
+                if (ipc && r != rank && peer[b][r]) cudaIpcCloseMemHandle(peer[b][r]);
         for (cudaEvent_t e : {ev_a, ev_b, ev_c, ev_side, ev_comm})
             if (e) cudaEventDestroy(e);
         if (side) cudaStreamDestroy(side);
@@ -214,6 +223,74 @@ void all_to_all(moe_handle* h, const void* send, void* recv, size_t chunk_elems,
                             h->comm, h->stream));
     }
     NCCL_CHECK(ncclGroupEnd());
+}
+
+// Expert-parallel exchange over NVLink: this rank stores chunk s of `send`
+// straight into chunk `rank` of peer s's receive buffer `buf` (IPC-mapped),
+// then one 4-byte NCCL all-reduce acts as the barrier that makes every
+// peer's stores visible before the receiver reads (stream order on each rank
+// puts the stores before its all-reduce).  Write-after-read safety comes from
+// the exchange points already between a buffer's last read and its next write
+// (see DESIGN.md §7).  Falls back to NCCL send/recv when IPC is unavailable.
+struct XSpec {
+    const void* send;
+    void* recv;
+    int buf;
+    size_t chunk_elems;
+    ncclDataType_t ty;
+    size_t esz;
+};
+
+void exchange(moe_handle* h, std::initializer_list<XSpec> specs) {
+    if (!h->ipc) {
+        NCCL_CHECK(ncclGroupStart());
+        for (const XSpec& x : specs) all_to_all(h, x.send, x.recv, x.chunk_elems, x.ty, x.esz);
+        NCCL_CHECK(ncclGroupEnd());
+        return;
+    }
+    PeerCopyJobs jobs{};
+    jobs.n = 0;
+    for (const XSpec& x : specs) {
+        const size_t bytes = x.chunk_elems * x.esz;
+        for (int s = 0; s < h->ep; ++s) {
+            jobs.src[jobs.n] = static_cast<const char*>(x.send) + s * bytes;
+            char* dst = s == h->rank ? static_cast<char*>(x.recv) : static_cast<char*>(h->peer[x.buf][s]);
+            jobs.dst[jobs.n] = dst + h->rank * bytes;
+            jobs.bytes[jobs.n] = static_cast<int64_t>(bytes);
+            ++jobs.n;
+        }
+    }
+    launch_peer_copy(jobs, h->stream);
+    NCCL_CHECK(ncclAllReduce(h->bar.p, h->bar.p, 1, ncclInt32, ncclSum, h->comm, h->stream));
+}
+
+void ipc_setup(moe_handle* h) {
+    // export the receive buffers, all-gather the handles over NCCL, open peers'
+    void* bufs[moe_handle::P_NBUF] = {h->Xr.p, h->Oloc.p, h->dOr.p, h->dXloc.p, h->counts_r.p};
+    const size_t hs = sizeof(cudaIpcMemHandle_t);
+    std::vector<cudaIpcMemHandle_t> mine(moe_handle::P_NBUF), all(moe_handle::P_NBUF * h->ep);
+    for (int b = 0; b < moe_handle::P_NBUF; ++b) MOE_CUDA_CHECK(cudaIpcGetMemHandle(&mine[b], bufs[b]));
+    DevMem dev;
+    dev.alloc(hs * moe_handle::P_NBUF * h->ep);
+    char* base = static_cast<char*>(dev.p);
+    MOE_CUDA_CHECK(cudaMemcpy(base + h->rank * hs * moe_handle::P_NBUF, mine.data(),
+                              hs * moe_handle::P_NBUF, cudaMemcpyHostToDevice));
+    NCCL_CHECK(ncclAllGather(base + h->rank * hs * moe_handle::P_NBUF, base, hs * moe_handle::P_NBUF,
+                             ncclUint8, h->comm, h->stream));
+    MOE_CUDA_CHECK(cudaStreamSynchronize(h->stream));
+    MOE_CUDA_CHECK(cudaMemcpy(all.data(), base, hs * moe_handle::P_NBUF * h->ep, cudaMemcpyDeviceToHost));
+    for (int r = 0; r < h->ep; ++r)
+        for (int b = 0; b < moe_handle::P_NBUF; ++b) {
+            if (r == h->rank) {
+                h->peer[b][r] = bufs[b];
+                continue;
+            }
+            MOE_CUDA_CHECK(cudaIpcOpenMemHandle(&h->peer[b][r], all[r * moe_handle::P_NBUF + b],
+                                                cudaIpcMemLazyEnablePeerAccess));
+        }
+    h->bar.alloc(16);
+    MOE_CUDA_CHECK(cudaMemset(h->bar.p, 0, 16));
+    h->ipc = true;
 }
 
 template <class TIO>
@@ -359,11 +436,9 @@ void forward_impl(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, c
     const int32_t* counts = h->kept.as<int32_t>();
     if (ep > 1) {
         // forward all-to-all: counts then rows (fixed-shape [E_local, cap_pad, d] slices)
-        NCCL_CHECK(ncclGroupStart());  // counts and rows in one NCCL group
-        all_to_all(h, h->kept.p, h->counts_r.p, El, ncclInt32, 4);
-        all_to_all(h, Xloc, h->Xr.p, static_cast<size_t>(El) * h->cap_pad * h->d,
-                   nccl_type(h->esz), h->esz);
-        NCCL_CHECK(ncclGroupEnd());
+        exchange(h, {{h->kept.p, h->counts_r.p, moe_handle::P_CNT, static_cast<size_t>(El), ncclInt32, 4},
+                     {Xloc, h->Xr.p, moe_handle::P_X, static_cast<size_t>(El) * h->cap_pad * h->d,
+                      nccl_type(h->esz), h->esz}});
         counts = h->counts_r.as<int32_t>();
         const double slice = static_cast<double>(El) * h->cap * h->d;
         h->last_logical_traffic = 2.0 * slice * 8.0 * (ep - 1);
@@ -379,8 +454,8 @@ void forward_impl(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, c
     h->mark("ffn2_fwd");
     TIO* Oloc = h->Or.as<TIO>();
     if (ep > 1) {
-        all_to_all(h, h->Or.p, h->Oloc.p, static_cast<size_t>(El) * h->cap_pad * h->d,
-                   nccl_type(h->esz), h->esz);
+        exchange(h, {{h->Or.p, h->Oloc.p, moe_handle::P_O, static_cast<size_t>(El) * h->cap_pad * h->d,
+                      nccl_type(h->esz), h->esz}});
         Oloc = h->Oloc.as<TIO>();
         h->mark("a2a_combine");
     }
@@ -433,8 +508,8 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
     h->mark("combine_bwd");
     const int32_t* counts = h->kept.as<int32_t>();
     if (ep > 1) {
-        all_to_all(h, dOloc, h->dOr.p, static_cast<size_t>(El) * h->cap_pad * d,
-                   nccl_type(h->esz), h->esz);
+        exchange(h, {{dOloc, h->dOr.p, moe_handle::P_DO, static_cast<size_t>(El) * h->cap_pad * d,
+                      nccl_type(h->esz), h->esz}});
         counts = h->counts_r.as<int32_t>();
         h->mark("a2a_dO");
     }
@@ -474,8 +549,8 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
         MOE_CUDA_CHECK(cudaStreamWaitEvent(h->comm_stream, h->ev_c, 0));
         cudaStream_t saved = h->stream;
         h->stream = h->comm_stream;
-        all_to_all(h, h->dXr.p, h->dXloc.p, static_cast<size_t>(El) * h->cap_pad * d,
-                   nccl_type(h->esz), h->esz);
+        exchange(h, {{h->dXr.p, h->dXloc.p, moe_handle::P_DX, static_cast<size_t>(El) * h->cap_pad * d,
+                      nccl_type(h->esz), h->esz}});
         h->stream = saved;
         MOE_CUDA_CHECK(cudaEventRecord(h->ev_comm, h->comm_stream));
         dXloc = h->dXloc.as<TIO>();
@@ -895,6 +970,11 @@ moe_status moe_ep_init(moe_handle* h, const void* unique_id) {
         ncclUniqueId id;
         std::memcpy(&id, unique_id, sizeof(id));
         NCCL_CHECK(ncclCommInitRank(&h->comm, h->ep, id, h->rank));
+        // NVLink peer map for the exchanges (single node, <= 8 ranks, 16-byte
+        // aligned count chunks); MOE_B200_EP_TRANSPORT=nccl keeps NCCL send/recv.
+        const char* tr = std::getenv("MOE_B200_EP_TRANSPORT");
+        const bool want_ipc = !(tr && std::string(tr) == "nccl");
+        if (want_ipc && h->ep <= 8 && (h->El * 4) % 16 == 0) ipc_setup(h);
     });
 }
 

@@ -381,3 +381,51 @@ INST(__nv_bfloat16)
 #undef INST
 
 }  // namespace moe
+
+namespace moe {
+
+// Multi-destination copy for the expert-parallel exchange: up to kMaxCopies
+// (src, dst, bytes) jobs, dst typically a peer GPU's buffer mapped over
+// NVLink (CUDA IPC).  16-byte vectors, 4 in flight per thread, grid-stride
+// over the concatenation of all jobs.
+__global__ void __launch_bounds__(256) peer_copy_kernel(PeerCopyJobs jobs) {
+    int64_t total = 0;
+    for (int j = 0; j < jobs.n; ++j) total += jobs.bytes[j] >> 4;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < total; v += 4 * stride) {
+        uint4 buf[4];
+        int64_t idx[4];
+        int jj[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            int64_t w = v + u * stride;
+            jj[u] = -1;
+            if (w < total) {
+                int j = 0;
+                while (w >= (jobs.bytes[j] >> 4)) { w -= jobs.bytes[j] >> 4; ++j; }
+                jj[u] = j;
+                idx[u] = w;
+                buf[u] = __ldg(reinterpret_cast<const uint4*>(jobs.src[j]) + w);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (jj[u] >= 0) reinterpret_cast<uint4*>(jobs.dst[jj[u]])[idx[u]] = buf[u];
+    }
+}
+
+void launch_peer_copy(const PeerCopyJobs& jobs, cudaStream_t st) {
+    int64_t total = 0;
+    for (int j = 0; j < jobs.n; ++j) {
+        if ((jobs.bytes[j] & 15) || (reinterpret_cast<uintptr_t>(jobs.src[j]) & 15) ||
+            (reinterpret_cast<uintptr_t>(jobs.dst[j]) & 15))
+            throw Status(1, "peer copy: 16-byte alignment required");
+        total += jobs.bytes[j] >> 4;
+    }
+    if (total == 0) return;
+    const int grid = (int)std::min<int64_t>(4 * kNumSMs, ceil_div(total, 256 * 4));
+    peer_copy_kernel<<<grid, 256, 0, st>>>(jobs);
+    MOE_LAUNCH_CHECK();
+}
+
+}  // namespace moe
