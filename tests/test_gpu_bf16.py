@@ -156,3 +156,18 @@ def test_bf16_c3_full_size_properties():
     assert max(errs) <= BF16_TOL
     layer.backward(torch.randn(T, d, device="cuda").to(torch.bfloat16), 1.0)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("pair", ["0", "1"])
+def test_bf16_gemm_variants_subprocess(pair):
+    """Both tcgen05 kernel variants (1-CTA and cta_group::2 CTA pairs, chosen by
+    MOE_B200_PAIR) pass the bf16-vs-oracle cases, including experts with an odd
+    number of 128-row tiles (the pair's second CTA then has no rows)."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, MOE_B200_PAIR=pair)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-k", "vs_oracle",
+                        os.path.abspath(__file__)], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
