@@ -426,6 +426,93 @@ def run_ours(args):
     return 0
 
 
+EXTRA = {
+    # BASELINE.json configs other than the headline (one GPU; device-timed)
+    "c1": dict(E=8, d=512, f=2048, T=4096, k=1, C=1.0, mode=0, dtype="fp32", layers=1,
+               phase=0, fwd_only=False, desc="config 1: fp32 parity path, E=8 top-1 C=1.0 plain"),
+    "c2": dict(E=32, d=1024, f=4096, T=16384, k=2, C=1.25, mode=2, dtype="bf16", layers=1,
+               phase=0, fwd_only=False, desc="config 2: E=32 top-2 C=1.25 RTS, aux loss"),
+    "c4": dict(E=64, d=1024, f=4096, T=16384, k=1, C=1.0, mode=2, dtype="bf16", layers=18,
+               phase=0, fwd_only=False,
+               desc="config 4: 18-layer MoE stack (d=1024, f=4096, E=64, RTS), x_{l+1}=y_l, bwd in reverse"),
+    "c5": dict(E=8, d=1024, f=4096, T=262144, k=1, C=2.0, mode=0, dtype="bf16", layers=1,
+               phase=1, fwd_only=True,
+               desc="config 5: inference (eval, C=2.0, no jitter), experts pruned to 8, T=256k, fwd only"),
+}
+
+
+def run_extra(args):
+    """Device-timed tokens/s for the other BASELINE configs (rank 0, 1 GPU)."""
+    import numpy as np
+    import torch
+
+    import paper_2109_10465_b200 as M
+    w = EXTRA[args.workload]
+    E, d, f, T, L = w["E"], w["d"], w["f"], args.tokens or w["T"], w["layers"]
+    dt = torch.float32 if w["dtype"] == "fp32" else torch.bfloat16
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev).manual_seed(7)
+    cfg = M.RouterConfig(num_experts=E, top_k=w["k"], capacity_factor_train=w["C"],
+                         capacity_factor_eval=w["C"] if w["phase"] == 1 else 2.0,
+                         assignment_mode=M.AssignmentMode(w["mode"]))
+    s_w = float(np.sqrt(6.0 / (d + f)))
+    layers, params = [], []
+    for _ in range(L):
+        layers.append(M.MoeLayer(cfg, T, d, f, dt))
+        params.append(M.MoeLayerParams(
+            (torch.rand(d, E, device=dev, generator=g) * 2 - 1) * float(np.sqrt(6.0 / (d + E))),
+            ((torch.rand(E, d, f, device=dev, generator=g) * 2 - 1) * s_w).to(dt),
+            (torch.rand(E, f, device=dev, generator=g) * 2 - 1) * 0.01,
+            ((torch.rand(E, f, d, device=dev, generator=g) * 2 - 1) * s_w).to(dt),
+            (torch.rand(E, d, device=dev, generator=g) * 2 - 1) * 0.01))
+    x0 = ((torch.rand(T, d, device=dev, generator=g) * 2 - 1)).to(dt)
+    dy0 = ((torch.rand(T, d, device=dev, generator=g) * 2 - 1)).to(dt)
+    ys = [torch.empty_like(x0) for _ in range(L)]
+    aux = torch.empty(1, device=dev)
+    grads = [dict(dx=torch.empty_like(x0), dgate_w=torch.empty(d, E, device=dev),
+                  dw1=torch.empty(E, d, f, device=dev, dtype=dt), db1=torch.empty(E, f, device=dev),
+                  dw2=torch.empty(E, f, d, device=dev, dtype=dt), db2=torch.empty(E, d, device=dev),
+                  dresidual=torch.empty_like(x0)) for _ in range(L)]
+    zero = torch.zeros_like(x0)
+    phase = M.Phase(w["phase"])
+
+    def step(i):
+        h = x0
+        for l in range(L):  # stack: zero residual inside blocks (model.cpp:340-350)
+            layers[l].forward(h, params[l], phase, M.derive_seed(M.derive_seed(42, i), l),
+                              residual=zero if L > 1 else None, y=ys[l], aux=aux, decision=False,
+                              check=False)
+            h = ys[l]
+        if w["fwd_only"]:
+            return
+        g_ = dy0
+        for l in reversed(range(L)):
+            layers[l].backward(g_, 1.0, check=False, grads=grads[l])
+            g_ = grads[l]["dx"]
+
+    for i in range(max(args.warmup, 3)):
+        step(i)
+    for lay in layers:
+        lay.handle.check()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(args.steps):
+        step(i)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    flops = (4.0 if w["fwd_only"] else 12.0) * T * w["k"] * d * f * L
+    print(json.dumps({"metric": "MoE layer " + ("fwd" if w["fwd_only"] else "fwd+bwd") + " tokens/sec",
+                      "value": T / (ms / 1e3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+                      "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                      "dtype": w["dtype"], "data": "synthetic",
+                      "config": {"workload": args.workload, "desc": w["desc"], "tokens": T,
+                                 "layers": L, "experts": E, "d_model": d, "d_ff": f, "top_k": w["k"]},
+                      "expert_tflops_upper_bound": flops / (ms / 1e3) / 1e12}), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -434,10 +521,14 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tokens-per-gpu", type=int, default=WORKLOAD["tokens_per_gpu"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="c3", choices=["c3"] + sorted(EXTRA))
+    ap.add_argument("--tokens", type=int, default=0, help="override T for --workload c1/c2/c4/c5")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.workload != "c3":
+        return run_extra(args)
     return run_ours(args)
 
 
