@@ -257,7 +257,16 @@ __device__ __forceinline__ uint64_t next_word(const uint64_t* __restrict__ o, in
     return twist(o[N - 1], n0, nm);
 }
 
-constexpr int kChunkThreads = 2 * N + 16;  // 640: two threads per window word for the jump
+constexpr int kChunkThreads = 2 * N + 16;  // 640 = 20 warps
+constexpr int kRing = 4;                    // generation ring depth (312-word blocks)
+constexpr int kBarFull = 1, kBarEmpty = kBarFull + kRing, kBarTw = kBarEmpty + kRing;
+
+__device__ __forceinline__ void bar_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int count) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
 
 // One CTA per chunk: jump to the chunk's window, then generate J outputs.
 __global__ void __launch_bounds__(kChunkThreads, 1)
@@ -268,7 +277,6 @@ chunk_kernel(const uint64_t* __restrict__ base, const uint64_t* __restrict__ jum
     uint64_t* sb = sm;              // base [BASE]
     uint64_t* sg = sm + BASE;       // g_c  [W]
     uint64_t* s0 = sg + W;          // ping [N]
-    uint64_t* s1 = s0 + N;          // pong [N]
     const int c = blockIdx.x;
     const int64_t q0 = static_cast<int64_t>(c) * J;
     if (q0 >= count) return;
@@ -312,26 +320,45 @@ chunk_kernel(const uint64_t* __restrict__ base, const uint64_t* __restrict__ jum
             if (j0 + r < N) atomicXor(reinterpret_cast<unsigned long long*>(&s0[j0 + r]), acc[r]);
     }
     __syncthreads();
+    // Generation, warp-specialised.  Warps 0-9 ("twisters") run only the block
+    // recurrence — the serial critical path — into a kRing-deep ring of
+    // 312-word blocks; warps 10-19 ("emitters") temper, convert and store each
+    // completed block.  Named barriers: FULL[slot] (twisters arrive, emitters
+    // wait), EMPTY[slot] (emitters arrive, twisters wait), TW (twisters only).
+    // Block 0 (the jump window) is already in ring slot 0.
     const int64_t n = min(J, count - q0);
-    uint64_t* cur = s0;
-    uint64_t* nxt = s1;
-    for (int64_t blk = 0; blk * N < n; ++blk) {
-        if (t < N) {
-            const int64_t q = blk * N + t;
-            if (q < n) {
-                const uint64_t out = temper(cur[t]);
+    const int64_t nblk = (n + N - 1) / N;
+    uint64_t* ring = s0;  // [kRing][N] (s0 and the following smem)
+    constexpr int kTw = 10 * 32;
+    const bool twister = t < kTw;
+    if (twister) {
+        bar_arrive(kBarFull + 0, kChunkThreads);
+        for (int64_t b = 1; b < nblk; ++b) {
+            const int slot = static_cast<int>(b % kRing);
+            if (b >= kRing) bar_sync(kBarEmpty + slot, kChunkThreads);  // slot's old block consumed
+            const uint64_t* prev = ring + static_cast<int>((b - 1) % kRing) * N;
+            uint64_t v = 0;
+            if (t < N) v = next_word(prev, t);
+            if (t < N) ring[slot * N + t] = v;
+            bar_sync(kBarTw, kTw);  // whole block written before it is the next input
+            bar_arrive(kBarFull + slot, kChunkThreads);
+        }
+    } else {
+        const int u = t - kTw;
+        for (int64_t b = 0; b < nblk; ++b) {
+            const int slot = static_cast<int>(b % kRing);
+            bar_sync(kBarFull + slot, kChunkThreads);
+            const int64_t q = b * N + u;
+            if (u < N && q < n) {
+                const uint64_t out = temper(ring[slot * N + u]);
                 if (raw_out) raw_out[q0 + q] = out;
                 if (noise) {
-                    const double u = static_cast<double>(out >> 11) * 0x1.0p-53;
-                    noise[q0 + q] = static_cast<float>(lo + span * u);
+                    const double uu = static_cast<double>(out >> 11) * 0x1.0p-53;
+                    noise[q0 + q] = static_cast<float>(lo + span * uu);
                 }
             }
-            if ((blk + 1) * N < n) nxt[t] = next_word(cur, t);
+            if (b + kRing < nblk) bar_arrive(kBarEmpty + slot, kChunkThreads);
         }
-        __syncthreads();
-        uint64_t* tmp = cur;
-        cur = nxt;
-        nxt = tmp;
     }
 }
 
@@ -353,7 +380,7 @@ void generate(uint64_t seed, int64_t count, double lo, double hi, float* noise, 
     Scratch& sc = scratch();
     base_kernel<<<1, kThreads, 0, st>>>(seed, sc.base);
     MOE_LAUNCH_CHECK();
-    const size_t smem = sizeof(uint64_t) * (BASE + W + 2 * N);
+    const size_t smem = sizeof(uint64_t) * (BASE + W + kRing * N);
     static bool attr = false;
     if (!attr) {
         MOE_CUDA_CHECK(cudaFuncSetAttribute(chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
