@@ -26,7 +26,7 @@ constexpr int kMaxGateSplits = 8;
 int gate_logit_splits(int64_t T, int d, int E);
 void launch_balance_finalize(const float* colsum_part, const int32_t* count_part, int nparts,
                              int64_t T, int E, double alpha, float* aux, float* fcoef,
-                             int32_t* counts, cudaStream_t st);
+                             int32_t* counts, double* term, unsigned* done, cudaStream_t st);
 
 struct AssignScratch {
     int32_t* hist;   // [chunks][K][E]
@@ -150,7 +150,7 @@ bool launch_jitter_noise_device(uint64_t seed, int64_t count, double eps, float*
 void launch_balance_from_probs(const float* probs, int64_t T, int E, int K,
                                const int32_t* expert_id, double alpha, float* loss,
                                float* colsum_part, int32_t* count_part, uint32_t* flags,
-                               cudaStream_t st);
+                               double* term, unsigned* done, cudaStream_t st);
 }  // namespace moe
 
 namespace moe {
@@ -177,4 +177,16 @@ struct PeerCopyJobs {
     int n;
 };
 void launch_peer_copy(const PeerCopyJobs& jobs, cudaStream_t st);
+
+// gate2.cu: larger-tile gate GEMMs (require gate2_ok(d, E))
+bool gate2_ok(int d, int E);
+int gate2_logit_splits(int64_t T, int d, int E);
+template <class TX>
+void launch_gate2_logits(const TX* x, const float* noise, const float* wg, float* logits, int64_t T,
+                         int d, int E, int splits, cudaStream_t st);
+void launch_gate2_transpose(const float* wg, float* wgt, int d, int E, cudaStream_t st);
+template <class TIO>
+void launch_gate2_dx(int64_t T, int d, int E, int K, int cap_pad, const float* dL, const float* wgt,
+                     const float* noise, const TIO* dX, const int32_t* choice, const int32_t* pos,
+                     const TIO* dy, bool residual_is_x, TIO* dx, TIO* dres, cudaStream_t st);
 }  // namespace moe

@@ -164,7 +164,8 @@ struct moe_handle {
     DevMem colsum_part, count_part, fcoef, fcount, aux_scratch, noise, ord, flags;
     DevMem hist, base, gkept;
     DevMem Xloc, Xr, H, Or, Oloc, dOloc, dOr, dH, dXr, dXloc;
-    DevMem dL, dxg, dwg_part;
+    DevMem dL, dxg, dwg_part, wgt;
+    DevMem bal_term, bal_done;  // balance_finalize per-expert terms + CTA counter
     AssignScratch as{};
     std::vector<uint32_t> host_ord;
 
@@ -360,7 +361,11 @@ void route(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, int phas
     }
     // logits = (x * noise) @ gate_w  (routing.cpp:71)
     int nsplit = 1;
-    if (gate_fast_ok(static_cast<int>(h->d), E)) {
+    if (gate2_ok(static_cast<int>(h->d), E)) {
+        nsplit = gate2_logit_splits(T, static_cast<int>(h->d), E);
+        launch_gate2_logits<TIO>(x, jitter ? h->noise.as<float>() : nullptr, gate_w,
+                                 h->logits.as<float>(), T, static_cast<int>(h->d), E, nsplit, st);
+    } else if (gate_fast_ok(static_cast<int>(h->d), E)) {
         nsplit = gate_logit_splits(T, static_cast<int>(h->d), E);
         launch_gate_logits<TIO>(x, jitter ? h->noise.as<float>() : nullptr, gate_w,
                                 h->logits.as<float>(), T, static_cast<int>(h->d), E, nsplit, st);
@@ -377,7 +382,8 @@ void route(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, int phas
     launch_balance_finalize(h->colsum_part.as<float>(), h->count_part.as<int32_t>(),
                             softmax_parts(T), T, E, h->cfg.balance_coeff,
                             aux ? aux : h->aux_scratch.as<float>(), h->fcoef.as<float>(),
-                            h->fcount.as<int32_t>(), st);
+                            h->fcount.as<int32_t>(), h->bal_term.as<double>(),
+                            h->bal_done.as<unsigned>(), st);
     h->mark("balance_loss");
     h->jitter_on = jitter;
 }
@@ -567,7 +573,12 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
                                  h->comm, st));
         h->mark("allreduce_dgate_w");
     }
-    if (fast) {  // dx = (dL Wg^T) * noise + dispatch bwd + residual, one kernel
+    if (gate2_ok(static_cast<int>(d), E)) {  // dx = (dL Wg^T) * noise + dispatch bwd + residual
+        launch_gate2_transpose(h->gate_w, h->wgt.as<float>(), static_cast<int>(d), E, st);
+        launch_gate2_dx<TIO>(T, static_cast<int>(d), E, K, h->cap_pad, h->dL.as<float>(),
+                             h->wgt.as<float>(), noise, dXloc, h->choice.as<int32_t>(),
+                             h->pos.as<int32_t>(), dy, !h->has_residual, dx, dres, st);
+    } else if (fast) {  // same, 64x64 tiles
         launch_gate_dx<TIO>(T, static_cast<int>(d), E, K, h->cap_pad, h->dL.as<float>(), h->gate_w,
                             noise, dXloc, h->choice.as<int32_t>(), h->pos.as<int32_t>(), dy,
                             !h->has_residual, dx, dres, st);
@@ -607,6 +618,9 @@ void alloc_workspace(moe_handle* h) {
     h->count_part.alloc(4 * static_cast<size_t>(nparts) * E);
     h->fcoef.alloc(4 * E);
     h->fcount.alloc(4 * E);
+    h->bal_term.alloc(8 * E);
+    h->bal_done.alloc(16);
+    MOE_CUDA_CHECK(cudaMemset(h->bal_done.p, 0, 16));
     h->aux_scratch.alloc(16);
     h->noise.alloc(4 * T * d);
     h->ord.alloc(4 * T);
@@ -639,6 +653,7 @@ void alloc_workspace(moe_handle* h) {
     h->dL.alloc(4 * T * E);
     h->dxg.alloc(4 * T * d);
     h->dwg_part.alloc(4 * 16 * d * E);
+    h->wgt.alloc(4 * d * E);
     MOE_CUDA_CHECK(cudaDeviceSynchronize());
 }
 
@@ -948,7 +963,8 @@ moe_status moe_balance_loss(moe_handle* h, int64_t T, const float* probs,
         // needed; compute partials directly from probs via a dedicated pass
         launch_balance_from_probs(probs, T, h->E, h->K, expert_id, alpha, loss,
                                   h->colsum_part.as<float>(), h->count_part.as<int32_t>(),
-                                  h->flags.as<uint32_t>(), h->stream);
+                                  h->flags.as<uint32_t>(), h->bal_term.as<double>(),
+                                  h->bal_done.as<unsigned>(), h->stream);
     });
     if (s) return s;
     return moe_check(h, nullptr);

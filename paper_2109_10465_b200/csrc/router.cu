@@ -23,6 +23,7 @@ namespace moe {
 // flags for non-finite values / rows not summing to one.
 // ---------------------------------------------------------------------------
 constexpr int kSoftmaxWarps = 8;
+constexpr int kRowsPerPart = 2 * kSoftmaxWarps;  // token rows per CTA (2 per warp)
 
 __global__ void __launch_bounds__(kSoftmaxWarps * 32)
 softmax_topk_kernel(const float* __restrict__ logits, int nsplit, int64_t T, int E, int K,
@@ -38,7 +39,7 @@ softmax_topk_kernel(const float* __restrict__ logits, int nsplit, int64_t T, int
     for (int i = threadIdx.x; i < E; i += blockDim.x) s_cnt[i] = 0;
     __syncthreads();
     uint32_t flag = 0;
-    const int64_t rows_per_cta = (int64_t)kSoftmaxWarps * 8;
+    const int64_t rows_per_cta = kRowsPerPart;
     const int64_t t0 = (int64_t)blockIdx.x * rows_per_cta;
     for (int64_t t = t0 + warp; t < min(T, t0 + rows_per_cta); t += kSoftmaxWarps) {
         const float* Lp = logits + t * E;
@@ -134,31 +135,50 @@ softmax_topk_kernel(const float* __restrict__ logits, int nsplit, int64_t T, int
 
 // aux = sum_e mean_t(P[:,e]) * f_e,  f_e = alpha * E * count_e / T.
 // Also emits fcoef[e] = f_e / T, the per-element gradient dP += daux * f_e/T.
-__global__ void balance_finalize_kernel(const float* __restrict__ colsum_part,
-                                        const int32_t* __restrict__ count_part, int nparts,
-                                        int64_t T, int E, double alpha, float* __restrict__ aux,
-                                        float* __restrict__ fcoef, int32_t* __restrict__ counts) {
-    __shared__ double s_acc[1024];
-    double my = 0.0;
-    for (int e = threadIdx.x; e < E; e += blockDim.x) {
-        double cs = 0.0;
-        int64_t cnt = 0;
-        for (int p = 0; p < nparts; ++p) {
-            cs += (double)colsum_part[(int64_t)p * E + e];
-            cnt += count_part[(int64_t)p * E + e];
-        }
-        const double f = alpha * (double)E * (double)cnt / (double)T;
-        if (fcoef) fcoef[e] = (float)(f / (double)T);
-        if (counts) counts[e] = (int32_t)cnt;
-        my += (cs / (double)T) * f;
+// One CTA per expert reduces that expert's per-part partials (fixed order:
+// strided per thread, then a shared-memory tree); the last CTA to finish sums
+// the E terms in expert order.  Deterministic, no float atomics.
+__global__ void __launch_bounds__(256)
+balance_finalize_kernel(const float* __restrict__ colsum_part, const int32_t* __restrict__ count_part,
+                        int nparts, int64_t T, int E, double alpha, float* __restrict__ aux,
+                        float* __restrict__ fcoef, int32_t* __restrict__ counts,
+                        double* __restrict__ term, unsigned* __restrict__ done) {
+    __shared__ double s_cs[256];
+    __shared__ long long s_cnt[256];
+    __shared__ bool last;
+    const int e = blockIdx.x;
+    double cs = 0.0;
+    long long cnt = 0;
+    for (int p = threadIdx.x; p < nparts; p += blockDim.x) {
+        cs += (double)colsum_part[(int64_t)p * E + e];
+        cnt += count_part[(int64_t)p * E + e];
     }
-    s_acc[threadIdx.x] = my;
+    s_cs[threadIdx.x] = cs;
+    s_cnt[threadIdx.x] = cnt;
     __syncthreads();
     for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-        if ((int)threadIdx.x < o) s_acc[threadIdx.x] += s_acc[threadIdx.x + o];
+        if ((int)threadIdx.x < o) {
+            s_cs[threadIdx.x] += s_cs[threadIdx.x + o];
+            s_cnt[threadIdx.x] += s_cnt[threadIdx.x + o];
+        }
         __syncthreads();
     }
-    if (threadIdx.x == 0) *aux = (float)s_acc[0];
+    if (threadIdx.x == 0) {
+        const double f = alpha * (double)E * (double)s_cnt[0] / (double)T;
+        if (fcoef) fcoef[e] = (float)(f / (double)T);
+        if (counts) counts[e] = (int32_t)s_cnt[0];
+        term[e] = (s_cs[0] / (double)T) * f;
+        __threadfence();
+        last = atomicAdd(done, 1u) == (unsigned)(E - 1);
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        double s = 0.0;
+        for (int q = 0; q < E; ++q) s += ((volatile double*)term)[q];
+        *aux = (float)s;
+        *done = 0u;  // reset for the next call
+    }
 }
 
 void launch_softmax_topk(const float* logits, int nsplit, int64_t T, int E, int K, float* probs,
@@ -172,13 +192,13 @@ void launch_softmax_topk(const float* logits, int nsplit, int64_t T, int E, int 
     MOE_LAUNCH_CHECK();
 }
 
-int softmax_parts(int64_t T) { return (int)ceil_div(T, (int64_t)kSoftmaxWarps * 8); }
+int softmax_parts(int64_t T) { return (int)ceil_div(T, (int64_t)kRowsPerPart); }
 
 void launch_balance_finalize(const float* colsum_part, const int32_t* count_part, int nparts,
                              int64_t T, int E, double alpha, float* aux, float* fcoef,
-                             int32_t* counts, cudaStream_t st) {
-    balance_finalize_kernel<<<1, 256, 0, st>>>(colsum_part, count_part, nparts, T, E, alpha, aux,
-                                               fcoef, counts);
+                             int32_t* counts, double* term, unsigned* done, cudaStream_t st) {
+    balance_finalize_kernel<<<E, 256, 0, st>>>(colsum_part, count_part, nparts, T, E, alpha, aux,
+                                               fcoef, counts, term, done);
     MOE_LAUNCH_CHECK();
 }
 
@@ -461,8 +481,8 @@ balance_partials_kernel(const float* __restrict__ probs, int64_t T, int E, int K
     for (int i = threadIdx.x; i < E; i += blockDim.x) s_cnt[i] = 0;
     __syncthreads();
     uint32_t flag = 0;
-    const int64_t t0 = (int64_t)blockIdx.x * 64;
-    for (int64_t t = t0 + warp; t < min(T, t0 + 64); t += 8) {
+    const int64_t t0 = (int64_t)blockIdx.x * kRowsPerPart;
+    for (int64_t t = t0 + warp; t < min(T, t0 + kRowsPerPart); t += 8) {
         float s = 0.f;
         for (int e = lane; e < E; e += 32) {
             const float p = probs[t * E + e];
@@ -489,12 +509,13 @@ balance_partials_kernel(const float* __restrict__ probs, int64_t T, int E, int K
 void launch_balance_from_probs(const float* probs, int64_t T, int E, int K,
                                const int32_t* expert_id, double alpha, float* loss,
                                float* colsum_part, int32_t* count_part, uint32_t* flags,
-                               cudaStream_t st) {
+                               double* term, unsigned* done, cudaStream_t st) {
     const int nparts = softmax_parts(T);
     balance_partials_kernel<<<nparts, 256, sizeof(float) * 8 * E + sizeof(int32_t) * E, st>>>(
         probs, T, E, K, expert_id, colsum_part, count_part, flags);
     MOE_LAUNCH_CHECK();
-    launch_balance_finalize(colsum_part, count_part, nparts, T, E, alpha, loss, nullptr, nullptr, st);
+    launch_balance_finalize(colsum_part, count_part, nparts, T, E, alpha, loss, nullptr, nullptr,
+                            term, done, st);
 }
 
 }  // namespace moe
