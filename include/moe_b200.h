@@ -193,6 +193,9 @@ moe_status moe_debug_mt64_chunk_host(uint64_t seed, int64_t J, int c, int64_t n,
 /* testing: the first `count` raw outputs of Rng(seed) from the device
  * generator into device memory out_dev. */
 moe_status moe_debug_mt64_device(uint64_t seed, int64_t count, uint64_t* out_dev);
+/* testing: the first `count` jitter values (float)Rng(seed).uniform(1-eps,
+ * 1+eps) (rng.cpp:41-43) from the device generator into device memory. */
+moe_status moe_debug_jitter_device(uint64_t seed, int64_t count, double eps, float* out_dev);
 
 /* ---- RNG streams (rng.cpp:15-102), host, bit-exact -------------------- */
 uint64_t moe_derive_seed_tag(uint64_t seed, const char* tag);

@@ -78,6 +78,7 @@ _SIGS = {
     "moe_debug_set_tensor_cores": (None, [C.c_int]),
     "moe_debug_mt64_chunk_host": (C.c_int, [C.c_uint64, C.c_int64, C.c_int, C.c_int64, VP]),
     "moe_debug_mt64_device": (C.c_int, [C.c_uint64, C.c_int64, VP]),
+    "moe_debug_jitter_device": (C.c_int, [C.c_uint64, C.c_int64, C.c_double, VP]),
     "moe_derive_seed_tag": (C.c_uint64, [C.c_uint64, C.c_char_p]),
     "moe_derive_seed_u64": (C.c_uint64, [C.c_uint64, C.c_uint64]),
 }

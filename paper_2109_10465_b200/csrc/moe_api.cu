@@ -1026,4 +1026,10 @@ moe_status moe_debug_mt64_device(uint64_t seed, int64_t count, uint64_t* out_dev
         MOE_CUDA_CHECK(cudaDeviceSynchronize());
     });
 }
+moe_status moe_debug_jitter_device(uint64_t seed, int64_t count, double eps, float* out_dev) {
+    return guarded(nullptr, [&] {
+        moe::launch_jitter_noise_device(seed, count, eps, out_dev, nullptr);
+        MOE_CUDA_CHECK(cudaDeviceSynchronize());
+    });
+}
 }

@@ -35,10 +35,6 @@ constexpr int N = 312, M = 156, DEG = 19937;
 constexpr uint64_t A = 0xB5026F5AA96619E9ULL, UM = 0xFFFFFFFF80000000ULL, LM = 0x7FFFFFFFULL;
 constexpr int W = (DEG + 63) / 64 + 1;  // words of a polynomial of degree < DEG (+1 spare)
 constexpr int kJumpR = 10;              // window words per lane in the jump
-// base words x[1 .. BASE]: DEG + N are needed by the jump; the sliding
-// window of the last lane reads up to 32*kJumpR + 2*kJumpR words past DEG.
-constexpr int BASE = DEG + 32 * kJumpR + 2 * kJumpR + 8;
-constexpr int kThreads = 320;
 
 __host__ __device__ __forceinline__ uint64_t temper(uint64_t z) {
     z ^= (z >> 29) & 0x5555555555555555ULL;
@@ -175,11 +171,163 @@ static const Field& field() {
     return *f;
 }
 
-// Jump table for chunk length J and P chunks: g_c = t^(311 + c*J) mod phi.
+// ---------------------------------------------------------------- device
+// One CTA per chunk, 1024 threads, four phases:
+//   1. base: x[1 .. BASE] regenerated from the seed in shared memory (every
+//      CTA redundantly; ~66 block twists, one barrier each);
+//   2. jump: the chunk's 312-word window = XOR_{i : g_c,i} x[1 + j + i];
+//   3./4. generation, warp-specialised: twister warps run the block
+//      recurrence (the serial critical path) into a ring of 312-word blocks;
+//      two emitter groups temper, convert and store alternate blocks.
+constexpr int kChunkThreads = 1024;
+constexpr int kJumpWarps = kChunkThreads / 32;
+// bits per warp in the jump, a multiple of kJumpR so each warp's range is
+// whole R-bit mask groups; bits >= DEG of g are zero.
+constexpr int kGroupsPerWarp = (DEG + kJumpWarps * kJumpR - 1) / (kJumpWarps * kJumpR);
+constexpr int kGroups = kJumpWarps * kGroupsPerWarp;
+// the last lane's register window reads up to kGroups*R + 32*R + R words
+constexpr int BASE = kGroups * kJumpR + 32 * kJumpR + kJumpR;
+constexpr int kBaseBlocks = (BASE + N) / N;  // x[312*b ..] blocks b = 1..kBaseBlocks
+constexpr int kRing = 6;                     // generation ring depth (even: 2 emitter groups)
+constexpr int kTwWarps = 10;                 // 320 twister threads (312 active)
+constexpr int kEmWarps = 11;                 // per emitter group (352 threads, 312 active)
+static_assert(kTwWarps + 2 * kEmWarps == kJumpWarps, "warp roles");
+constexpr int kBarFull = 1, kBarEmpty = kBarFull + kRing, kBarTw = kBarEmpty + kRing;
+static_assert(kBarTw <= 15, "named barriers");
+constexpr int kHand = (kTwWarps + kEmWarps) * 32;  // FULL/EMPTY participants
+
+__device__ __forceinline__ void bar_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int count) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// New word i of the next 312-block computed from the OLD block only (the
+// reference twist updates in place; words >= 156 read already-updated words
+// 0..155, which we recompute locally), so a block needs one barrier.
+template <class F>
+__device__ __forceinline__ uint64_t next_word(F o, int i) {
+    if (i < N - M) return twist(o(i), o(i + 1), o(i + M));
+    if (i < N - 1) return twist(o(i), o(i + 1), twist(o(i - (N - M)), o(i - (N - M) + 1), o(i)));
+    // i == N-1: needs new[0] and new[M-1]
+    const uint64_t n0 = twist(o(0), o(1), o(M));
+    const uint64_t nm = twist(o(M - 1), o(M), o(N - 1));
+    return twist(o(N - 1), n0, nm);
+}
+
+__global__ void __launch_bounds__(kChunkThreads, 1)
+chunk_kernel(uint64_t seed, const uint16_t* __restrict__ masks, int64_t J, int64_t count,
+             double lo, double span, float* __restrict__ noise, uint64_t* __restrict__ raw_out) {
+    extern __shared__ uint64_t sm[];
+    uint64_t* sb = sm;                                        // x[1 .. BASE]  [BASE]
+    uint64_t* ring = sb + BASE;                               // [kRing][N]
+    uint16_t* sg = reinterpret_cast<uint16_t*>(ring + kRing * N);  // g_c masks [kGroups]
+    __shared__ uint64_t x0;
+    const int c = blockIdx.x;
+    const int64_t q0 = static_cast<int64_t>(c) * J;
+    if (q0 >= count) return;
+    const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31;
+    for (int i = t; i < kGroups; i += kChunkThreads) sg[i] = masks[static_cast<int64_t>(c) * kGroups + i];
+    for (int i = t; i < N; i += kChunkThreads) ring[i] = 0;
+    // ---- 1. base sequence (init_genrand64 + block twists)
+    if (t == 0) {
+        uint64_t v = seed;
+        x0 = v;
+        for (int i = 1; i < N; ++i) {
+            v = 6364136223846793005ULL * (v ^ (v >> 62)) + static_cast<uint64_t>(i);
+            sb[i - 1] = v;
+        }
+    }
+    __syncthreads();
+    for (int b = 1; b <= kBaseBlocks; ++b) {
+        if (t < N) {
+            const int k0 = (b - 1) * N;  // previous block x[k0 .. k0+311]
+            const uint64_t v = next_word([&](int i) { return k0 + i == 0 ? x0 : sb[k0 + i - 1]; }, t);
+            const int k = b * N + t;
+            if (k <= BASE) sb[k - 1] = v;
+        }
+        __syncthreads();
+    }
+    // ---- 2. jump.  Warp w takes mask groups [w*G, (w+1)*G); lane l owns
+    // R consecutive window words j = l*R + r in registers and slides a
+    // register window over the base, so each bit costs one shared load plus
+    // (if set) R XORs; the mask is warp-uniform (no divergence).  Partial
+    // windows meet in ring slot 0 via shared atomic XOR.
+    {
+        constexpr int R = kJumpR;
+        const int i0 = warp * kGroupsPerWarp * R;
+        const int j0 = lane * R;
+        uint64_t acc[R], win[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            acc[r] = 0;
+            win[r] = sb[i0 + j0 + r];
+        }
+        const uint16_t* gm = sg + warp * kGroupsPerWarp;
+        for (int g = 0; g < kGroupsPerWarp; ++g) {
+            const int i = i0 + g * R;
+            const uint32_t m = gm[g];
+#pragma unroll
+            for (int s = 0; s < R; ++s) {
+                if (m & (1u << s)) {
+#pragma unroll
+                    for (int r = 0; r < R; ++r) acc[r] ^= win[(s + r) % R];
+                }
+                win[s] = sb[i + j0 + R + s];
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+            if (j0 + r < N) atomicXor(reinterpret_cast<unsigned long long*>(&ring[j0 + r]), acc[r]);
+    }
+    __syncthreads();
+    // ---- 3./4. generation.  Block b lives in ring slot b % kRing and is
+    // emitted by group b % 2 (slot parity == group).  Named barriers:
+    // FULL[slot] (twisters arrive, the slot's group syncs), EMPTY[slot] (the
+    // group arrives, twisters sync), TW (twisters only).  Block 0 (the jump
+    // window) is already in slot 0.
+    const int64_t n = min(J, count - q0);
+    const int64_t nblk = (n + N - 1) / N;
+    if (warp < kTwWarps) {
+        bar_arrive(kBarFull + 0, kHand);
+        for (int64_t b = 1; b < nblk; ++b) {
+            const int slot = static_cast<int>(b % kRing);
+            if (b >= kRing) bar_sync(kBarEmpty + slot, kHand);  // slot's old block consumed
+            const uint64_t* prev = ring + static_cast<int>((b - 1) % kRing) * N;
+            if (t < N) ring[slot * N + t] = next_word([&](int i) { return prev[i]; }, t);
+            bar_sync(kBarTw, kTwWarps * 32);  // whole block written before it is the next input
+            bar_arrive(kBarFull + slot, kHand);
+        }
+    } else {
+        const int grp = (warp - kTwWarps) / kEmWarps;
+        const int u = t - kTwWarps * 32 - grp * kEmWarps * 32;
+        for (int64_t b = grp; b < nblk; b += 2) {
+            const int slot = static_cast<int>(b % kRing);
+            bar_sync(kBarFull + slot, kHand);
+            const int64_t q = b * N + u;
+            if (u < N && q < n) {
+                const uint64_t out = temper(ring[slot * N + u]);
+                if (raw_out) raw_out[q0 + q] = out;
+                if (noise) {
+                    // lo + (hi - lo) * u53 * 2^-53 in f64 without contraction,
+                    // exactly as the reference (rng.cpp:36-43)
+                    const double uu = static_cast<double>(out >> 11) * 0x1.0p-53;
+                    noise[q0 + q] = static_cast<float>(__dadd_rn(lo, __dmul_rn(span, uu)));
+                }
+            }
+            if (b + kRing < nblk) bar_arrive(kBarEmpty + slot, kHand);
+        }
+    }
+}
+
+// Jump masks for chunk length J and P chunks: g_c = t^(311 + c*J) mod phi,
+// repacked as kJumpR-bit groups (one uint16 per group) for the device loop.
 struct Table {
     int64_t J = 0;
     int P = 0;
-    uint64_t* dev = nullptr;  // [P][W]
+    uint16_t* dev = nullptr;  // [P][kGroups]
 };
 
 static std::mutex g_mu;
@@ -191,184 +339,21 @@ static const Table& table_for(int64_t J, int P) {
     auto it = g_tables.find(key);
     if (it != g_tables.end()) return it->second;
     const Field& F = field();
-    std::vector<uint64_t> host(static_cast<size_t>(P) * W);
+    std::vector<uint16_t> host(static_cast<size_t>(P) * kGroups, 0);
     Poly g = F.pow_t(311);
     const Poly step = F.pow_t(static_cast<uint64_t>(J));
     for (int c = 0; c < P; ++c) {
-        std::memcpy(host.data() + static_cast<size_t>(c) * W, g.data(), sizeof(uint64_t) * W);
+        uint16_t* dst = host.data() + static_cast<size_t>(c) * kGroups;
+        for (long i = 0; i < DEG; ++i)
+            if (getbit(g, i)) dst[i / kJumpR] |= static_cast<uint16_t>(1u << (i % kJumpR));
         if (c + 1 < P) g = F.mul(g, step);
     }
     Table t;
     t.J = J;
     t.P = P;
-    MOE_CUDA_CHECK(cudaMalloc(&t.dev, sizeof(uint64_t) * host.size()));
-    MOE_CUDA_CHECK(cudaMemcpy(t.dev, host.data(), sizeof(uint64_t) * host.size(), cudaMemcpyHostToDevice));
+    MOE_CUDA_CHECK(cudaMalloc(&t.dev, sizeof(uint16_t) * host.size()));
+    MOE_CUDA_CHECK(cudaMemcpy(t.dev, host.data(), sizeof(uint16_t) * host.size(), cudaMemcpyHostToDevice));
     return g_tables.emplace(key, t).first->second;
-}
-
-// ---------------------------------------------------------------- device
-// Base sequence x[1 .. BASE] from the seed (single CTA).
-__global__ void __launch_bounds__(kThreads) base_kernel(uint64_t seed, uint64_t* __restrict__ base) {
-    __shared__ uint64_t s[N];
-    if (threadIdx.x == 0) {
-        uint64_t v = seed;
-        s[0] = v;
-        for (int i = 1; i < N; ++i) {
-            v = 6364136223846793005ULL * (v ^ (v >> 62)) + static_cast<uint64_t>(i);
-            s[i] = v;
-        }
-    }
-    __syncthreads();
-    // x[1..311]
-    for (int i = threadIdx.x + 1; i < N; i += blockDim.x) base[i - 1] = s[i];
-    // twist blocks: x[312*b .. 312*b + 311]
-    const int nblk = (BASE + 1 + N - 1) / N;  // enough blocks to cover x[BASE]
-    for (int b = 1; b <= nblk; ++b) {
-        const int i = threadIdx.x;
-        uint64_t v0 = 0;
-        if (i < N - M) v0 = twist(s[i], s[i + 1], s[i + M]);
-        __syncthreads();
-        if (i < N - M) s[i] = v0;
-        __syncthreads();
-        uint64_t v1 = 0;
-        if (i >= N - M && i < N - 1) v1 = twist(s[i], s[i + 1], s[i + M - N]);
-        __syncthreads();
-        if (i >= N - M && i < N - 1) s[i] = v1;
-        __syncthreads();
-        if (i == N - 1) s[N - 1] = twist(s[N - 1], s[0], s[M - 1]);
-        __syncthreads();
-        for (int q = threadIdx.x; q < N; q += blockDim.x) {
-            const long k = static_cast<long>(b) * N + q;  // raw index
-            if (k - 1 < BASE) base[k - 1] = s[q];
-        }
-        __syncthreads();
-    }
-}
-
-// New word i of the next 312-block computed from the OLD block only (the
-// reference twist updates in place; words >= 156 read already-updated words
-// 0..155, which we recompute locally), so a block needs one barrier.
-__device__ __forceinline__ uint64_t next_word(const uint64_t* __restrict__ o, int i) {
-    if (i < N - M) return twist(o[i], o[i + 1], o[i + M]);
-    if (i < N - 1) return twist(o[i], o[i + 1], twist(o[i - (N - M)], o[i - (N - M) + 1], o[i]));
-    // i == N-1: needs new[0] and new[M-1]
-    const uint64_t n0 = twist(o[0], o[1], o[M]);
-    const uint64_t nm = twist(o[M - 1], o[M], o[N - 1]);
-    return twist(o[N - 1], n0, nm);
-}
-
-constexpr int kChunkThreads = 2 * N + 16;  // 640 = 20 warps
-constexpr int kRing = 4;                    // generation ring depth (312-word blocks)
-constexpr int kBarFull = 1, kBarEmpty = kBarFull + kRing, kBarTw = kBarEmpty + kRing;
-
-__device__ __forceinline__ void bar_sync(int id, int count) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-__device__ __forceinline__ void bar_arrive(int id, int count) {
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-
-// One CTA per chunk: jump to the chunk's window, then generate J outputs.
-__global__ void __launch_bounds__(kChunkThreads, 1)
-chunk_kernel(const uint64_t* __restrict__ base, const uint64_t* __restrict__ jump, int64_t J,
-             int64_t count, double lo, double span, float* __restrict__ noise,
-             uint64_t* __restrict__ raw_out) {
-    extern __shared__ uint64_t sm[];
-    uint64_t* sb = sm;              // base [BASE]
-    uint64_t* sg = sm + BASE;       // g_c  [W]
-    uint64_t* s0 = sg + W;          // ping [N]
-    const int c = blockIdx.x;
-    const int64_t q0 = static_cast<int64_t>(c) * J;
-    if (q0 >= count) return;
-    for (int i = threadIdx.x; i < BASE; i += blockDim.x) sb[i] = base[i];
-    for (int i = threadIdx.x; i < W; i += blockDim.x) sg[i] = jump[static_cast<int64_t>(c) * W + i];
-    __syncthreads();
-    // window word j = XOR_{i : g_i} base[j + i].  Warp w takes bit range
-    // [w*L, (w+1)*L) of g; lane l owns R consecutive words j = l*R + r in
-    // registers and slides a register window over base, so each bit costs one
-    // shared load plus R predicated XORs (g's bit is warp-uniform: no
-    // divergence).  Partial windows meet in shared memory via atomic XOR.
-    const int t = threadIdx.x;
-    const int warp = t >> 5, lane = t & 31;
-    for (int i = t; i < N; i += blockDim.x) s0[i] = 0;
-    __syncthreads();
-    {
-        constexpr int R = kJumpR;
-        const int nwarps = blockDim.x >> 5;
-        const int L = (DEG + nwarps - 1) / nwarps;
-        const int i0 = warp * L, i1 = min(DEG, i0 + L);
-        const int j0 = lane * R;
-        uint64_t acc[R], win[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            acc[r] = 0;
-            win[r] = sb[i0 + j0 + r];
-        }
-        for (int i = i0; i < i1; i += R) {
-#pragma unroll
-            for (int s = 0; s < R; ++s) {
-                const int ii = i + s;
-                if (ii < i1 && ((sg[ii >> 6] >> (ii & 63)) & 1ULL)) {
-#pragma unroll
-                    for (int r = 0; r < R; ++r) acc[r] ^= win[(s + r) % R];
-                }
-                win[s] = sb[i + j0 + R + s];
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-            if (j0 + r < N) atomicXor(reinterpret_cast<unsigned long long*>(&s0[j0 + r]), acc[r]);
-    }
-    __syncthreads();
-    // Generation, warp-specialised.  Warps 0-9 ("twisters") run only the block
-    // recurrence — the serial critical path — into a kRing-deep ring of
-    // 312-word blocks; warps 10-19 ("emitters") temper, convert and store each
-    // completed block.  Named barriers: FULL[slot] (twisters arrive, emitters
-    // wait), EMPTY[slot] (emitters arrive, twisters wait), TW (twisters only).
-    // Block 0 (the jump window) is already in ring slot 0.
-    const int64_t n = min(J, count - q0);
-    const int64_t nblk = (n + N - 1) / N;
-    uint64_t* ring = s0;  // [kRing][N] (s0 and the following smem)
-    constexpr int kTw = 10 * 32;
-    const bool twister = t < kTw;
-    if (twister) {
-        bar_arrive(kBarFull + 0, kChunkThreads);
-        for (int64_t b = 1; b < nblk; ++b) {
-            const int slot = static_cast<int>(b % kRing);
-            if (b >= kRing) bar_sync(kBarEmpty + slot, kChunkThreads);  // slot's old block consumed
-            const uint64_t* prev = ring + static_cast<int>((b - 1) % kRing) * N;
-            uint64_t v = 0;
-            if (t < N) v = next_word(prev, t);
-            if (t < N) ring[slot * N + t] = v;
-            bar_sync(kBarTw, kTw);  // whole block written before it is the next input
-            bar_arrive(kBarFull + slot, kChunkThreads);
-        }
-    } else {
-        const int u = t - kTw;
-        for (int64_t b = 0; b < nblk; ++b) {
-            const int slot = static_cast<int>(b % kRing);
-            bar_sync(kBarFull + slot, kChunkThreads);
-            const int64_t q = b * N + u;
-            if (u < N && q < n) {
-                const uint64_t out = temper(ring[slot * N + u]);
-                if (raw_out) raw_out[q0 + q] = out;
-                if (noise) {
-                    const double uu = static_cast<double>(out >> 11) * 0x1.0p-53;
-                    noise[q0 + q] = static_cast<float>(lo + span * uu);
-                }
-            }
-            if (b + kRing < nblk) bar_arrive(kBarEmpty + slot, kChunkThreads);
-        }
-    }
-}
-
-struct Scratch {
-    uint64_t* base = nullptr;
-    Scratch() { MOE_CUDA_CHECK(cudaMalloc(&base, sizeof(uint64_t) * BASE)); }
-};
-static Scratch& scratch() {
-    static Scratch* s = new Scratch();
-    return *s;
 }
 
 void generate(uint64_t seed, int64_t count, double lo, double hi, float* noise, uint64_t* raw,
@@ -377,21 +362,19 @@ void generate(uint64_t seed, int64_t count, double lo, double hi, float* noise, 
     const int P = static_cast<int>(std::min<int64_t>(kNumSMs, ceil_div(count, 4096)));
     const int64_t J = ceil_div(count, P);
     const Table& tab = table_for(J, P);
-    Scratch& sc = scratch();
-    base_kernel<<<1, kThreads, 0, st>>>(seed, sc.base);
-    MOE_LAUNCH_CHECK();
-    const size_t smem = sizeof(uint64_t) * (BASE + W + kRing * N);
+    const size_t smem = sizeof(uint64_t) * (BASE + kRing * N) + sizeof(uint16_t) * kGroups;
     static bool attr = false;
     if (!attr) {
         MOE_CUDA_CHECK(cudaFuncSetAttribute(chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             static_cast<int>(smem)));
         attr = true;
     }
-    chunk_kernel<<<P, kChunkThreads, smem, st>>>(sc.base, tab.dev, J, count, lo, hi - lo, noise, raw);
+    chunk_kernel<<<P, kChunkThreads, smem, st>>>(seed, tab.dev, J, count, lo, hi - lo, noise, raw);
     MOE_LAUNCH_CHECK();
 }
 
 }  // namespace mt
+
 
 bool launch_jitter_noise_device(uint64_t seed, int64_t count, double eps, float* noise,
                                 cudaStream_t st) {

@@ -38,3 +38,21 @@ def test_device_stream_matches_reference(count):
     ref = O.restatement().mt64(seed, count)
     bad = np.nonzero(got != ref)[0]
     assert bad.size == 0, (bad[:5], count)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("count,eps", [(5000, 0.01), (16_777_216, 0.01), (1_000_003, 0.25)])
+def test_device_jitter_values_bit_exact(count, eps):
+    """noise = (float)(lo + (hi - lo) * ((x >> 11) * 2^-53)) with the f64
+    arithmetic of rng.cpp:36-43 (no fused multiply-add), then rounded to fp32."""
+    import torch
+    from paper_2109_10465_b200 import _lib
+    seed = O.restatement().derive_seed(7, "jitter")
+    out = torch.empty(count, dtype=torch.float32, device="cuda")
+    assert _lib.load().moe_debug_jitter_device(seed, count, eps, C.c_void_p(out.data_ptr())) == 0
+    raw = O.restatement().mt64(seed, count)
+    lo, hi = 1.0 - eps, 1.0 + eps
+    u = (raw >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    ref = (lo + (hi - lo) * u).astype(np.float32)
+    got = out.cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
