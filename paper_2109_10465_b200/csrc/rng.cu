@@ -18,6 +18,8 @@
 //
 // The jump polynomials depend only on (J, P) — not on the seed — and are
 // computed on the host once per geometry and cached.
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -172,14 +174,17 @@ static const Field& field() {
 }
 
 // ---------------------------------------------------------------- device
-// One CTA per chunk, 1024 threads, four phases:
+// One CTA per chunk, 768 threads, three phases:
 //   1. base: x[1 .. BASE] regenerated from the seed in shared memory (every
-//      CTA redundantly; ~66 block twists, one barrier each);
-//   2. jump: the chunk's 312-word window = XOR_{i : g_c,i} x[1 + j + i];
-//   3./4. generation, warp-specialised: twister warps run the block
-//      recurrence (the serial critical path) into a ring of 312-word blocks;
-//      two emitter groups temper, convert and store alternate blocks.
-constexpr int kChunkThreads = 1024;
+//      CTA redundantly) by the warp twister below;
+//   2. jump: the chunk's 312-word window = XOR_{i : g_c,i} x[1 + j + i], all
+//      32 warps;
+//   3. generation: warp 0 runs the block recurrence (the serial critical
+//      path) entirely in registers and publishes each 312-word block into a
+//      shared-memory ring (mbarrier full/empty per slot); 18 emitter warps
+//      (those not on warp 0's SM sub-partition) temper, convert and store
+//      whole blocks, round-robin.
+constexpr int kChunkThreads = 768;
 constexpr int kJumpWarps = kChunkThreads / 32;
 // bits per warp in the jump, a multiple of kJumpR so each warp's range is
 // whole R-bit mask groups; bits >= DEG of g are zero.
@@ -188,82 +193,160 @@ constexpr int kGroups = kJumpWarps * kGroupsPerWarp;
 // the last lane's register window reads up to kGroups*R + 32*R + R words
 constexpr int BASE = kGroups * kJumpR + 32 * kJumpR + kJumpR;
 constexpr int kBaseBlocks = (BASE + N) / N;  // x[312*b ..] blocks b = 1..kBaseBlocks
-constexpr int kRing = 6;                     // generation ring depth (even: 2 emitter groups)
-constexpr int kTwWarps = 10;                 // 320 twister threads (312 active)
-constexpr int kEmWarps = 11;                 // per emitter group (352 threads, 312 active)
-static_assert(kTwWarps + 2 * kEmWarps == kJumpWarps, "warp roles");
-constexpr int kBarFull = 1, kBarEmpty = kBarFull + kRing, kBarTw = kBarEmpty + kRing;
-static_assert(kBarTw <= 15, "named barriers");
-constexpr int kHand = (kTwWarps + kEmWarps) * 32;  // FULL/EMPTY participants
+constexpr int kEmitters = kJumpWarps / 4 * 3;  // warps w with w % 4 != 0
+constexpr int kRing = 2 * kEmitters;         // ring slots (a multiple of kEmitters)
+static_assert(kRing * N <= BASE, "ring reuses the base region after the jump");
 
-__device__ __forceinline__ void bar_sync(int id, int count) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void bar_arrive(int id, int count) {
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
 }
 
-// New word i of the next 312-block computed from the OLD block only (the
-// reference twist updates in place; words >= 156 read already-updated words
-// 0..155, which we recompute locally), so a block needs one barrier.
-template <class F>
-__device__ __forceinline__ uint64_t next_word(F o, int i) {
-    if (i < N - M) return twist(o(i), o(i + 1), o(i + M));
-    if (i < N - 1) return twist(o(i), o(i + 1), twist(o(i - (N - M)), o(i - (N - M) + 1), o(i)));
-    // i == N-1: needs new[0] and new[M-1]
-    const uint64_t n0 = twist(o(0), o(1), o(M));
-    const uint64_t nm = twist(o(M - 1), o(M), o(N - 1));
-    return twist(o(N - 1), n0, nm);
+// twist(lo, hi, mid) = mid ^ mix(lo, hi)
+__device__ __forceinline__ uint64_t mix(uint64_t lo_word, uint64_t hi_word) {
+    const uint64_t y = (lo_word & UM) | (hi_word & LM);
+    return (y >> 1) ^ ((y & 1ULL) ? A : 0ULL);
+}
+
+// One warp advances the 312-word state by one block, in registers.  Lane l
+// holds the word pairs j = 5l + r and j + 156 (r < 5, j < 156): A[r] = o[j],
+// B[r] = o[j + 156].  Then both halves of the block twist are lane-local:
+//   new[j]       = mix(o[j], o[j+1])         ^ o[j+156]   = mix(A[r], A[r+1]) ^ B[r]
+//   new[j + 156] = mix(o[j+156], o[j+157])   ^ new[j]     = mix(B[r], B[r+1]) ^ newA[r]
+// with the r+1 = 5 neighbours from lane l+1, and lane 31 (j = 155, 311 only)
+// taking o[156] and new[0] from lane 0.
+__device__ __forceinline__ void warp_twist(uint64_t (&Aw)[5], uint64_t (&Bw)[5], int lane) {
+    const uint64_t a_next = __shfl_down_sync(0xffffffffu, Aw[0], 1);
+    const uint64_t b_next = __shfl_down_sync(0xffffffffu, Bw[0], 1);
+    const uint64_t o156 = __shfl_sync(0xffffffffu, Bw[0], 0);
+    uint64_t nA[5];
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+        uint64_t hi = r < 4 ? Aw[r + 1] : a_next;
+        if (r == 0 && lane == 31) hi = o156;  // j = 155
+        nA[r] = mix(Aw[r], hi) ^ Bw[r];
+    }
+    const uint64_t new0 = __shfl_sync(0xffffffffu, nA[0], 0);
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+        uint64_t hi = r < 4 ? Bw[r + 1] : b_next;
+        if (r == 0 && lane == 31) hi = new0;  // j = 311
+        Bw[r] = mix(Bw[r], hi) ^ nA[r];
+        Aw[r] = nA[r];
+    }
 }
 
 __global__ void __launch_bounds__(kChunkThreads, 1)
 chunk_kernel(uint64_t seed, const uint16_t* __restrict__ masks, int64_t J, int64_t count,
-             double lo, double span, float* __restrict__ noise, uint64_t* __restrict__ raw_out) {
+             double lo, double span, float* __restrict__ noise, uint64_t* __restrict__ raw_out,
+             unsigned long long* __restrict__ tdbg) {
     extern __shared__ uint64_t sm[];
-    uint64_t* sb = sm;                                        // x[1 .. BASE]  [BASE]
-    uint64_t* ring = sb + BASE;                               // [kRing][N]
-    uint16_t* sg = reinterpret_cast<uint16_t*>(ring + kRing * N);  // g_c masks [kGroups]
-    __shared__ uint64_t x0;
+    uint64_t* sb = sm;                                   // x[1 .. BASE]; later the ring [kRing][N]
+    uint64_t* win = sb + BASE;                           // jump result [N]
+    uint64_t* full = win + N;                            // mbarriers [kRing]
+    uint64_t* empty = full + kRing;                      // mbarriers [kRing]
+    uint16_t* sg = reinterpret_cast<uint16_t*>(empty + kRing);  // g_c masks [kGroups]
+    uint64_t* ring = sb;
     const int c = blockIdx.x;
     const int64_t q0 = static_cast<int64_t>(c) * J;
     if (q0 >= count) return;
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
+    auto stamp = [&](int k) {  // debug phase timeline (MOE_B200_RNG_TIMING)
+        if (tdbg) {
+            unsigned long long ns;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+            tdbg[c * 8 + k] = ns;
+        }
+    };
+    if (t == 0) stamp(0);
     for (int i = t; i < kGroups; i += kChunkThreads) sg[i] = masks[static_cast<int64_t>(c) * kGroups + i];
-    for (int i = t; i < N; i += kChunkThreads) ring[i] = 0;
-    // ---- 1. base sequence (init_genrand64 + block twists)
+    for (int i = t; i < N; i += kChunkThreads) win[i] = 0;
     if (t == 0) {
-        uint64_t v = seed;
-        x0 = v;
-        for (int i = 1; i < N; ++i) {
-            v = 6364136223846793005ULL * (v ^ (v >> 62)) + static_cast<uint64_t>(i);
-            sb[i - 1] = v;
+        for (int i = 0; i < kRing; ++i) {
+            mbar_init(&full[i], 32);   // all twister lanes arrive
+            mbar_init(&empty[i], 32);  // all lanes of the slot's emitter arrive
+        }
+    }
+    // ---- 1. base sequence: init_genrand64 (thread 0), then warp 0 twists
+    // blocks b = 1.. in registers and writes x[312b + j] to sb[312b + j - 1].
+    if (warp == 0) {
+        if (lane == 0) {
+            uint64_t v = seed;
+            win[0] = v;  // x[0] (scratch; win is cleared again below)
+            for (int i = 1; i < N; ++i) {
+                v = 6364136223846793005ULL * (v ^ (v >> 62)) + static_cast<uint64_t>(i);
+                sb[i - 1] = v;
+            }
+        }
+        __syncwarp();
+        uint64_t Aw[5], Bw[5];
+#pragma unroll
+        for (int r = 0; r < 5; ++r) {
+            const int j = lane * 5 + r;
+            Aw[r] = j == 0 ? win[0] : (j < M ? sb[j - 1] : 0);
+            Bw[r] = j < M ? sb[j + M - 1] : 0;
+        }
+        __syncwarp();
+        if (lane == 0) win[0] = 0;
+        for (int b = 1; b <= kBaseBlocks; ++b) {
+            warp_twist(Aw, Bw, lane);
+#pragma unroll
+            for (int r = 0; r < 5; ++r) {
+                const int j = lane * 5 + r;
+                const int k = b * N + j;
+                if (j < M) {
+                    if (k <= BASE) sb[k - 1] = Aw[r];
+                    if (k + M <= BASE) sb[k + M - 1] = Bw[r];
+                }
+            }
         }
     }
     __syncthreads();
-    for (int b = 1; b <= kBaseBlocks; ++b) {
-        if (t < N) {
-            const int k0 = (b - 1) * N;  // previous block x[k0 .. k0+311]
-            const uint64_t v = next_word([&](int i) { return k0 + i == 0 ? x0 : sb[k0 + i - 1]; }, t);
-            const int k = b * N + t;
-            if (k <= BASE) sb[k - 1] = v;
-        }
-        __syncthreads();
-    }
+    if (t == 0) stamp(1);
     // ---- 2. jump.  Warp w takes mask groups [w*G, (w+1)*G); lane l owns
     // R consecutive window words j = l*R + r in registers and slides a
     // register window over the base, so each bit costs one shared load plus
     // (if set) R XORs; the mask is warp-uniform (no divergence).  Partial
-    // windows meet in ring slot 0 via shared atomic XOR.
+    // windows meet in `win` via shared atomic XOR.
     {
         constexpr int R = kJumpR;
         const int i0 = warp * kGroupsPerWarp * R;
         const int j0 = lane * R;
-        uint64_t acc[R], win[R];
+        uint64_t acc[R], wr[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             acc[r] = 0;
-            win[r] = sb[i0 + j0 + r];
+            wr[r] = sb[i0 + j0 + r];
         }
         const uint16_t* gm = sg + warp * kGroupsPerWarp;
         for (int g = 0; g < kGroupsPerWarp; ++g) {
@@ -273,52 +356,79 @@ chunk_kernel(uint64_t seed, const uint16_t* __restrict__ masks, int64_t J, int64
             for (int s = 0; s < R; ++s) {
                 if (m & (1u << s)) {
 #pragma unroll
-                    for (int r = 0; r < R; ++r) acc[r] ^= win[(s + r) % R];
+                    for (int r = 0; r < R; ++r) acc[r] ^= wr[(s + r) % R];
                 }
-                win[s] = sb[i + j0 + R + s];
+                wr[s] = sb[i + j0 + R + s];
             }
         }
 #pragma unroll
         for (int r = 0; r < R; ++r)
-            if (j0 + r < N) atomicXor(reinterpret_cast<unsigned long long*>(&ring[j0 + r]), acc[r]);
+            if (j0 + r < N) atomicXor(reinterpret_cast<unsigned long long*>(&win[j0 + r]), acc[r]);
     }
-    __syncthreads();
-    // ---- 3./4. generation.  Block b lives in ring slot b % kRing and is
-    // emitted by group b % 2 (slot parity == group).  Named barriers:
-    // FULL[slot] (twisters arrive, the slot's group syncs), EMPTY[slot] (the
-    // group arrives, twisters sync), TW (twisters only).  Block 0 (the jump
-    // window) is already in slot 0.
+    __syncthreads();  // base no longer read: its space becomes the ring
+    if (t == 0) stamp(2);
+    // ---- 3. generation.  Block b -> ring slot b % kRing, emitter b % kEmitters.
     const int64_t n = min(J, count - q0);
-    const int64_t nblk = (n + N - 1) / N;
-    if (warp < kTwWarps) {
-        bar_arrive(kBarFull + 0, kHand);
-        for (int64_t b = 1; b < nblk; ++b) {
-            const int slot = static_cast<int>(b % kRing);
-            if (b >= kRing) bar_sync(kBarEmpty + slot, kHand);  // slot's old block consumed
-            const uint64_t* prev = ring + static_cast<int>((b - 1) % kRing) * N;
-            if (t < N) ring[slot * N + t] = next_word([&](int i) { return prev[i]; }, t);
-            bar_sync(kBarTw, kTwWarps * 32);  // whole block written before it is the next input
-            bar_arrive(kBarFull + slot, kHand);
+    const int nblk = static_cast<int>((n + N - 1) / N);
+    if (warp == 0) {
+        uint64_t Aw[5], Bw[5];
+#pragma unroll
+        for (int r = 0; r < 5; ++r) {
+            const int j = lane * 5 + r;
+            Aw[r] = j < M ? win[j] : 0;
+            Bw[r] = j < M ? win[j + M] : 0;
         }
-    } else {
-        const int grp = (warp - kTwWarps) / kEmWarps;
-        const int u = t - kTwWarps * 32 - grp * kEmWarps * 32;
-        for (int64_t b = grp; b < nblk; b += 2) {
-            const int slot = static_cast<int>(b % kRing);
-            bar_sync(kBarFull + slot, kHand);
-            const int64_t q = b * N + u;
-            if (u < N && q < n) {
-                const uint64_t out = temper(ring[slot * N + u]);
-                if (raw_out) raw_out[q0 + q] = out;
-                if (noise) {
-                    // lo + (hi - lo) * u53 * 2^-53 in f64 without contraction,
-                    // exactly as the reference (rng.cpp:36-43)
-                    const double uu = static_cast<double>(out >> 11) * 0x1.0p-53;
-                    noise[q0 + q] = static_cast<float>(__dadd_rn(lo, __dmul_rn(span, uu)));
+        // Every lane arrives on full[] (count 32), one block late, so the
+        // release never waits on stores still in flight; the empty[] check
+        // for the next slot is issued before the twist so its latency hides.
+        int slot = 0, prev = -1;
+        uint32_t lap = 0;
+        for (int b = 0; b < nblk; ++b) {
+            const bool ready = b < kRing || mbar_test(&empty[slot], lap ^ 1u);
+            if (b > 0) warp_twist(Aw, Bw, lane);
+            if (prev >= 0) mbar_arrive(&full[prev]);
+            if (!ready) mbar_wait(&empty[slot], lap ^ 1u);
+            uint64_t* dst = ring + slot * N + lane * 5;
+#pragma unroll
+            for (int r = 0; r < 5; ++r) {
+                if (lane * 5 + r < M) {
+                    dst[r] = Aw[r];
+                    dst[r + M] = Bw[r];
                 }
             }
-            if (b + kRing < nblk) bar_arrive(kBarEmpty + slot, kHand);
+            prev = slot;
+            if (++slot == kRing) {
+                slot = 0;
+                lap ^= 1u;
+            }
         }
+        if (prev >= 0) mbar_arrive(&full[prev]);
+        if (lane == 0) stamp(3);
+    } else if (warp & 3) {
+        const int k = (warp >> 2) * 3 + (warp & 3) - 1;  // 0 .. kEmitters-1
+        for (int b = k; b < nblk; b += kEmitters) {
+            const int slot = b % kRing;
+            mbar_wait(&full[slot], (b / kRing) & 1);
+            const uint64_t* src = ring + slot * N;
+            const int64_t qb = static_cast<int64_t>(b) * N;
+#pragma unroll
+            for (int it = 0; it < (N + 31) / 32; ++it) {
+                const int i = lane + 32 * it;
+                const int64_t q = qb + i;
+                if (i < N && q < n) {
+                    const uint64_t out = temper(src[i]);
+                    if (raw_out) raw_out[q0 + q] = out;
+                    if (noise) {
+                        // lo + (hi - lo) * u53 * 2^-53 in f64 without
+                        // contraction, exactly as the reference (rng.cpp:36-43)
+                        const double uu = static_cast<double>(out >> 11) * 0x1.0p-53;
+                        noise[q0 + q] = static_cast<float>(__dadd_rn(lo, __dmul_rn(span, uu)));
+                    }
+                }
+            }
+            mbar_arrive(&empty[slot]);
+        }
+        if (lane == 0 && warp == 1) stamp(4);
     }
 }
 
@@ -362,15 +472,30 @@ void generate(uint64_t seed, int64_t count, double lo, double hi, float* noise, 
     const int P = static_cast<int>(std::min<int64_t>(kNumSMs, ceil_div(count, 4096)));
     const int64_t J = ceil_div(count, P);
     const Table& tab = table_for(J, P);
-    const size_t smem = sizeof(uint64_t) * (BASE + kRing * N) + sizeof(uint16_t) * kGroups;
+    const size_t smem = sizeof(uint64_t) * (BASE + N + 2 * kRing) + sizeof(uint16_t) * kGroups;
     static bool attr = false;
     if (!attr) {
         MOE_CUDA_CHECK(cudaFuncSetAttribute(chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             static_cast<int>(smem)));
         attr = true;
     }
-    chunk_kernel<<<P, kChunkThreads, smem, st>>>(seed, tab.dev, J, count, lo, hi - lo, noise, raw);
+    static unsigned long long* tdbg = nullptr;
+    static const bool timing = std::getenv("MOE_B200_RNG_TIMING") != nullptr;
+    if (timing && !tdbg) MOE_CUDA_CHECK(cudaMalloc(&tdbg, sizeof(unsigned long long) * 8 * kNumSMs));
+    chunk_kernel<<<P, kChunkThreads, smem, st>>>(seed, tab.dev, J, count, lo, hi - lo, noise, raw,
+                                                 timing ? tdbg : nullptr);
     MOE_LAUNCH_CHECK();
+    if (timing) {  // debug: per-phase times averaged over CTAs (synchronises)
+        std::vector<unsigned long long> h(8 * static_cast<size_t>(P));
+        MOE_CUDA_CHECK(cudaStreamSynchronize(st));
+        MOE_CUDA_CHECK(cudaMemcpy(h.data(), tdbg, sizeof(unsigned long long) * h.size(),
+                                  cudaMemcpyDeviceToHost));
+        double ph[4] = {0, 0, 0, 0};
+        for (int c = 0; c < P; ++c)
+            for (int k = 0; k < 4; ++k) ph[k] += double(static_cast<long long>(h[c * 8 + k + 1] - h[c * 8 + k])) / P;
+        std::fprintf(stderr, "[rng] P=%d J=%lld base %.1f us, jump %.1f us, twister %.1f us, emit tail %.1f us\n",
+                     P, static_cast<long long>(J), ph[0] / 1e3, ph[1] / 1e3, ph[2] / 1e3, ph[3] / 1e3);
+    }
 }
 
 }  // namespace mt
