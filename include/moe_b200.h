@@ -197,6 +197,18 @@ moe_status moe_debug_mt64_device(uint64_t seed, int64_t count, uint64_t* out_dev
  * 1+eps) (rng.cpp:41-43) from the device generator into device memory. */
 moe_status moe_debug_jitter_device(uint64_t seed, int64_t count, double eps, float* out_dev);
 
+/* testing: the tensor-core gate GEMMs (gate_tc.cu) on device buffers; x,
+ * dX, dy, dx, dres are bf16.  logits_part is [splits][T][E]; dw_part is
+ * [splits][d][E]. */
+moe_status moe_debug_gate_tc_logits(const void* x, const float* noise, const float* gate_w,
+                                    float* logits_part, int64_t T, int d, int E, int splits);
+moe_status moe_debug_gate_tc_dw(const void* x, const float* noise, const float* dL, float* dw_part,
+                                int64_t T, int d, int E, int splits);
+moe_status moe_debug_gate_tc_dx(int64_t T, int d, int E, int K, int cap_pad, const float* dL,
+                                const float* gate_w, const float* noise, const void* dX,
+                                const int32_t* choice, const int32_t* pos, const void* dy,
+                                int residual_is_x, void* dx, void* dres);
+
 /* ---- RNG streams (rng.cpp:15-102), host, bit-exact -------------------- */
 uint64_t moe_derive_seed_tag(uint64_t seed, const char* tag);
 uint64_t moe_derive_seed_u64(uint64_t seed, uint64_t salt);

@@ -110,7 +110,10 @@ __global__ void transpose_kernel(const float* __restrict__ wg, float* __restrict
 }
 
 // ---- dx: CTA = 64 tokens x 256 columns, thread = 8 tokens x 8 columns;
-// E staged in chunks of 16 rows of WgT.
+// E staged in chunks of 16 rows of WgT.  With dxg_out set the kernel only
+// writes dxg_out = (dL Wg^T) * noise in fp32 (the dispatch-backward gather is
+// then done by dx_assemble); this variant runs on the side stream next to the
+// expert weight-gradient GEMMs.
 constexpr int DT = 64, DJ = 256, DE = 16, MAXE = 64;
 
 template <class TIO>
@@ -119,7 +122,7 @@ dx_kernel(int64_t T, int d, int E, int K, int cap_pad, const float* __restrict__
           const float* __restrict__ wgt, const float* __restrict__ noise,
           const TIO* __restrict__ dX, const int32_t* __restrict__ choice,
           const int32_t* __restrict__ pos, const TIO* __restrict__ dy, bool residual_is_x,
-          TIO* __restrict__ dx, TIO* __restrict__ dres) {
+          TIO* __restrict__ dx, TIO* __restrict__ dres, float* __restrict__ dxg_out) {
     __shared__ __align__(16) float Ls[DT][MAXE + 1];
     __shared__ __align__(16) float Ws[DE][DJ + 4];
     __shared__ int64_t rows[DT][2];
@@ -133,7 +136,7 @@ dx_kernel(int64_t T, int d, int E, int K, int cap_pad, const float* __restrict__
         const int64_t t = t0 + tt;
         Ls[tt][e] = t < T ? dL[t * E + e] : 0.f;
     }
-    if (tid < DT) {
+    if (tid < DT && !dxg_out) {
         const int64_t t = t0 + tid;
         int any = 0;
         for (int k = 0; k < 2; ++k) {
@@ -191,6 +194,11 @@ dx_kernel(int64_t T, int d, int E, int K, int cap_pad, const float* __restrict__
         } else {
 #pragma unroll
             for (int q = 0; q < 8; ++q) v[q] = acc[i][q];
+        }
+        if (dxg_out) {
+            *reinterpret_cast<float4*>(dxg_out + t * d + j) = make_float4(v[0], v[1], v[2], v[3]);
+            *reinterpret_cast<float4*>(dxg_out + t * d + j + 4) = make_float4(v[4], v[5], v[6], v[7]);
+            continue;
         }
         for (int k = 0; k < K; ++k) {
             const int64_t r = rows[tt][k];
@@ -259,7 +267,15 @@ void launch_gate2_dx(int64_t T, int d, int E, int K, int cap_pad, const float* d
                      const TIO* dy, bool residual_is_x, TIO* dx, TIO* dres, cudaStream_t st) {
     dim3 grid((unsigned)ceil_div(T, gate2::DT), (unsigned)(d / gate2::DJ));
     gate2::dx_kernel<TIO><<<grid, gate2::NT, 0, st>>>(T, d, E, K, cap_pad, dL, wgt, noise, dX, choice,
-                                                       pos, dy, residual_is_x, dx, dres);
+                                                       pos, dy, residual_is_x, dx, dres, nullptr);
+    MOE_LAUNCH_CHECK();
+}
+
+void launch_gate2_dxg(int64_t T, int d, int E, const float* dL, const float* wgt, const float* noise,
+                      float* dxg, cudaStream_t st) {
+    dim3 grid((unsigned)ceil_div(T, gate2::DT), (unsigned)(d / gate2::DJ));
+    gate2::dx_kernel<float><<<grid, gate2::NT, 0, st>>>(T, d, E, 1, 0, dL, wgt, noise, nullptr, nullptr,
+                                                         nullptr, nullptr, false, nullptr, nullptr, dxg);
     MOE_LAUNCH_CHECK();
 }
 

@@ -29,6 +29,7 @@
 
 #include "common.cuh"
 #include "gemm_tc.h"
+#include "tc_ptx.cuh"
 
 namespace moe {
 
@@ -74,98 +75,8 @@ struct __align__(64) Params {
     int ep, El, cap_pad;
     int epi;
     int b_mn;        // ROW: 1 if W is N-major
+    float* colsum;   // ROW: optional per-32-row-block column sums of C
 };
-
-// ---------------------------------------------------------------- PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst,
-                                            int32_t c0, int32_t c1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-        : "memory");
-}
-__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                     smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                       uint32_t idesc, uint32_t accumulate) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-        "}\n" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-
-// TMEM -> registers: 32 lanes x 32 consecutive 32-bit columns
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
-        "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-          "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
-          "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
-          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
-          "=r"(v[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-
-// Shared-memory matrix descriptor (tcgen05 "matrix descriptor"), 128B swizzle.
-//   K-major tile (rows x 64 K, 128 B per row): LBO unused (1), SBO = 1024 B
-//   (8-row core-matrix groups); advance along K by +32 B per K=16 step.
-//   MN-major tile (64-wide MN blocks of BK rows): LBO = MN-block stride,
-//   SBO = 1024 B (8-row K groups); advance along K by +2048 B per K=16 step.
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-    uint64_t d = 0;
-    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
-    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
-    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
-    d |= static_cast<uint64_t>(1) << 46;  // descriptor version (Blackwell)
-    d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
-    return d;
-}
 
 // Instruction descriptor, kind::f16: bf16 A/B, fp32 D, M=128, N=256.
 __host__ __device__ constexpr uint32_t make_idesc(uint32_t a_mn, uint32_t b_mn) {
@@ -462,6 +373,8 @@ __global__ void __launch_bounds__(kThreads, 1) grouped_gemm_kernel(const __grid_
                         }
                     }
                 }
+                if (KIND == ROW && p.colsum)
+                    epi_colsum64(f, lane, p.colsum + static_cast<int64_t>(box_row / 32) * p.N + ncol0 + c);
                 // stage the warp's 32 x 64 bf16 block (128B-swizzled rows) and
                 // hand it to the TMA engine; two buffers alternate per warp
                 uint8_t* sbuf = cstage + ((quarter * kEpiBufs + (cbuf % kEpiBufs)) * kStageCBytes);
@@ -857,6 +770,8 @@ gemm2_kernel(const __grid_constant__ Params p) {
                         }
                     }
                 }
+                if (KIND == ROW && p.colsum)
+                    epi_colsum64(f, lane, p.colsum + static_cast<int64_t>(box_row / 32) * p.N + ncol0 + c);
                 uint8_t* sbuf = cstage + quarter * kStageCBytes;
                 if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 __syncwarp();
@@ -982,6 +897,7 @@ static int pair_override() {
 
 static bool g_tc_enabled = true;
 void tc_set_enabled(bool on) { g_tc_enabled = on; }
+bool tc_enabled() { return g_tc_enabled; }
 
 bool tc_row_gemm_supported(const RowGemmArgs& a) {
     return g_tc_enabled && a.N % tc::BN == 0 && a.K % tc::BK == 0 && a.cap_pad % tc::BM == 0 &&
@@ -1014,6 +930,7 @@ void launch_row_gemm_tc(const RowGemmArgs& a, cudaStream_t st) {
     p.cap_pad = a.cap_pad;
     p.epi = a.epi;
     p.b_mn = a.w_nmajor ? 1 : 0;
+    p.colsum = a.epi == EPI_RELU_MASK ? a.colsum : nullptr;
     const int64_t max_tiles = rows / tc::BM * (a.N / tc::BN);
     const int ov = tc::pair_override();
     const bool use_pair = ov >= 0 ? ov == 1 : static_cast<int64_t>(a.ep) * a.cap_pad >= 2 * tc::BM;

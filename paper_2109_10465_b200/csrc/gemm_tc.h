@@ -11,5 +11,6 @@ bool tc_wgrad_gemm_supported(const WgradGemmArgs& a);
 void launch_wgrad_gemm_tc(const WgradGemmArgs& a, cudaStream_t st);
 // Force the SIMT path for bf16 as well (testing / A-B comparisons).
 void tc_set_enabled(bool on);
+bool tc_enabled();
 
 }  // namespace moe

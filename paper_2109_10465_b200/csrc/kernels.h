@@ -83,6 +83,10 @@ void launch_combine_weights(int64_t T, int E, int K, const float* gate_prob, flo
 template <class TIO>
 void launch_colsum_groups(const TIO* src, int64_t N, int ep, int El, int cap_pad,
                           const int32_t* counts, float* db, cudaStream_t st);
+// db[g][n] = sum over the group's computed 32-row blocks of part[blk][n]
+// (the fused GEMM-epilogue column sums of RowGemmArgs::colsum), fixed order
+void launch_colsum_parts(const float* part, int64_t N, int ep, int El, int cap_pad,
+                         const int32_t* counts, float* db, cudaStream_t st);
 // reference-layout per-stage dispatch / combine (routing.cpp:208-298)
 template <class TIO>
 void launch_dispatch_ref(const TIO* x, int64_t T, int64_t d, int E, int K, int cap,
@@ -123,6 +127,9 @@ struct RowGemmArgs {
     int ep, El, cap_pad;
     bool w_nmajor;
     int epi;
+    // optional (tensor-core path, EPI_RELU_MASK): per-32-row-block column sums
+    // of the stored C, [rows/32][N]; reduce with launch_colsum_parts
+    float* colsum = nullptr;
 };
 template <class T>
 void launch_row_gemm_simt(const RowGemmArgs& a, cudaStream_t st);
@@ -189,4 +196,21 @@ template <class TIO>
 void launch_gate2_dx(int64_t T, int d, int E, int K, int cap_pad, const float* dL, const float* wgt,
                      const float* noise, const TIO* dX, const int32_t* choice, const int32_t* pos,
                      const TIO* dy, bool residual_is_x, TIO* dx, TIO* dres, cudaStream_t st);
+// gate_tc.cu: tensor-core (kind::tf32) gate GEMMs for the bf16 path
+bool gate_tc_ok(int d, int E);
+int gate_tc_logit_splits(int64_t T, int d);
+// wgt = Wg^T [E][d] (launch_gate2_transpose)
+template <class TX>
+void launch_gate_tc_logits(const TX* x, const float* noise, const float* wgt, float* logits, int64_t T,
+                           int d, int E, int splits, cudaStream_t st);
+template <class TX>
+void launch_gate_tc_dw(const TX* x, const float* noise, const float* dL, float* part, int64_t T, int d,
+                       int E, int splits, cudaStream_t st);
+template <class TIO>
+void launch_gate_tc_dx(int64_t T, int d, int E, int K, int cap_pad, const float* dL, const float* wg,
+                       const float* noise, const TIO* dX, const int32_t* choice, const int32_t* pos,
+                       const TIO* dy, bool residual_is_x, TIO* dx, TIO* dres, cudaStream_t st);
+// dxg = (dL Wg^T) * noise in fp32 (noise may be null)
+void launch_gate2_dxg(int64_t T, int d, int E, const float* dL, const float* wgt, const float* noise,
+                      float* dxg, cudaStream_t st);
 }  // namespace moe

@@ -166,6 +166,7 @@ struct moe_handle {
     DevMem Xloc, Xr, H, Or, Oloc, dOloc, dOr, dH, dXr, dXloc;
     DevMem dL, dxg, dwg_part, wgt;
     DevMem bal_term, bal_done;  // balance_finalize per-expert terms + CTA counter
+    DevMem db1_part;            // [rows/32][f] column sums from the dgrad2 epilogue
     AssignScratch as{};
     std::vector<uint32_t> host_ord;
 
@@ -294,10 +295,11 @@ void ipc_setup(moe_handle* h) {
     h->ipc = true;
 }
 
+// Returns true iff the GEMM also produced the per-block column sums `colsum`.
 template <class TIO>
-void row_gemm(moe_handle* h, const TIO* A, const TIO* W, TIO* C, const float* bias,
+bool row_gemm(moe_handle* h, const TIO* A, const TIO* W, TIO* C, const float* bias,
               const TIO* mask, const int32_t* counts, int64_t N, int64_t K, bool w_nmajor,
-              int epi, int nseg_ep) {
+              int epi, int nseg_ep, float* colsum = nullptr) {
     RowGemmArgs a;
     a.A = A;
     a.W = W;
@@ -312,13 +314,15 @@ void row_gemm(moe_handle* h, const TIO* A, const TIO* W, TIO* C, const float* bi
     a.cap_pad = h->cap_pad;
     a.w_nmajor = w_nmajor;
     a.epi = epi;
+    a.colsum = colsum;
     if constexpr (std::is_same<TIO, __nv_bfloat16>::value) {
         if (tc_row_gemm_supported(a)) {
             launch_row_gemm_tc(a, h->stream);
-            return;
+            return colsum != nullptr;
         }
     }
     launch_row_gemm_simt<TIO>(a, h->stream);
+    return false;
 }
 
 template <class TIO>
@@ -343,6 +347,13 @@ void wgrad_gemm(moe_handle* h, const TIO* A, const TIO* B, TIO* C, int64_t M, in
     launch_wgrad_gemm_simt<TIO>(a, h->stream);
 }
 
+// Tensor-core gate GEMMs (gate_tc.cu) serve the bf16 path when the shape fits.
+template <class TIO>
+bool use_gate_tc(const moe_handle* h) {
+    return std::is_same<TIO, __nv_bfloat16>::value && tc_enabled() &&
+           gate_tc_ok(static_cast<int>(h->d), h->E);
+}
+
 // ---------------------------------------------------------------------------
 // router: gate -> softmax/top-k -> balance loss -> assignment
 // ---------------------------------------------------------------------------
@@ -361,7 +372,14 @@ void route(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, int phas
     }
     // logits = (x * noise) @ gate_w  (routing.cpp:71)
     int nsplit = 1;
-    if (gate2_ok(static_cast<int>(h->d), E)) {
+    if (use_gate_tc<TIO>(h)) {
+        if constexpr (std::is_same<TIO, __nv_bfloat16>::value) {
+            nsplit = gate_tc_logit_splits(T, static_cast<int>(h->d));
+            launch_gate2_transpose(gate_w, h->wgt.as<float>(), static_cast<int>(h->d), E, st);
+            launch_gate_tc_logits<TIO>(x, jitter ? h->noise.as<float>() : nullptr, h->wgt.as<float>(),
+                                       h->logits.as<float>(), T, static_cast<int>(h->d), E, nsplit, st);
+        }
+    } else if (gate2_ok(static_cast<int>(h->d), E)) {
         nsplit = gate2_logit_splits(T, static_cast<int>(h->d), E);
         launch_gate2_logits<TIO>(x, jitter ? h->noise.as<float>() : nullptr, gate_w,
                                  h->logits.as<float>(), T, static_cast<int>(h->d), E, nsplit, st);
@@ -519,33 +537,17 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
         counts = h->counts_r.as<int32_t>();
         h->mark("a2a_dO");
     }
-    // Side stream: work that only needs dL / dO / dH runs next to the expert
-    // GEMMs (those are HBM- or tensor-bound persistent kernels that leave
-    // shared memory and registers for these FMA/HBM-light kernels):
-    //   dWg = (x*noise)^T dL (split-K, fixed order), db2 = colsum(dO), db1 = colsum(dH)
     const float* noise = h->jitter_on ? h->noise.as<float>() : nullptr;
     const bool fast = gate_fast_ok(static_cast<int>(d), E);
-    const int splits = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(1, T / 512)));
+    const bool g2 = gate2_ok(static_cast<int>(d), E);
     cudaStream_t side = h->side;
-    MOE_CUDA_CHECK(cudaEventRecord(h->ev_a, st));
-    MOE_CUDA_CHECK(cudaStreamWaitEvent(side, h->ev_a, 0));
-    if (fast) {
-        launch_gate_dw<TIO>(x, noise, h->dL.as<float>(), h->dwg_part.as<float>(), T,
-                            static_cast<int>(d), E, splits, side);
-    } else {
-        launch_gemm_dense<TIO>(x, 1, d, noise, h->dL.as<float>(), E, 1, h->dwg_part.as<float>(), d,
-                               E, T, splits, side);
-    }
-    launch_splitk_reduce(h->dwg_part.as<float>(), splits, d * E, dgate_w, side);
-    launch_colsum_groups<TIO>(h->dOr.as<TIO>(), d, ep, El, h->cap_pad, counts, db2, side);
     // expert backward: dH = (dO W2^T) * [H > 0]; dX = dH W1^T; dW2 = H^T dO; dW1 = X^T dH
-    row_gemm<TIO>(h, h->dOr.as<TIO>(), w2, h->dH.as<TIO>(), nullptr, h->H.as<TIO>(), counts, f, d,
-                  false, EPI_RELU_MASK, ep);
+    // db1 = colsum(dH) comes out of the dgrad2 epilogue on the tensor-core path
+    const bool db1_fused = row_gemm<TIO>(h, h->dOr.as<TIO>(), w2, h->dH.as<TIO>(), nullptr,
+                                         h->H.as<TIO>(), counts, f, d, false, EPI_RELU_MASK, ep,
+                                         h->db1_part.as<float>());
     h->mark("ffn2_dgrad");
-    MOE_CUDA_CHECK(cudaEventRecord(h->ev_b, st));
-    MOE_CUDA_CHECK(cudaStreamWaitEvent(side, h->ev_b, 0));
-    launch_colsum_groups<TIO>(h->dH.as<TIO>(), f, ep, El, h->cap_pad, counts, db1, side);
-    MOE_CUDA_CHECK(cudaEventRecord(h->ev_side, side));
+    if (db1_fused) launch_colsum_parts(h->db1_part.as<float>(), f, ep, El, h->cap_pad, counts, db1, st);
     row_gemm<TIO>(h, h->dH.as<TIO>(), w1, h->dXr.as<TIO>(), nullptr, nullptr, counts, d, f, false,
                   EPI_NONE, ep);
     h->mark("ffn1_dgrad");
@@ -561,10 +563,46 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
         MOE_CUDA_CHECK(cudaEventRecord(h->ev_comm, h->comm_stream));
         dXloc = h->dXloc.as<TIO>();
     }
+    // Side stream, next to the weight-gradient GEMMs (persistent kernels that
+    // leave ~40 KB of shared memory, most registers and the FMA pipes free;
+    // the dgrad GEMMs before them fill shared memory, so nothing co-runs there):
+    //   db2 = colsum(dO), db1 = colsum(dH) when not fused into the dgrad2
+    //   epilogue, and on the FMA path dWg = (x*noise)^T dL and
+    //   dxg = (dL Wg^T) * noise.  On the tensor-core path the gate GEMMs run on
+    //   the main stream after the weight gradients (gate_tc.cu).
+    const bool gtc = use_gate_tc<TIO>(h);
+    MOE_CUDA_CHECK(cudaEventRecord(h->ev_a, st));
+    MOE_CUDA_CHECK(cudaStreamWaitEvent(side, h->ev_a, 0));
+    const int dw_splits = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(1, T / 512)));
+    if (!gtc) {
+        if (fast) {
+            launch_gate_dw<TIO>(x, noise, h->dL.as<float>(), h->dwg_part.as<float>(), T,
+                                static_cast<int>(d), E, dw_splits, side);
+        } else {
+            launch_gemm_dense<TIO>(x, 1, d, noise, h->dL.as<float>(), E, 1, h->dwg_part.as<float>(),
+                                   d, E, T, dw_splits, side);
+        }
+        launch_splitk_reduce(h->dwg_part.as<float>(), dw_splits, d * E, dgate_w, side);
+        if (g2) {
+            launch_gate2_transpose(h->gate_w, h->wgt.as<float>(), static_cast<int>(d), E, side);
+            launch_gate2_dxg(T, static_cast<int>(d), E, h->dL.as<float>(), h->wgt.as<float>(), noise,
+                             h->dxg.as<float>(), side);
+        }
+    }
+    launch_colsum_groups<TIO>(h->dOr.as<TIO>(), d, ep, El, h->cap_pad, counts, db2, side);
+    if (!db1_fused) launch_colsum_groups<TIO>(h->dH.as<TIO>(), f, ep, El, h->cap_pad, counts, db1, side);
+    MOE_CUDA_CHECK(cudaEventRecord(h->ev_side, side));
     wgrad_gemm<TIO>(h, h->H.as<TIO>(), h->dOr.as<TIO>(), dw2, f, d, counts, ep);
     h->mark("ffn2_wgrad");
     wgrad_gemm<TIO>(h, h->Xr.as<TIO>(), h->dH.as<TIO>(), dw1, d, f, counts, ep);
     h->mark("ffn1_wgrad");
+    if (gtc) {  // dWg = (x*noise)^T dL on the tensor cores, split-K + fixed-order reduce
+        if constexpr (std::is_same<TIO, __nv_bfloat16>::value)
+            launch_gate_tc_dw<TIO>(x, noise, h->dL.as<float>(), h->dwg_part.as<float>(), T,
+                                   static_cast<int>(d), E, dw_splits, st);
+        launch_splitk_reduce(h->dwg_part.as<float>(), dw_splits, d * E, dgate_w, st);
+        h->mark("gate_dw");
+    }
     MOE_CUDA_CHECK(cudaStreamWaitEvent(st, h->ev_side, 0));
     if (ep > 1) MOE_CUDA_CHECK(cudaStreamWaitEvent(st, h->ev_comm, 0));
     h->mark("bwd_join");
@@ -573,11 +611,15 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
                                  h->comm, st));
         h->mark("allreduce_dgate_w");
     }
-    if (gate2_ok(static_cast<int>(d), E)) {  // dx = (dL Wg^T) * noise + dispatch bwd + residual
-        launch_gate2_transpose(h->gate_w, h->wgt.as<float>(), static_cast<int>(d), E, st);
-        launch_gate2_dx<TIO>(T, static_cast<int>(d), E, K, h->cap_pad, h->dL.as<float>(),
-                             h->wgt.as<float>(), noise, dXloc, h->choice.as<int32_t>(),
-                             h->pos.as<int32_t>(), dy, !h->has_residual, dx, dres, st);
+    if (gtc) {  // dx = (dL Wg^T) * noise + dispatch bwd + residual, one tensor-core kernel
+        if constexpr (std::is_same<TIO, __nv_bfloat16>::value)
+            launch_gate_tc_dx<TIO>(T, static_cast<int>(d), E, K, h->cap_pad, h->dL.as<float>(),
+                                   h->gate_w, noise, dXloc, h->choice.as<int32_t>(),
+                                   h->pos.as<int32_t>(), dy, !h->has_residual, dx, dres, st);
+    } else if (g2) {  // dx = dxg (side stream, noise applied) + dispatch bwd + residual
+        launch_dx_assemble<TIO>(T, d, E, K, h->cap_pad, h->dxg.as<float>(), nullptr, dXloc,
+                                h->choice.as<int32_t>(), h->pos.as<int32_t>(), dy,
+                                !h->has_residual, dx, dres, st);
     } else if (fast) {  // same, 64x64 tiles
         launch_gate_dx<TIO>(T, static_cast<int>(d), E, K, h->cap_pad, h->dL.as<float>(), h->gate_w,
                             noise, dXloc, h->choice.as<int32_t>(), h->pos.as<int32_t>(), dy,
@@ -641,6 +683,7 @@ void alloc_workspace(moe_handle* h) {
     h->dOr.alloc(es * R * d);
     h->dH.alloc(es * R * f);
     h->dXr.alloc(es * R * d);
+    if (es == 2) h->db1_part.alloc(4 * static_cast<size_t>(R / 32 + 1) * f);
     if (h->ep > 1) {
         h->Xloc.alloc(es * R * d);
         h->Oloc.alloc(es * R * d);
@@ -1023,6 +1066,42 @@ moe_status moe_debug_mt64_chunk_host(uint64_t seed, int64_t J, int c, int64_t n,
 moe_status moe_debug_mt64_device(uint64_t seed, int64_t count, uint64_t* out_dev) {
     return guarded(nullptr, [&] {
         moe::launch_mt64_raw_device(seed, count, out_dev, nullptr);
+        MOE_CUDA_CHECK(cudaDeviceSynchronize());
+    });
+}
+moe_status moe_debug_gate_tc_logits(const void* x, const float* noise, const float* gate_w,
+                                    float* logits_part, int64_t T, int d, int E, int splits) {
+    return guarded(nullptr, [&] {
+        require(moe::gate_tc_ok(d, E), MOE_SHAPE, "gate_tc: unsupported shape");
+        float* wgt = nullptr;
+        MOE_CUDA_CHECK(cudaMalloc(&wgt, sizeof(float) * static_cast<size_t>(d) * E));
+        moe::launch_gate2_transpose(gate_w, wgt, d, E, nullptr);
+        moe::launch_gate_tc_logits<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(x), noise, wgt,
+                                                  logits_part, T, d, E, splits, nullptr);
+        MOE_CUDA_CHECK(cudaDeviceSynchronize());
+        MOE_CUDA_CHECK(cudaFree(wgt));
+        MOE_CUDA_CHECK(cudaDeviceSynchronize());
+    });
+}
+moe_status moe_debug_gate_tc_dw(const void* x, const float* noise, const float* dL, float* dw_part,
+                                int64_t T, int d, int E, int splits) {
+    return guarded(nullptr, [&] {
+        require(moe::gate_tc_ok(d, E), MOE_SHAPE, "gate_tc: unsupported shape");
+        moe::launch_gate_tc_dw<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(x), noise, dL, dw_part, T,
+                                              d, E, splits, nullptr);
+        MOE_CUDA_CHECK(cudaDeviceSynchronize());
+    });
+}
+moe_status moe_debug_gate_tc_dx(int64_t T, int d, int E, int K, int cap_pad, const float* dL,
+                                const float* gate_w, const float* noise, const void* dX,
+                                const int32_t* choice, const int32_t* pos, const void* dy,
+                                int residual_is_x, void* dx, void* dres) {
+    using B = __nv_bfloat16;
+    return guarded(nullptr, [&] {
+        require(moe::gate_tc_ok(d, E), MOE_SHAPE, "gate_tc: unsupported shape");
+        moe::launch_gate_tc_dx<B>(T, d, E, K, cap_pad, dL, gate_w, noise, static_cast<const B*>(dX), choice,
+                                  pos, static_cast<const B*>(dy), residual_is_x != 0, static_cast<B*>(dx),
+                                  static_cast<B*>(dres), nullptr);
         MOE_CUDA_CHECK(cudaDeviceSynchronize());
     });
 }

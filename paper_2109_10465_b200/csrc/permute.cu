@@ -10,6 +10,8 @@
 // row, so each output row is written exactly once (no atomics, deterministic).
 // The fused layer uses a compact internal row index e*cap_pad + pos (pos ==
 // slot except in grouped mode) whose occupied rows are dense per expert.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -195,10 +197,23 @@ dx_assemble_kernel(int64_t T, int64_t d, int K, int cap_pad, const float* __rest
 #pragma unroll
             for (int q = 0; q < V; ++q) acc[q] += v[q];
         }
+        {
+            float g[V];
+            if constexpr (V % 4 == 0) {
 #pragma unroll
-        for (int q = 0; q < V; ++q) {
-            const float nz = noise ? noise[t * d + j + q] : 1.f;
-            acc[q] = fmaf(dxg[t * d + j + q], nz, acc[q]);
+                for (int q = 0; q < V; q += 4) {
+                    const float4 u = __ldg(reinterpret_cast<const float4*>(dxg + t * d + j + q));
+                    g[q] = u.x; g[q + 1] = u.y; g[q + 2] = u.z; g[q + 3] = u.w;
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < V; ++q) g[q] = dxg[t * d + j + q];
+            }
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+                const float nz = noise ? noise[t * d + j + q] : 1.f;
+                acc[q] = fmaf(g[q], nz, acc[q]);
+            }
         }
         if (!any) {
             float g[V];
@@ -253,28 +268,59 @@ void launch_combine_weights(int64_t T, int E, int K, const float* gate_prob, flo
 }
 
 // db[g][n] = sum_{r, i < count(r,g)} src[(r*El+g)*cap_pad + i][n], fixed order.
+// One CTA per SM at most (grid-stride over (group, 128-column block) items):
+// the kernel runs on the side stream next to persistent GEMMs and must never
+// take the registers / warp slots a GEMM CTA needs.
 template <class TIO>
 __global__ void colsum_groups_kernel(const TIO* __restrict__ src, int64_t N, int ep, int El,
                                      int cap_pad, const int32_t* __restrict__ counts,
                                      float* __restrict__ db) {
+    const int64_t nblk = (N + 127) / 128;
+    for (int64_t item = blockIdx.x; item < nblk * El; item += gridDim.x) {
+        const int g = static_cast<int>(item / nblk);
+        const int64_t n = (item % nblk) * 128 + threadIdx.x;
+        if (n >= N) continue;
+        float acc = 0.f;
+        for (int r = 0; r < ep; ++r) {
+            const int seg = r * El + g;
+            const int cnt = counts[seg];
+            const TIO* base = src + (int64_t)seg * cap_pad * N + n;
+            for (int i = 0; i < cnt; ++i) acc += to_f(base[(int64_t)i * N]);
+        }
+        db[(int64_t)g * N + n] = acc;
+    }
+}
+
+template <class TIO>
+void launch_colsum_groups(const TIO* src, int64_t N, int ep, int El, int cap_pad,
+                          const int32_t* counts, float* db, cudaStream_t st) {
+    const int64_t items = ceil_div(N, (int64_t)128) * El;
+    colsum_groups_kernel<TIO><<<(unsigned)std::min<int64_t>(items, kNumSMs), 128, 0, st>>>(
+        src, N, ep, El, cap_pad, counts, db);
+    MOE_LAUNCH_CHECK();
+}
+
+__global__ void colsum_parts_kernel(const float* __restrict__ part, int64_t N, int ep, int El,
+                                    int cap_pad, const int32_t* __restrict__ counts,
+                                    float* __restrict__ db) {
     const int g = blockIdx.y;
     const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= N) return;
     float acc = 0.f;
     for (int r = 0; r < ep; ++r) {
         const int seg = r * El + g;
-        const int cnt = counts[seg];
-        const TIO* base = src + (int64_t)seg * cap_pad * N + n;
-        for (int i = 0; i < cnt; ++i) acc += to_f(base[(int64_t)i * N]);
+        // 32-row blocks of the 128-row tiles the GEMM computed for this segment
+        const int nblk = 4 * ((counts[seg] + 127) / 128);
+        const float* base = part + ((int64_t)seg * cap_pad / 32) * N + n;
+        for (int b = 0; b < nblk; ++b) acc += base[(int64_t)b * N];
     }
     db[(int64_t)g * N + n] = acc;
 }
 
-template <class TIO>
-void launch_colsum_groups(const TIO* src, int64_t N, int ep, int El, int cap_pad,
-                          const int32_t* counts, float* db, cudaStream_t st) {
+void launch_colsum_parts(const float* part, int64_t N, int ep, int El, int cap_pad,
+                         const int32_t* counts, float* db, cudaStream_t st) {
     dim3 grid((unsigned)ceil_div(N, 128), El);
-    colsum_groups_kernel<TIO><<<grid, 128, 0, st>>>(src, N, ep, El, cap_pad, counts, db);
+    colsum_parts_kernel<<<grid, 128, 0, st>>>(part, N, ep, El, cap_pad, counts, db);
     MOE_LAUNCH_CHECK();
 }
 
