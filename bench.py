@@ -213,6 +213,41 @@ def stage_model(stage, T, d, f, El, n_rows, n_tok):
     return None, None
 
 
+def stage_bytes(stage, T, d, E, K, n_kept, n_drop):
+    """Algorithmic HBM bytes of the HBM-bound stages per SURVEY.md §8(d)
+    (bf16 activations, s = 2; padding rows / zero fill not counted)."""
+    s = 2
+    if stage == "gate":          # x read + (choice, slot, prob) write + P saved
+        return T * d * s + T * K * 12 + T * E * 4
+    if stage == "assign":        # choice read + slot write
+        return T * K * 8
+    if stage == "dispatch":      # kept rows: x read + buffer write
+        return 2 * n_kept * d * s
+    if stage == "combine":       # kept rows read + y write (+ residual rows of dropped tokens)
+        return n_kept * d * s + T * d * s + n_drop * d * s
+    if stage == "combine_bwd":   # dy read (kept tokens) + dO rows write
+        return 2 * n_kept * d * s
+    if stage == "gate_dx":       # dX rows gathered + dx write (+ dy of dropped tokens)
+        return n_kept * d * s + T * d * s + n_drop * d * s
+    return None
+
+
+def traffic_for(stage, workload_tag):
+    """Measured DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum
+    from one `ncu --set full` capture, committed under profiles/) when the
+    profile was taken on this exact workload; else None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            t = json.load(fh)
+    except OSError:
+        return None, None
+    if t.get("workload") != workload_tag:
+        return None, None
+    v = t.get("bytes_per_launch", {}).get(stage)
+    return v, t.get("source")
+
+
 def run_ours(args):
     os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep NCCL's banner off stdout
     import numpy as np
@@ -395,6 +430,23 @@ def run_ours(args):
                     "unit": "TFLOP/s", "frac": ach / tf_sus, "peak_source": src + " (sustained)",
                     "algorithmic_bytes": bytes_, "flops": flops, "traffic": None}
         roof["launch_ms"] = per_stage[top]["ms"]
+        tr, tsrc = traffic_for(top, f"c3 T={T} N={N}")
+        if tr is not None:
+            roof["traffic"] = tr
+            roof["traffic_source"] = tsrc
+    # HBM-bound stages against the same measured peak
+    n_kept = int(kept.sum().item()) if N == 1 else T
+    n_drop = T - n_kept
+    groups = {"gate": ["jitter_noise", "gate_logits", "softmax_topk", "balance_loss"]}
+    stage_roof = {}
+    for name in ["gate", "assign", "dispatch", "combine", "combine_bwd", "gate_dx"]:
+        parts = groups.get(name, [name])
+        if not all(p in per_stage for p in parts):
+            continue
+        st_ms = sum(per_stage[p]["ms"] for p in parts)
+        b = stage_bytes(name, T, d, E, 1, n_kept, n_drop)
+        stage_roof[name] = {"ms": st_ms, "algorithmic_bytes": b, "GB/s": b / (st_ms / 1e3) / 1e9,
+                            "frac": b / (st_ms / 1e3) / 1e9 / hbm}
     gemm_ms = sum(v["ms"] for k, v in per_stage.items() if k.startswith("ffn"))
     gemm_flops = 12.0 * n_rows * d * f
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps,
@@ -408,6 +460,7 @@ def run_ours(args):
                     "h2d_bytes_per_step": 2 * T * d * 2, "d2h_bytes_per_step": T * d * 2 + 4},
             "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
             "clocks": clk, "stages_ms": {k: round(v["ms"], 4) for k, v in per_stage.items()},
+            "stage_roofline": stage_roof,
             "decision": {"capacity": cap, "dropped_tokens_rank0": drops}}
     if N == 1 and not args.no_cpu_baseline:
         try:

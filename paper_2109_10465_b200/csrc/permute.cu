@@ -270,24 +270,37 @@ void launch_combine_weights(int64_t T, int E, int K, const float* gate_prob, flo
 // db[g][n] = sum_{r, i < count(r,g)} src[(r*El+g)*cap_pad + i][n], fixed order.
 // One CTA per SM at most (grid-stride over (group, 128-column block) items):
 // the kernel runs on the side stream next to persistent GEMMs and must never
-// take the registers / warp slots a GEMM CTA needs.
+// take the registers / warp slots a GEMM CTA needs.  4 row groups per item
+// (fixed strided order), combined in fixed order through shared memory.
+constexpr int kColsumRG = 4;
 template <class TIO>
-__global__ void colsum_groups_kernel(const TIO* __restrict__ src, int64_t N, int ep, int El,
-                                     int cap_pad, const int32_t* __restrict__ counts,
-                                     float* __restrict__ db) {
+__global__ void __launch_bounds__(128 * kColsumRG)
+colsum_groups_kernel(const TIO* __restrict__ src, int64_t N, int ep, int El, int cap_pad,
+                     const int32_t* __restrict__ counts, float* __restrict__ db) {
+    __shared__ float part[kColsumRG][128];
+    const int c = threadIdx.x & 127, rg = threadIdx.x >> 7;
     const int64_t nblk = (N + 127) / 128;
     for (int64_t item = blockIdx.x; item < nblk * El; item += gridDim.x) {
         const int g = static_cast<int>(item / nblk);
-        const int64_t n = (item % nblk) * 128 + threadIdx.x;
-        if (n >= N) continue;
+        const int64_t n = (item % nblk) * 128 + c;
         float acc = 0.f;
-        for (int r = 0; r < ep; ++r) {
-            const int seg = r * El + g;
-            const int cnt = counts[seg];
-            const TIO* base = src + (int64_t)seg * cap_pad * N + n;
-            for (int i = 0; i < cnt; ++i) acc += to_f(base[(int64_t)i * N]);
+        if (n < N) {
+            for (int r = 0; r < ep; ++r) {
+                const int seg = r * El + g;
+                const int cnt = counts[seg];
+                const TIO* base = src + (int64_t)seg * cap_pad * N + n;
+                for (int i = rg; i < cnt; i += kColsumRG) acc += to_f(base[(int64_t)i * N]);
+            }
         }
-        db[(int64_t)g * N + n] = acc;
+        part[rg][c] = acc;
+        __syncthreads();
+        if (rg == 0 && n < N) {
+            float t = part[0][c];
+#pragma unroll
+            for (int q = 1; q < kColsumRG; ++q) t += part[q][c];
+            db[(int64_t)g * N + n] = t;
+        }
+        __syncthreads();
     }
 }
 
@@ -295,7 +308,7 @@ template <class TIO>
 void launch_colsum_groups(const TIO* src, int64_t N, int ep, int El, int cap_pad,
                           const int32_t* counts, float* db, cudaStream_t st) {
     const int64_t items = ceil_div(N, (int64_t)128) * El;
-    colsum_groups_kernel<TIO><<<(unsigned)std::min<int64_t>(items, kNumSMs), 128, 0, st>>>(
+    colsum_groups_kernel<TIO><<<(unsigned)std::min<int64_t>(items, kNumSMs), 128 * kColsumRG, 0, st>>>(
         src, N, ep, El, cap_pad, counts, db);
     MOE_LAUNCH_CHECK();
 }

@@ -79,7 +79,11 @@ def main():
     dw2 = sum(rr.dw2 for rr in refs)[lo:hi]
     db1 = sum(rr.db1 for rr in refs)[lo:hi]
     db2 = sum(rr.db2 for rr in refs)[lo:hi]
-    errs = dict(y=rel(y, ref.y), dx=rel(g["dx"], ref.dx), aux=abs(aux.item() - ref.aux),
+    # fp32: element-wise 1e-5.  bf16: norm-wise like test_gpu_bf16 —
+    # element-wise maxima over 4 ranks of bf16-rounded chains (dH, dX, y all
+    # rounded to 2^-8) sit at the 2e-2 line by chance alone
+    ew = rel if mode == "fp32" else reln
+    errs = dict(y=ew(y, ref.y), dx=ew(g["dx"], ref.dx), aux=abs(aux.item() - ref.aux),
                 dgate_w=reln(g["dgate_w"], dwg), dw1=reln(g["dw1"], dw1), dw2=reln(g["dw2"], dw2),
                 db1=reln(g["db1"], db1), db2=reln(g["db2"], db2))
     tol = 1e-5 if mode == "fp32" else 2e-2
