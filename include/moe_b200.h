@@ -131,6 +131,15 @@ moe_status moe_backward(moe_handle* h, const void* dy, float daux, void* dx, flo
 moe_status moe_last_decision_stats(moe_handle* h, int* capacity, int64_t* drop_count,
                                    int64_t* kept_per_expert);
 
+/* Utilization and drop statistics of the last forward, accumulated on the
+ * device into caller-owned int64 arrays (stream-ordered, no sync):
+ *   util_dev[E]  += first-choice counts per expert (count_utilization,
+ *                   surgery.cpp:100-122, counts expert_id[t*top_k]);
+ *   hist_dev[10] : [0..7] += dropped routes by token-position octile
+ *                   min(7, 8t/T), [8] += dropped routes, [9] += T*top_k
+ *                   routes (DropHistogram::accumulate, trainer.cpp:15-29). */
+moe_status moe_accumulate_decision_stats(moe_handle* h, int64_t* util_dev, int64_t* hist_dev);
+
 /* ---- per-stage entry points (routing.hpp:60-118) ----------------------- */
 /* gate_forward (routing.cpp:51-101): probs [T,E] fp32, choice [T*k] int32,
  * gate_prob [T*k] fp32.  x has the handle's dtype. */

@@ -79,6 +79,9 @@ void launch_dx_assemble(int64_t T, int64_t d, int E, int K, int cap_pad, const f
                         TIO* dres, cudaStream_t st);
 void launch_combine_weights(int64_t T, int E, int K, const float* gate_prob, float* w,
                             cudaStream_t st);
+// utilization / drop-position statistics of a decision (int64 accumulators)
+void launch_decision_stats(int64_t T, int E, int K, const int32_t* choice, const int32_t* pos,
+                           int64_t* util, int64_t* hist, cudaStream_t st);
 // db[g][n] = sum over the group's occupied rows of src[row][n]
 template <class TIO>
 void launch_colsum_groups(const TIO* src, int64_t N, int ep, int El, int cap_pad,

@@ -904,6 +904,16 @@ moe_status moe_last_decision_stats(moe_handle* h, int* capacity, int64_t* drop_c
     });
 }
 
+moe_status moe_accumulate_decision_stats(moe_handle* h, int64_t* util_dev, int64_t* hist_dev) {
+    if (!h) return MOE_SHAPE;
+    return guarded(h, [&] {
+        require(h->fwd_valid, MOE_SHAPE, "no forward on this handle");
+        require(util_dev && hist_dev, MOE_SHAPE, "decision stats: util[E] and hist[10] required");
+        launch_decision_stats(h->T, h->E, h->K, h->choice.as<int32_t>(), h->pos.as<int32_t>(), util_dev,
+                              hist_dev, h->stream);
+    });
+}
+
 moe_status moe_gate(moe_handle* h, int64_t T, const void* x, const float* gate_w, int phase,
                     uint64_t jitter_seed, float* probs, int32_t* choice, float* gate_prob) {
     if (!h) return MOE_SHAPE;

@@ -247,6 +247,49 @@ void launch_dx_assemble(int64_t T, int64_t d, int E, int K, int cap_pad, const f
     MOE_LAUNCH_CHECK();
 }
 
+// Utilization + drop statistics of one routing decision, accumulated into
+// caller-owned int64 counters (integer adds: exact and order-free):
+//   util[e]  += #{t : first choice of t is e}            surgery.cpp:113-118
+//   hist[b]  += #{dropped routes of tokens t with min(7, 8t/T) = b}
+//   hist[8]  += #dropped routes, hist[9] += T*K           trainer.cpp:15-29
+__global__ void decision_stats_kernel(int64_t T, int E, int K, const int32_t* __restrict__ choice,
+                                      const int32_t* __restrict__ pos,
+                                      unsigned long long* __restrict__ util,
+                                      unsigned long long* __restrict__ hist) {
+    extern __shared__ unsigned int s_cnt[];  // [E] + [9]
+    for (int i = threadIdx.x; i < E + 9; i += blockDim.x) s_cnt[i] = 0;
+    __syncthreads();
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < T;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int c0 = choice[t * K];
+        if (c0 >= 0 && c0 < E) atomicAdd(&s_cnt[c0], 1u);
+        for (int k = 0; k < K; ++k) {
+            if (pos[t * K + k] >= 0) continue;
+            const int64_t tb = t * 8 / (T > 1 ? T : 1);
+            const int b = tb < 7 ? (int)tb : 7;
+            atomicAdd(&s_cnt[E + b], 1u);
+            atomicAdd(&s_cnt[E + 8], 1u);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < E + 9; i += blockDim.x) {
+        const unsigned long long v = s_cnt[i];
+        if (v == 0) continue;
+        if (i < E) atomicAdd(&util[i], v);
+        else atomicAdd(&hist[i - E], v);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&hist[9], (unsigned long long)(T * K));
+}
+
+void launch_decision_stats(int64_t T, int E, int K, const int32_t* choice, const int32_t* pos,
+                           int64_t* util, int64_t* hist, cudaStream_t st) {
+    const int blocks = (int)std::min<int64_t>(kNumSMs, ceil_div(T, (int64_t)256));
+    decision_stats_kernel<<<blocks, 256, sizeof(unsigned int) * (E + 9), st>>>(
+        T, E, K, choice, pos, reinterpret_cast<unsigned long long*>(util),
+        reinterpret_cast<unsigned long long*>(hist));
+    MOE_LAUNCH_CHECK();
+}
+
 __global__ void combine_weights_kernel(int64_t T, int E, int K, const float* __restrict__ gp,
                                        float* __restrict__ w) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -1,0 +1,137 @@
+"""§8(f) rows 1 and 3: the model.cpp run_moe caller pattern (zero residual,
+per-ordinal seeds, aux sum, residual stream) over a stack of B200 layers,
+and the utilization / drop statistics (surgery.cpp:100-122,
+trainer.cpp:15-29), against the oracle composed the same way."""
+import numpy as np
+import pytest
+
+import oracle as O
+from oracle.margin import margin_guard
+
+pytestmark = pytest.mark.gpu
+
+
+def _ref_stack(x0, layers, cfg, seed, dy):
+    """Oracle: x_{l+1} = x_l + moe_l(x_l, residual=0, seed=derive_seed(seed, l));
+    loss = <dy, x_L> + sum_l aux_l; backward through the stream."""
+    o = O.restatement()
+    xs, refs, aux = [x0], [], 0.0
+    for l, (gw, w1, b1, w2, b2) in enumerate(layers):
+        r = o.moe_layer(xs[-1], gw, w1, b1, w2, b2, cfg, O.TRAIN, o.derive_seed(seed, l),
+                        residual=np.zeros_like(xs[-1]), dy=None)
+        refs.append(r)
+        aux += r.aux
+        xs.append(xs[-1] + r.y)
+    g = dy.copy()
+    grads = [None] * len(layers)
+    for l in range(len(layers) - 1, -1, -1):
+        gw, w1, b1, w2, b2 = layers[l]
+        r = o.moe_layer(xs[l], gw, w1, b1, w2, b2, cfg, O.TRAIN, o.derive_seed(seed, l),
+                        residual=np.zeros_like(xs[l]), dy=g, daux=1.0)
+        grads[l] = r
+        g = g + r.dx
+    return xs, refs, aux, g, grads
+
+
+def test_stack_matches_oracle_composition_fp32():
+    import torch
+    import paper_2109_10465_b200 as M
+    from paper_2109_10465_b200.stack import MoeStack
+
+    T, d, f, E, nl, seed = 256, 64, 128, 8, 3, 1234
+    cfg_o = O.make_cfg(num_experts=E, capacity_factor_train=1.0)
+    o = O.restatement()
+    layers = []
+    x0 = None
+    for l in range(nl):
+        x, gw, w1, b1, w2, b2, dy = O.layer_inputs(T, d, f, E, seed=100 + l)
+        layers.append(tuple(a.astype(np.float32).astype(np.float64) for a in (gw, w1, b1, w2, b2)))
+        if l == 0:
+            x0 = x.astype(np.float32).astype(np.float64)
+            dy0 = dy.astype(np.float32).astype(np.float64)
+    # only layer 0's input is drawn; later inputs are stream values, so guard
+    # decisions by checking them (a near-tie would show up as a decision diff)
+    x0 = margin_guard(x0, layers[0][0], cfg_o, O.TRAIN, o.derive_seed(seed, 0))
+    xs, refs, aux, dx_ref, grads_ref = _ref_stack(x0, layers, cfg_o, seed, dy0)
+
+    dev = torch.device("cuda")
+    to = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev, torch.float32)  # noqa: E731
+    params = [M.MoeLayerParams(to(gw), to(w1), to(b1), to(w2), to(b2)) for gw, w1, b1, w2, b2 in layers]
+    st = MoeStack(M.RouterConfig(num_experts=E), nl, T, d, f, torch.float32)
+    out, aux_g, decs = st.forward(to(x0), params, M.Phase.TRAIN, seed)
+    for l in range(nl):
+        assert np.array_equal(decs[l].expert_id.cpu().numpy(), refs[l].expert_id), l
+        assert np.array_equal(decs[l].slot.cpu().numpy(), refs[l].slot), l
+    # Norm-wise (max|diff| / max(1, max|ref|)), 1e-5: through the residual
+    # stream the gradient grows (max|dx| ~ 3e2 here) and small dx elements are
+    # differences of large terms, so the per-element max(1,|ref|) metric of a
+    # single layer would measure fp32 cancellation, not the kernels (measured:
+    # norm-wise 2.5e-6, element-wise 3e-4 on a 0.014 element of a 343-scale dx).
+    rel = lambda a, b: float(np.max(np.abs(a - b)) / max(1.0, np.max(np.abs(b))))  # noqa: E731
+    tol = 1e-5
+    assert rel(out.cpu().numpy().astype(np.float64), xs[-1]) < tol
+    assert abs(aux_g.item() - aux) < 1e-6
+    dx, grads = st.backward(to(dy0), 1.0)
+    assert rel(dx.cpu().numpy().astype(np.float64), dx_ref) < tol
+    for l in range(nl):
+        for k in ("dw1", "dw2", "db1", "db2", "dgate_w"):
+            a = grads[l][k].cpu().numpy().astype(np.float64)
+            b = getattr(grads_ref[l], k)
+            assert np.max(np.abs(a - b)) / max(1.0, np.max(np.abs(b))) < tol, (l, k)
+
+    # statistics: the reference's counters computed from the oracle decisions
+    util_ref = [np.bincount(r.expert_id.reshape(T, -1)[:, 0], minlength=E) for r in refs]
+    assert st.util.as_lists() == [list(map(int, u)) for u in util_ref]
+    buckets = np.zeros(8, np.int64)
+    dropped = 0
+    for r in refs:
+        slot = r.slot.reshape(T, -1)
+        for t in range(T):
+            for k in range(slot.shape[1]):
+                if slot[t, k] == -1:
+                    dropped += 1
+                    buckets[min(7, t * 8 // T)] += 1
+    assert st.drops.buckets == list(map(int, buckets))
+    assert st.drops.total_dropped == dropped
+    assert st.drops.total_routed == nl * T
+    assert st.util.total_tokens == T
+
+
+def test_drop_histogram_top2_rts_bf16():
+    """Decision statistics on a top-2 RTS bf16 layer equal the counters
+    recomputed from the returned decision arrays."""
+    import torch
+    import paper_2109_10465_b200 as M
+    from paper_2109_10465_b200.stack import DropHistogram, UtilizationCounts
+
+    T, d, f, E = 1000, 256, 512, 16
+    cfg = M.RouterConfig(num_experts=E, top_k=2, capacity_factor_train=0.75,
+                         assignment_mode=M.AssignmentMode.RTS)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    layer = M.MoeLayer(cfg, T, d, f, torch.bfloat16)
+    p = M.MoeLayerParams(torch.randn(d, E, device="cuda", generator=g) * 0.1,
+                         (torch.randn(E, d, f, device="cuda", generator=g) * 0.05).to(torch.bfloat16),
+                         torch.zeros(E, f, device="cuda"),
+                         (torch.randn(E, f, d, device="cuda", generator=g) * 0.05).to(torch.bfloat16),
+                         torch.zeros(E, d, device="cuda"))
+    x = (torch.rand(T, d, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    h, u = DropHistogram(), UtilizationCounts()
+    for step in range(2):
+        _, _, dec = layer.forward(x, p, M.Phase.TRAIN, 77 + step)
+        u.accumulate(0, layer, hist=h.dev)
+        torch.cuda.synchronize()
+    eid = dec.expert_id.cpu().numpy().reshape(T, 2)
+    slot = dec.slot.cpu().numpy().reshape(T, 2)
+    assert h.total_routed == 2 * 2 * T
+    assert h.total_dropped > 0  # capacity 0.75 < 1 drops routes every step
+    # last step only: recompute by subtracting a fresh single-step accumulation
+    h1, u1 = DropHistogram(), UtilizationCounts()
+    u1.accumulate(0, layer, hist=h1.dev)
+    b = np.zeros(8, np.int64)
+    for t in range(T):
+        for k in range(2):
+            if slot[t, k] == -1:
+                b[min(7, t * 8 // T)] += 1
+    assert h1.buckets == list(map(int, b))
+    assert h1.total_dropped == int((slot == -1).sum())
+    assert u1.as_lists()[0] == list(map(int, np.bincount(eid[:, 0], minlength=E)))
