@@ -140,6 +140,24 @@ moe_status moe_last_decision_stats(moe_handle* h, int* capacity, int64_t* drop_c
  *                   routes (DropHistogram::accumulate, trainer.cpp:15-29). */
 moe_status moe_accumulate_decision_stats(moe_handle* h, int64_t* util_dev, int64_t* hist_dev);
 
+/* ---- expert optimizer step: AdamOptimizer::step, optim.cpp:21-57 ------- */
+/* *acc_dev += sum of squares of grad[0..n) (f64, fixed-order reduction);
+ * grad_dtype is moe_dtype.  Call once per tensor, in a fixed order, then
+ * moe_clip_scale: *scale_dev = clip / sqrt(*sq_dev) if clip > 0 and the norm
+ * exceeds it, else 1 (optim.cpp:26-37).  All stream-ordered on `stream`
+ * (a cudaStream_t, NULL = legacy default stream). */
+moe_status moe_grad_sqnorm(const void* grad, int64_t n, int grad_dtype, double* acc_dev, void* stream);
+moe_status moe_clip_scale(const double* sq_dev, double clip_norm, double* scale_dev, void* stream);
+/* One bias-corrected Adam update of one tensor (optim.cpp:38-55), `step` =
+ * the optimizer's step count after increment (1 for the first update).
+ * theta (fp32 master), m, v: fp32 [n], updated in place; grad: fp32 or bf16;
+ * theta_bf16 (nullable): bf16 copy of the new theta for the next forward;
+ * scale_dev (nullable): gradient scale from moe_clip_scale.  The update is
+ * evaluated in f64. */
+moe_status moe_adam_update(float* theta, float* m, float* v, const void* grad, int64_t n,
+                           int grad_dtype, void* theta_bf16, const double* scale_dev, double lr,
+                           double beta1, double beta2, double eps, int64_t step, void* stream);
+
 /* ---- per-stage entry points (routing.hpp:60-118) ----------------------- */
 /* gate_forward (routing.cpp:51-101): probs [T,E] fp32, choice [T*k] int32,
  * gate_prob [T*k] fp32.  x has the handle's dtype. */

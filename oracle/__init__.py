@@ -347,3 +347,58 @@ def layer_inputs(T, d, f, E, seed=42, xscale=1.0, gscale=None, wscale=None, bsca
     b2 = uniform(o.derive_seed(seed, "b2"), E * d, -bscale, bscale).reshape(E, d)
     dy = uniform(o.derive_seed(seed, "dy"), T * d, -1.0, 1.0).reshape(T, d)
     return x, gw, w1, b1, w2, b2, dy
+
+
+# ---------------------------------------------------------------------------
+# Expert optimizer step: AdamOptimizer, optim.cpp:10-57
+# ---------------------------------------------------------------------------
+def adam_restated(thetas, grads_per_step, lrs, clip=0.0, beta1=0.9, beta2=0.999, eps=1e-8):
+    """f64 restatement of AdamOptimizer::step (optim.cpp:21-57) applied
+    len(lrs) times.  thetas: list of flat arrays; grads_per_step[s][i] the
+    gradient of tensor i at step s.  Returns (thetas, ms, vs)."""
+    th = [np.array(t, np.float64, copy=True) for t in thetas]
+    m = [np.zeros_like(t) for t in th]
+    v = [np.zeros_like(t) for t in th]
+    for s, lr in enumerate(lrs):
+        if lr <= 0.0:
+            raise ValueError("adam: learning rate must be positive")       # optim.cpp:22-24
+        scale = 1.0
+        if clip > 0.0:                                                      # optim.cpp:26-37
+            sq = 0.0
+            for g in grads_per_step[s]:
+                for x in np.asarray(g, np.float64).ravel():                 # sequential order
+                    sq += x * x
+            norm = np.sqrt(sq)
+            if norm > clip:
+                scale = clip / norm
+        step = s + 1                                                        # optim.cpp:38
+        bc1 = 1.0 - beta1 ** step
+        bc2 = 1.0 - beta2 ** step
+        for i in range(len(th)):                                            # optim.cpp:41-55
+            g = np.asarray(grads_per_step[s][i], np.float64) * scale
+            m[i] = beta1 * m[i] + (1.0 - beta1) * g
+            v[i] = beta2 * v[i] + (1.0 - beta2) * g * g
+            th[i] = th[i] - lr * (m[i] / bc1) / (np.sqrt(v[i] / bc2) + eps)
+    return th, m, v
+
+
+def adam_reference(thetas, grads_per_step, lrs, clip=0.0, beta1=0.9, beta2=0.999, eps=1e-8):
+    """The reference's own AdamOptimizer (oracle/_ref), same contract."""
+    lib = reference().lib
+    fn = lib.ref_adam
+    fn.argtypes = [C.c_int, C.POINTER(C.c_int64), D, D, C.c_int, D, C.c_double, C.c_double,
+                   C.c_double, C.c_double, D, D]
+    n = len(thetas)
+    numel = np.array([np.asarray(t).size for t in thetas], np.int64)
+    th = np.ascontiguousarray(np.concatenate([np.asarray(t, np.float64).ravel() for t in thetas]))
+    gs = np.ascontiguousarray(np.stack([np.concatenate([np.asarray(g, np.float64).ravel() for g in gl])
+                                        for gl in grads_per_step]))
+    lr = np.ascontiguousarray(np.asarray(lrs, np.float64))
+    m = np.zeros_like(th)
+    v = np.zeros_like(th)
+    st = fn(n, numel.ctypes.data_as(C.POINTER(C.c_int64)), _p(th, C.c_double), _p(gs, C.c_double),
+            len(lrs), _p(lr, C.c_double), clip, beta1, beta2, eps, _p(m, C.c_double), _p(v, C.c_double))
+    if st:
+        raise OracleError(st, "ref_adam")
+    split = np.cumsum(numel)[:-1]
+    return np.split(th, split), np.split(m, split), np.split(v, split)

@@ -7,6 +7,8 @@
 // (moe_oracle.c) with golden vectors and (b) time the reference's CPU path
 // for bench.py --impl reference.  Signatures mirror moe_oracle.h.
 #include <moeforge/common.hpp>
+#include <moeforge/ops.hpp>
+#include <moeforge/optim.hpp>
 #include <moeforge/parallel.hpp>
 #include <moeforge/rng.hpp>
 #include <moeforge/routing.hpp>
@@ -241,6 +243,46 @@ double ref_time_layer_mt(const double* x, const double* gate_w, const double* w1
     for (int s : st)
         if (s) *status = s;
     return std::chrono::duration<double>(t1 - t0).count();
+}
+
+
+// AdamOptimizer (optim.cpp:10-57) on n flat leaves for `steps` steps; the
+// gradient of step s is grads[s] (concatenated), injected through
+// loss = sum_i dot_constant(theta_i, g_i) so backward() yields exactly g.
+// theta is updated in place; final moments are returned concatenated.
+int ref_adam(int n, const int64_t* numel, double* theta, const double* grads, int steps,
+             const double* lrs, double clip, double beta1, double beta2, double eps,
+             double* m_out, double* v_out) {
+    return guarded([&] {
+        std::vector<Tensor> params;
+        int64_t total = 0;
+        for (int i = 0; i < n; ++i) {
+            params.push_back(Tensor::leaf({numel[i]}, std::vector<double>(theta + total, theta + total + numel[i]), true));
+            total += numel[i];
+        }
+        AdamOptimizer opt(params, beta1, beta2, eps);
+        for (int s = 0; s < steps; ++s) {
+            opt.zero_grad();
+            Tensor loss = Tensor::scalar(0.0);
+            int64_t off = 0;
+            for (int i = 0; i < n; ++i) {
+                const double* g = grads + static_cast<int64_t>(s) * total + off;
+                loss = add(loss, dot_constant(params[i], std::span<const double>(g, static_cast<size_t>(numel[i]))));
+                off += numel[i];
+            }
+            loss.backward();
+            opt.step(lrs[s], clip);
+        }
+        int64_t off = 0;
+        for (int i = 0; i < n; ++i) {
+            auto d = params[i].leaf_data();
+            std::memcpy(theta + off, d.data(), sizeof(double) * d.size());
+            const auto& st = opt.state(static_cast<size_t>(i));
+            if (m_out) std::memcpy(m_out + off, st.m.data(), sizeof(double) * st.m.size());
+            if (v_out) std::memcpy(v_out + off, st.v.data(), sizeof(double) * st.v.size());
+            off += numel[i];
+        }
+    });
 }
 
 }  // extern "C"

@@ -217,3 +217,12 @@ void launch_gate_tc_dx(int64_t T, int d, int E, int K, int cap_pad, const float*
 void launch_gate2_dxg(int64_t T, int d, int E, const float* dL, const float* wgt, const float* noise,
                       float* dxg, cudaStream_t st);
 }  // namespace moe
+
+namespace moe {
+// optim.cu: AdamOptimizer::step on the device (optim.cpp:21-57)
+void launch_grad_sqnorm(const void* g, int64_t n, bool bf16, double* acc, cudaStream_t st);
+void launch_clip_scale(const double* sq, double clip, double* scale, cudaStream_t st);
+void launch_adam(float* theta, float* m, float* v, const void* g, int64_t n, bool g_bf16,
+                 __nv_bfloat16* shadow, const double* scale, double lr, double b1, double b2,
+                 double eps, int64_t step, cudaStream_t st);
+}  // namespace moe

@@ -904,6 +904,32 @@ moe_status moe_last_decision_stats(moe_handle* h, int* capacity, int64_t* drop_c
     });
 }
 
+moe_status moe_grad_sqnorm(const void* grad, int64_t n, int grad_dtype, double* acc_dev, void* stream) {
+    return guarded(nullptr, [&] {
+        require(grad && acc_dev && n >= 0, MOE_SHAPE, "grad_sqnorm: grad and acc required");
+        require(grad_dtype == MOE_F32 || grad_dtype == MOE_BF16, MOE_CONFIG, "grad_sqnorm: dtype");
+        launch_grad_sqnorm(grad, n, grad_dtype == MOE_BF16, acc_dev, static_cast<cudaStream_t>(stream));
+    });
+}
+moe_status moe_clip_scale(const double* sq_dev, double clip_norm, double* scale_dev, void* stream) {
+    return guarded(nullptr, [&] {
+        require(sq_dev && scale_dev, MOE_SHAPE, "clip_scale: sq and scale required");
+        launch_clip_scale(sq_dev, clip_norm, scale_dev, static_cast<cudaStream_t>(stream));
+    });
+}
+moe_status moe_adam_update(float* theta, float* m, float* v, const void* grad, int64_t n,
+                           int grad_dtype, void* theta_bf16, const double* scale_dev, double lr,
+                           double beta1, double beta2, double eps, int64_t step, void* stream) {
+    return guarded(nullptr, [&] {
+        // optim.cpp:22-24
+        require(lr > 0.0, MOE_CONFIG, "adam: learning rate must be positive");
+        require(theta && m && v && grad && n >= 0 && step >= 1, MOE_SHAPE, "adam: bad arguments");
+        require(grad_dtype == MOE_F32 || grad_dtype == MOE_BF16, MOE_CONFIG, "adam: grad dtype");
+        launch_adam(theta, m, v, grad, n, grad_dtype == MOE_BF16, static_cast<__nv_bfloat16*>(theta_bf16),
+                    scale_dev, lr, beta1, beta2, eps, step, static_cast<cudaStream_t>(stream));
+    });
+}
+
 moe_status moe_accumulate_decision_stats(moe_handle* h, int64_t* util_dev, int64_t* hist_dev) {
     if (!h) return MOE_SHAPE;
     return guarded(h, [&] {
