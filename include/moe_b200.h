@@ -239,6 +239,14 @@ moe_status moe_debug_gate_tc_dx(int64_t T, int d, int E, int K, int cap_pad, con
 /* ---- RNG streams (rng.cpp:15-102), host, bit-exact -------------------- */
 uint64_t moe_derive_seed_tag(uint64_t seed, const char* tag);
 uint64_t moe_derive_seed_u64(uint64_t seed, uint64_t salt);
+/* Rng(seed).permutation(n), rng.cpp:94-102 (prune_experts' random strategy,
+ * surgery.cpp:167-172; the RTS order), host. */
+moe_status moe_rng_permutation(uint64_t seed, int64_t n, uint32_t* out_host);
+
+/* ---- checkpoint -> device layout (checkpoint.cpp f64 records) ---------- */
+/* dst[i] = (dtype)src[i] for i < n, round-to-nearest-even; src and dst are
+ * device buffers (the f64 checkpoint record staged on the device). */
+moe_status moe_convert_f64(const double* src, int64_t n, int dtype, void* dst, void* stream);
 
 #ifdef __cplusplus
 }

@@ -402,3 +402,30 @@ def adam_reference(thetas, grads_per_step, lrs, clip=0.0, beta1=0.9, beta2=0.999
         raise OracleError(st, "ref_adam")
     split = np.cumsum(numel)[:-1]
     return np.split(th, split), np.split(m, split), np.split(v, split)
+
+
+# ---------------------------------------------------------------------------
+# Checkpoints: written and pruned by the reference's
+# own checkpoint.cpp / surgery.cpp (oracle/_ref) for the loader's parity tests.
+# ---------------------------------------------------------------------------
+def ref_save_toy_checkpoint(path, vocab=50, d_model=64, ffn_dim=128, enc_layers=2, dec_layers=2,
+                            heads=2, num_experts=8, moe_every=2, seed=7):
+    fn = reference().lib.ref_save_toy_checkpoint
+    fn.argtypes = [C.c_char_p, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int,
+                   C.c_int, C.c_uint64]
+    st = fn(str(path).encode(), vocab, d_model, ffn_dim, enc_layers, dec_layers, heads, num_experts,
+            moe_every, seed)
+    if st:
+        raise OracleError(st, "ref_save_toy_checkpoint")
+
+
+def ref_prune_checkpoint(src, dst, k, strategy="top_utilization", counts=None, seed=0):
+    fn = reference().lib.ref_prune_checkpoint
+    fn.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_int64), C.c_uint64]
+    cp = None
+    if counts is not None:
+        arr = np.ascontiguousarray(np.asarray(counts, np.int64))
+        cp = arr.ctypes.data_as(C.POINTER(C.c_int64))
+    st = fn(str(src).encode(), str(dst).encode(), k, 0 if strategy == "top_utilization" else 1, cp, seed)
+    if st:
+        raise OracleError(st, "ref_prune_checkpoint")

@@ -6,7 +6,10 @@
 // into oracle/_ref/libmoeforge_ref.so.  Used to (a) pin the C restatement
 // (moe_oracle.c) with golden vectors and (b) time the reference's CPU path
 // for bench.py --impl reference.  Signatures mirror moe_oracle.h.
+#include <moeforge/checkpoint.hpp>
 #include <moeforge/common.hpp>
+#include <moeforge/model.hpp>
+#include <moeforge/surgery.hpp>
 #include <moeforge/ops.hpp>
 #include <moeforge/optim.hpp>
 #include <moeforge/parallel.hpp>
@@ -282,6 +285,42 @@ int ref_adam(int n, const int64_t* numel, double* theta, const double* grads, in
             if (v_out) std::memcpy(v_out + off, st.v.data(), sizeof(double) * st.v.size());
             off += numel[i];
         }
+    });
+}
+
+// Checkpoint -> device layout pinning: a small
+// reference model built and saved by the reference itself, and its
+// prune_experts (surgery.cpp:135-212).
+int ref_save_toy_checkpoint(const char* dir, int64_t vocab, int64_t d_model, int64_t ffn_dim,
+                            int enc_layers, int dec_layers, int heads, int num_experts,
+                            int moe_every, uint64_t seed) {
+    return guarded([&] {
+        ArchConfig a = ArchConfig::toy(vocab, num_experts);
+        a.d_model = d_model;
+        a.ffn_dim = ffn_dim;
+        a.enc_layers = enc_layers;
+        a.dec_layers = dec_layers;
+        a.heads = heads;
+        a.moe_every = moe_every;
+        save_checkpoint(build_model(a, seed), dir);
+    });
+}
+
+// strategy 0 = top utilization (counts [num_moe_layers][E]), 1 = random(seed)
+int ref_prune_checkpoint(const char* dir_in, const char* dir_out, int k, int strategy,
+                         const int64_t* counts, uint64_t seed) {
+    return guarded([&] {
+        Checkpoint c = load_checkpoint(dir_in);
+        UtilizationCounts u;
+        const int L = c.arch.num_moe_layers(), E = c.arch.num_experts;
+        if (counts) {
+            u.per_layer.assign(static_cast<size_t>(L), std::vector<int64_t>(static_cast<size_t>(E)));
+            for (int l = 0; l < L; ++l)
+                for (int e = 0; e < E; ++e) u.per_layer[l][e] = counts[l * E + e];
+        }
+        Checkpoint p = prune_experts(c, k, strategy == 0 ? PruneStrategy::kTopUtilization : PruneStrategy::kRandom,
+                                     counts ? &u : nullptr, seed);
+        save_checkpoint(p, dir_out);
     });
 }
 

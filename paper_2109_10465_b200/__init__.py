@@ -12,5 +12,6 @@ from .routing import (KDROPPED, AssignmentMode, ConfigError, DispatchBuffer, Exp
                       assign_plain, assign_rts, balance_loss, capacity, combine, derive_seed,
                       dispatch, ep_unique_id, gate_forward, make_assignment, moe_layer_forward)
 from .stack import DropHistogram, MoeStack, UtilizationCounts
+from . import checkpoint, optim  # noqa: F401  (checkpoint -> device layout; Adam step)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

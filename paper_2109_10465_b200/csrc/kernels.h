@@ -226,3 +226,8 @@ void launch_adam(float* theta, float* m, float* v, const void* g, int64_t n, boo
                  __nv_bfloat16* shadow, const double* scale, double lr, double b1, double b2,
                  double eps, int64_t step, cudaStream_t st);
 }  // namespace moe
+
+namespace moe {
+// permute.cu: f64 checkpoint record -> fp32 / bf16 device tensor
+void launch_convert_f64(const double* src, int64_t n, bool bf16, void* dst, cudaStream_t st);
+}  // namespace moe

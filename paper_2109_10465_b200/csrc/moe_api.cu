@@ -739,6 +739,19 @@ moe_status moe_capacity(int64_t tokens, const moe_router_cfg* cfg, int phase, in
 
 uint64_t moe_derive_seed_tag(uint64_t seed, const char* tag) { return derive_seed_tag(seed, tag); }
 uint64_t moe_derive_seed_u64(uint64_t seed, uint64_t salt) { return derive_seed_u64(seed, salt); }
+moe_status moe_rng_permutation(uint64_t seed, int64_t n, uint32_t* out_host) {
+    return guarded(nullptr, [&] {
+        require(n >= 0 && (n == 0 || out_host), MOE_SHAPE, "permutation: output required");
+        moe::permutation(seed, n, out_host);
+    });
+}
+moe_status moe_convert_f64(const double* src, int64_t n, int dtype, void* dst, void* stream) {
+    return guarded(nullptr, [&] {
+        require(src && dst && n >= 0, MOE_SHAPE, "convert_f64: src and dst required");
+        require(dtype == MOE_F32 || dtype == MOE_BF16, MOE_CONFIG, "convert_f64: dtype");
+        launch_convert_f64(src, n, dtype == MOE_BF16, dst, static_cast<cudaStream_t>(stream));
+    });
+}
 
 moe_status moe_create(const moe_router_cfg* cfg, const moe_layer_dims* dims, moe_handle** out) {
     if (!cfg || !dims || !out) return MOE_SHAPE;

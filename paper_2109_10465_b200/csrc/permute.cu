@@ -380,6 +380,21 @@ void launch_colsum_parts(const float* part, int64_t N, int ep, int El, int cap_p
     MOE_LAUNCH_CHECK();
 }
 
+__global__ void convert_f64_kernel(const double* __restrict__ src, int64_t n, bool bf16, void* dst) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (bf16) static_cast<__nv_bfloat16*>(dst)[i] = __double2bfloat16(src[i]);
+        else static_cast<float*>(dst)[i] = __double2float_rn(src[i]);
+    }
+}
+
+void launch_convert_f64(const double* src, int64_t n, bool bf16, void* dst, cudaStream_t st) {
+    if (n <= 0) return;
+    convert_f64_kernel<<<(unsigned)std::min<int64_t>(8 * kNumSMs, ceil_div(n, (int64_t)256)), 256, 0, st>>>(
+        src, n, bf16, dst);
+    MOE_LAUNCH_CHECK();
+}
+
 // ---- reference-layout per-stage kernels ------------------------------------
 template <class TIO>
 __global__ void dispatch_ref_kernel(const TIO* __restrict__ x, int64_t T, int64_t d, int K,
