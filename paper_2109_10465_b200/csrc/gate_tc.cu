@@ -31,7 +31,8 @@ namespace gtc {
 
 using namespace tc;
 
-constexpr int NT = 128;  // 4 warps: producers, MMA issuer (thread 0), epilogue
+constexpr int NT = 128;   // logits, dx: 4 warps (epilogue rows = TMEM lanes)
+constexpr int NTS = 512;  // dWg: 16 warps stage and transform each K step
 constexpr int BM = 128;  // accumulator rows (TMEM lanes)
 constexpr int BK = 32;   // fp32 K elements per step = one 128 B swizzle row
 
@@ -120,6 +121,19 @@ __device__ __forceinline__ void publish_and_issue(uint64_t* bar, F issue) {
         tc_commit(bar);
     }
 }
+
+// ---- cp.async staging: each K step's raw operand bytes are copied global ->
+// shared by all threads with 16-byte cp.async (no registers held), kRaw
+// steps ahead of the transform, so ~3 steps of loads are in flight per CTA.
+constexpr int kRaw = 4;
+__device__ __forceinline__ void cp16(void* dst, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+                 "r"(valid ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // ============================================================== logits
 // CTA = 128 tokens x E experts, K range = one split of d.  A = x*noise
@@ -251,29 +265,31 @@ logits_kernel(const TX* __restrict__ x, const float* __restrict__ noise, const f
 
 // ============================================================== dWg
 // CTA = 128 j x E, K = the split's tokens.  A(j, t) = x[t][j] noise[t][j],
-// B(e, t) = dL[t][e], both K-major (t contiguous): each step's tiles are
-// loaded coalesced along j / e, staged row-major in shared memory and
-// written transposed into the swizzled operand layout.
+// B(e, t) = dL[t][e], both K-major (t contiguous): each step's raw tiles are
+// copied row-major (coalesced along j / e) and read transposed by the
+// transform into the swizzled operand layout.
 template <int E>
 struct DwSmem {
-    static constexpr int SA = BM + 4, SB = E + 4;  // staging row pitch (floats)
-    static constexpr uint32_t A = BM * 128;        // 128 rows x 128 B
+    static constexpr uint32_t RX = BK * BM * 2;   // raw x  [32 t][128 j] bf16  8 KB
+    static constexpr uint32_t RN = BK * BM * 4;   // raw n  [32][128] fp32     16 KB
+    static constexpr uint32_t RL = BK * E * 4;    // raw dL [32][E]  fp32       8 KB
+    static constexpr uint32_t raw = RX + RN + RL;
+    static constexpr uint32_t A = BM * 128;       // 128 rows x 128 B
     static constexpr uint32_t B = E * 128;
     static constexpr uint32_t buf = A + B;
-    static constexpr uint32_t stg = BK * (SA + SB) * 4;
-    static constexpr uint32_t bytes = 1024 + 2 * buf + stg + 256;
+    static constexpr uint32_t bytes = 1024 + 2 * buf + kRaw * raw + 256;
 };
 
 template <class TX, int E>
-__global__ void __launch_bounds__(NT, 2)
+__global__ void __launch_bounds__(NTS, 1)
 dw_kernel(const TX* __restrict__ x, const float* __restrict__ noise, const float* __restrict__ dL,
           float* __restrict__ part, int64_t T, int d, int64_t t_per_split) {
+    static_assert(sizeof(TX) == 2, "gate_tc dw: bf16 activations");
     using S = DwSmem<E>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    float* stA = reinterpret_cast<float*>(sm + 2 * S::buf);  // [BK][SA]
-    float* stB = stA + BK * S::SA;                           // [BK][SB]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + 2 * S::buf + S::stg);
+    uint8_t* raw = sm + 2 * S::buf;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(raw + kRaw * S::raw);
     uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
     const int tid = threadIdx.x;
     const int j0 = blockIdx.x * BM;
@@ -283,73 +299,69 @@ dw_kernel(const TX* __restrict__ x, const float* __restrict__ noise, const float
     part += (int64_t)blockIdx.y * d * E;
     const uint32_t tmem = setup(bars, 3, tslot, E < 32 ? 32 : E);
 
-    // loads: A lane jc = tid % 32 -> j = 4 jc.., token rows tid/32 + 4 i (i < 8);
-    //        B float4 q = tid + 128 i: token row q / (E/4), e4 = q % (E/4)
-    const int jc = tid & 31, tr = tid >> 5;
-    constexpr int NB = E / 16;
-    Raw4<TX> xa[8];
-    Raw4<float> na[8], lb[NB];
-    auto load = [&](int step) {
-        const int64_t k0 = tb + (int64_t)step * BK;
+    auto issue = [&](int step) {
+        if (step < nsteps) {
+            uint8_t* r = raw + (step % kRaw) * S::raw;
+            const int64_t k0 = tb + (int64_t)step * BK;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int64_t t = k0 + tr + 4 * i;
-            if (t < te) {
-                xa[i].load(x + t * d + j0 + 4 * jc);
-                if (noise) na[i].load(noise + t * d + j0 + 4 * jc);
-            } else {
-                xa[i].zero();
+            for (int i = 0; i < BK * 16 / NTS; ++i) {  // x: 32 rows x 16 chunks (8 bf16)
+                const int q = tid + NTS * i, row = q >> 4, c = q & 15;
+                const int64_t t = k0 + row;
+                cp16(r + row * 256 + c * 16, x + (t < te ? t : 0) * d + j0 + 8 * c, t < te);
+            }
+            if (noise) {
+#pragma unroll
+                for (int i = 0; i < BK * 32 / NTS; ++i) {  // noise: 32 rows x 32 chunks
+                    const int q = tid + NTS * i, row = q >> 5, c = q & 31;
+                    const int64_t t = k0 + row;
+                    cp16(r + S::RX + row * 512 + c * 16, noise + (t < te ? t : 0) * d + j0 + 4 * c, t < te);
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < E * 8 / NTS; ++i) {  // dL: 32 rows x E/4 chunks
+                const int q = tid + NTS * i, row = q / (E / 4), c = q % (E / 4);
+                const int64_t t = k0 + row;
+                cp16(r + S::RX + S::RN + row * (E * 4) + c * 16, dL + (t < te ? t : 0) * E + 4 * c, t < te);
             }
         }
-#pragma unroll
-        for (int i = 0; i < NB; ++i) {
-            const int q = tid + NT * i;
-            const int64_t t = k0 + q / (E / 4);
-            if (t < te) lb[i].load(dL + t * E + 4 * (q % (E / 4)));
-            else lb[i].zero();
-        }
+        cp_commit();
     };
-    auto stage = [&]() {  // registers -> row-major staging
+    auto store = [&](const uint8_t* r, uint8_t* buf) {  // raw (row-major) -> transposed, swizzled, tf32
+        const __nv_bfloat16* rx = reinterpret_cast<const __nv_bfloat16*>(r);
+        const float* rn = reinterpret_cast<const float*>(r + S::RX);
+        const float* rl = reinterpret_cast<const float*>(r + S::RX + S::RN);
+        const int j = tid % BM;  // A row; this thread's chunks c = tid/BM + (NTS/BM) i
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            float v[4], nv[4] = {1.f, 1.f, 1.f, 1.f};
-            xa[i].get(v);
-            if (noise) na[i].get(nv);
+        for (int c = tid / BM; c < 8; c += NTS / BM) {
+            float v[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) v[q] *= nv[q];
-            *reinterpret_cast<float4*>(stA + (tr + 4 * i) * S::SA + 4 * jc) = make_float4(v[0], v[1], v[2], v[3]);
+            for (int u = 0; u < 4; ++u) {
+                const int tt = 4 * c + u;
+                const float xv = __bfloat162float(rx[tt * BM + j]);
+                v[u] = tf32_rna(noise ? xv * rn[tt * BM + j] : xv);
+            }
+            st4(buf, swz(j, c), v[0], v[1], v[2], v[3]);
         }
-#pragma unroll
-        for (int i = 0; i < NB; ++i) {
-            const int q = tid + NT * i;
-            *reinterpret_cast<float4*>(stB + (q / (E / 4)) * S::SB + 4 * (q % (E / 4))) = lb[i].u;
-        }
-    };
-    auto store = [&](uint8_t* buf) {  // staging -> transposed, swizzled, tf32
-        const int j = tid;  // A row
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-            st4(buf, swz(j, c), tf32_rna(stA[(4 * c) * S::SA + j]), tf32_rna(stA[(4 * c + 1) * S::SA + j]),
-                tf32_rna(stA[(4 * c + 2) * S::SA + j]), tf32_rna(stA[(4 * c + 3) * S::SA + j]));
-        constexpr int RPT = E * 8 / NT;  // B chunks per thread
+        constexpr int RPT = E * 8 / NTS;  // B chunks per thread
 #pragma unroll
         for (int i = 0; i < RPT; ++i) {
-            const int q = tid + NT * i;
+            const int q = tid + NTS * i;
             const int e = q % E, c = q / E;
-            st4(buf + S::A, swz(e, c), tf32_rna(stB[(4 * c) * S::SB + e]), tf32_rna(stB[(4 * c + 1) * S::SB + e]),
-                tf32_rna(stB[(4 * c + 2) * S::SB + e]), tf32_rna(stB[(4 * c + 3) * S::SB + e]));
+            st4(buf + S::A, swz(e, c), tf32_rna(rl[(4 * c) * E + e]), tf32_rna(rl[(4 * c + 1) * E + e]),
+                tf32_rna(rl[(4 * c + 2) * E + e]), tf32_rna(rl[(4 * c + 3) * E + e]));
         }
     };
     constexpr uint32_t idesc = make_idesc_tf32(BM, E, 0, 0);
-    if (nsteps > 0) load(0);
+#pragma unroll
+    for (int s = 0; s < kRaw - 1; ++s) issue(s);
     for (int s = 0; s < nsteps; ++s) {
         const int b = s & 1;
         uint8_t* buf = sm + b * S::buf;
-        stage();
-        if (s + 1 < nsteps) load(s + 1);
+        issue(s + kRaw - 1);
+        cp_wait<kRaw - 1>();
         __syncthreads();
         if (s >= 2) mbar_wait(&bars[b], ((s - 2) >> 1) & 1);
-        store(buf);
+        store(raw + (s % kRaw) * S::raw, buf);
         publish_and_issue(&bars[b], [&] {
             const uint32_t a = smem_u32(buf), bb = a + S::A;
 #pragma unroll
@@ -358,15 +370,16 @@ dw_kernel(const TX* __restrict__ x, const float* __restrict__ noise, const float
                             (s | kk) ? 1u : 0u);
         });
     }
+    cp_wait<0>();
     if (tid == 0) tc_commit(&bars[2]);
     mbar_wait(&bars[2], 0);
     tc_fence_after();
     const int warp = tid >> 5, lane = tid & 31;
-    const int j = j0 + warp * 32 + lane;
-#pragma unroll
-    for (int c = 0; c < E; c += 32) {
+    const int quarter = warp & 3;
+    const int j = j0 + quarter * 32 + lane;
+    for (int c = 32 * (warp >> 2); c < E; c += 32 * (NTS / 128)) {
         uint32_t v[32];
-        tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + c, v);
+        tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + c, v);
         float* o = part + (int64_t)j * E + c;
 #pragma unroll
         for (int q = 0; q < 32; q += 4) {
@@ -567,7 +580,7 @@ void launch_gate_tc_dw(const TX* x, const float* noise, const float* dL, float* 
     if (!attr) { gtc::set_smem(k, gtc::DwSmem<kE>::bytes); attr = true; }
     const int64_t tps = round_up(ceil_div(T, (int64_t)splits), (int64_t)gtc::BK);
     dim3 grid((unsigned)(d / gtc::BM), (unsigned)splits);
-    k<<<grid, gtc::NT, gtc::DwSmem<kE>::bytes, st>>>(x, noise, dL, part, T, d, tps);
+    k<<<grid, gtc::NTS, gtc::DwSmem<kE>::bytes, st>>>(x, noise, dL, part, T, d, tps);
     MOE_LAUNCH_CHECK();
 }
 

@@ -596,11 +596,14 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
     h->mark("ffn2_wgrad");
     wgrad_gemm<TIO>(h, h->Xr.as<TIO>(), h->dH.as<TIO>(), dw1, d, f, counts, ep);
     h->mark("ffn1_wgrad");
+    // one CTA per SM: (d/128 column tiles) x splits <= 148
+    const int tc_dw_splits = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>({16, kNumSMs / std::max<int64_t>(1, d / 128), (T + 31) / 32})));
     if (gtc) {  // dWg = (x*noise)^T dL on the tensor cores, split-K + fixed-order reduce
         if constexpr (std::is_same<TIO, __nv_bfloat16>::value)
             launch_gate_tc_dw<TIO>(x, noise, h->dL.as<float>(), h->dwg_part.as<float>(), T,
-                                   static_cast<int>(d), E, dw_splits, st);
-        launch_splitk_reduce(h->dwg_part.as<float>(), dw_splits, d * E, dgate_w, st);
+                                   static_cast<int>(d), E, tc_dw_splits, st);
+        launch_splitk_reduce(h->dwg_part.as<float>(), tc_dw_splits, d * E, dgate_w, st);
         h->mark("gate_dw");
     }
     MOE_CUDA_CHECK(cudaStreamWaitEvent(st, h->ev_side, 0));

@@ -245,9 +245,14 @@ __device__ __forceinline__ uint64_t mix(uint64_t lo_word, uint64_t hi_word) {
 // with the r+1 = 5 neighbours from lane l+1, and lane 31 (j = 155, 311 only)
 // taking o[156] and new[0] from lane 0.
 __device__ __forceinline__ void warp_twist(uint64_t (&Aw)[5], uint64_t (&Bw)[5], int lane) {
+    // all cross-lane inputs are fetched up front (one batch of shuffles):
+    // lane 31 also rebuilds new[0] = mix(o[0], o[1]) ^ o[156] from lane 0's
+    // old words instead of waiting for lane 0's result
     const uint64_t a_next = __shfl_down_sync(0xffffffffu, Aw[0], 1);
     const uint64_t b_next = __shfl_down_sync(0xffffffffu, Bw[0], 1);
     const uint64_t o156 = __shfl_sync(0xffffffffu, Bw[0], 0);
+    const uint64_t o0 = __shfl_sync(0xffffffffu, Aw[0], 0);
+    const uint64_t o1 = __shfl_sync(0xffffffffu, Aw[1], 0);
     uint64_t nA[5];
 #pragma unroll
     for (int r = 0; r < 5; ++r) {
@@ -255,7 +260,7 @@ __device__ __forceinline__ void warp_twist(uint64_t (&Aw)[5], uint64_t (&Bw)[5],
         if (r == 0 && lane == 31) hi = o156;  // j = 155
         nA[r] = mix(Aw[r], hi) ^ Bw[r];
     }
-    const uint64_t new0 = __shfl_sync(0xffffffffu, nA[0], 0);
+    const uint64_t new0 = mix(o0, o1) ^ o156;
 #pragma unroll
     for (int r = 0; r < 5; ++r) {
         uint64_t hi = r < 4 ? Bw[r + 1] : b_next;

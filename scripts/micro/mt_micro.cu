@@ -27,8 +27,15 @@ __device__ __forceinline__ void warp_twist(uint64_t (&Aw)[5], uint64_t (&Bw)[5],
         Aw[r] = nA[r];
     }
 }
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __global__ void k_twist(int iters, int store, unsigned long long* out, uint64_t* sink) {
     __shared__ uint64_t ring[8 * 312];
+    __shared__ uint64_t bar[2];
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&bar[0])), "r"(store == 2 ? 32 : 1));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&bar[1])), "r"(1));
+    }
+    __syncthreads();
     const int lane = threadIdx.x & 31;
     if (threadIdx.x >= 32) return;
     uint64_t Aw[5], Bw[5];
@@ -42,6 +49,14 @@ __global__ void k_twist(int iters, int store, unsigned long long* out, uint64_t*
             for (int r = 0; r < 5; ++r)
                 if (lane * 5 + r < 156) { dst[r] = Aw[r]; dst[r + 156] = Bw[r]; }
             __syncwarp();
+            if (store == 2) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&bar[0])) : "memory");
+            if (store == 3 && lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&bar[0])) : "memory");
+            if (store == 4) {
+                uint32_t ok;
+                asm volatile("{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+                             : "=r"(ok) : "r"(su32(&bar[1])), "r"(1u) : "memory");
+                if (!ok) sink[0] = 1;
+            }
         }
     }
     long long t1 = clock64();
@@ -52,8 +67,8 @@ __global__ void k_twist(int iters, int store, unsigned long long* out, uint64_t*
 }
 int main() {
     unsigned long long* d; uint64_t* s; cudaMalloc(&d, 8); cudaMalloc(&s, 8 * 1024);
-    for (int store = 0; store < 2; ++store) {
-        for (int threads : {32, 768}) {
+    for (int store = 0; store < 5; ++store) {
+        for (int threads : {32}) {
             k_twist<<<1, threads>>>(1000, store, d, s);
             k_twist<<<1, threads>>>(10000, store, d, s);
             unsigned long long h; cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
