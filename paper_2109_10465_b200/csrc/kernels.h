@@ -187,6 +187,11 @@ struct PeerCopyJobs {
     int n;
 };
 void launch_peer_copy(const PeerCopyJobs& jobs, cudaStream_t st);
+struct PeerFlags {
+    unsigned long long* f[8];  // each rank's flag array, mapped into this process
+};
+void launch_ipc_barrier(const PeerFlags& peers, const unsigned long long* mine, int rank, int ep,
+                        unsigned long long epoch, cudaStream_t st);
 
 // gate2.cu: larger-tile gate GEMMs (require gate2_ok(d, E))
 bool gate2_ok(int d, int E);

@@ -145,10 +145,13 @@ struct moe_handle {
     cudaStream_t side = nullptr, comm_stream = nullptr;
     cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr, ev_side = nullptr, ev_comm = nullptr;
     // NVLink peer map (CUDA IPC) of the receive buffers: [buffer][rank]
-    enum { P_X = 0, P_O, P_DO, P_DX, P_CNT, P_NBUF };
+    enum { P_X = 0, P_O, P_DO, P_DX, P_CNT, P_FLAG, P_NBUF };
     bool ipc = false;
     void* peer[P_NBUF][8] = {};
-    DevMem bar;  // 1-int NCCL all-reduce used as the exchange barrier
+    DevMem bar;       // 1-int NCCL all-reduce (barrier fallback, MOE_B200_EP_BARRIER=nccl)
+    DevMem flags_ipc; // [8] u64 barrier flags, written by the peers over NVLink
+    unsigned long long epoch = 0;
+    bool nccl_barrier = false;
     ~moe_handle() {
         for (int b = 0; b < P_NBUF; ++b)
             for (int r = 0; r < 8; ++r)
@@ -263,12 +266,21 @@ void exchange(moe_handle* h, std::initializer_list<XSpec> specs) {
         }
     }
     launch_peer_copy(jobs, h->stream);
-    NCCL_CHECK(ncclAllReduce(h->bar.p, h->bar.p, 1, ncclInt32, ncclSum, h->comm, h->stream));
+    if (std::getenv("MOE_B200_PROFILE_BARRIER")) h->mark("xchg_copy");
+    if (h->nccl_barrier) {
+        NCCL_CHECK(ncclAllReduce(h->bar.p, h->bar.p, 1, ncclInt32, ncclSum, h->comm, h->stream));
+    } else {
+        PeerFlags pf{};
+        for (int r = 0; r < h->ep; ++r) pf.f[r] = static_cast<unsigned long long*>(h->peer[moe_handle::P_FLAG][r]);
+        launch_ipc_barrier(pf, h->flags_ipc.as<unsigned long long>(), h->rank, h->ep, ++h->epoch, h->stream);
+    }
 }
 
 void ipc_setup(moe_handle* h) {
     // export the receive buffers, all-gather the handles over NCCL, open peers'
-    void* bufs[moe_handle::P_NBUF] = {h->Xr.p, h->Oloc.p, h->dOr.p, h->dXloc.p, h->counts_r.p};
+    h->flags_ipc.alloc(8 * 16);
+    MOE_CUDA_CHECK(cudaMemset(h->flags_ipc.p, 0, 8 * 16));
+    void* bufs[moe_handle::P_NBUF] = {h->Xr.p, h->Oloc.p, h->dOr.p, h->dXloc.p, h->counts_r.p, h->flags_ipc.p};
     const size_t hs = sizeof(cudaIpcMemHandle_t);
     std::vector<cudaIpcMemHandle_t> mine(moe_handle::P_NBUF), all(moe_handle::P_NBUF * h->ep);
     for (int b = 0; b < moe_handle::P_NBUF; ++b) MOE_CUDA_CHECK(cudaIpcGetMemHandle(&mine[b], bufs[b]));
@@ -292,6 +304,11 @@ void ipc_setup(moe_handle* h) {
         }
     h->bar.alloc(16);
     MOE_CUDA_CHECK(cudaMemset(h->bar.p, 0, 16));
+    const char* bt = std::getenv("MOE_B200_EP_BARRIER");
+    h->nccl_barrier = bt && std::string(bt) == "nccl";
+    MOE_CUDA_CHECK(cudaDeviceSynchronize());  // flags zeroed everywhere before first use
+    NCCL_CHECK(ncclAllReduce(h->bar.p, h->bar.p, 1, ncclInt32, ncclSum, h->comm, h->stream));
+    MOE_CUDA_CHECK(cudaStreamSynchronize(h->stream));
     h->ipc = true;
 }
 

@@ -505,43 +505,66 @@ namespace moe {
 // (src, dst, bytes) jobs, dst typically a peer GPU's buffer mapped over
 // NVLink (CUDA IPC).  16-byte vectors, 4 in flight per thread, grid-stride
 // over the concatenation of all jobs.
-__global__ void __launch_bounds__(256) peer_copy_kernel(PeerCopyJobs jobs) {
-    int64_t total = 0;
-    for (int j = 0; j < jobs.n; ++j) total += jobs.bytes[j] >> 4;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < total; v += 4 * stride) {
-        uint4 buf[4];
-        int64_t idx[4];
-        int jj[4];
+// Each job (one destination slice) gets a contiguous range of CTAs in
+// proportion to its size; a CTA streams 16-byte vectors, 8 per thread in
+// flight, from local HBM to the (local or NVLink peer) destination.
+__global__ void __launch_bounds__(256) peer_copy_kernel(PeerCopyJobs jobs, int ctas_per_job) {
+    const int j = blockIdx.x / ctas_per_job;
+    if (j >= jobs.n) return;
+    const int64_t nv = jobs.bytes[j] >> 4;
+    const uint4* __restrict__ src = reinterpret_cast<const uint4*>(jobs.src[j]);
+    uint4* __restrict__ dst = reinterpret_cast<uint4*>(jobs.dst[j]);
+    const int64_t stride = (int64_t)ctas_per_job * blockDim.x;
+    constexpr int U = 8;
+    for (int64_t v = (int64_t)(blockIdx.x % ctas_per_job) * blockDim.x + threadIdx.x; v < nv; v += U * stride) {
+        uint4 buf[U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            int64_t w = v + u * stride;
-            jj[u] = -1;
-            if (w < total) {
-                int j = 0;
-                while (w >= (jobs.bytes[j] >> 4)) { w -= jobs.bytes[j] >> 4; ++j; }
-                jj[u] = j;
-                idx[u] = w;
-                buf[u] = __ldg(reinterpret_cast<const uint4*>(jobs.src[j]) + w);
-            }
-        }
+        for (int u = 0; u < U; ++u)
+            if (v + u * stride < nv) buf[u] = __ldg(src + v + u * stride);
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (jj[u] >= 0) reinterpret_cast<uint4*>(jobs.dst[jj[u]])[idx[u]] = buf[u];
+        for (int u = 0; u < U; ++u)
+            if (v + u * stride < nv) dst[v + u * stride] = buf[u];
     }
 }
 
 void launch_peer_copy(const PeerCopyJobs& jobs, cudaStream_t st) {
-    int64_t total = 0;
+    int64_t maxv = 0;
     for (int j = 0; j < jobs.n; ++j) {
         if ((jobs.bytes[j] & 15) || (reinterpret_cast<uintptr_t>(jobs.src[j]) & 15) ||
             (reinterpret_cast<uintptr_t>(jobs.dst[j]) & 15))
             throw Status(1, "peer copy: 16-byte alignment required");
-        total += jobs.bytes[j] >> 4;
+        maxv = std::max<int64_t>(maxv, jobs.bytes[j] >> 4);
     }
-    if (total == 0) return;
-    const int grid = (int)std::min<int64_t>(4 * kNumSMs, ceil_div(total, 256 * 4));
-    peer_copy_kernel<<<grid, 256, 0, st>>>(jobs);
+    if (maxv == 0 || jobs.n == 0) return;
+    const int per = (int)std::max<int64_t>(1, std::min<int64_t>(4 * kNumSMs / jobs.n, ceil_div(maxv, (int64_t)256 * 8)));
+    peer_copy_kernel<<<per * jobs.n, 256, 0, st>>>(jobs, per);
+    MOE_LAUNCH_CHECK();
+}
+
+// Device-side barrier over NVLink peer memory for the IPC exchanges: every
+// rank stores `epoch` into its slot of every peer's flag array (release,
+// system scope, after a system fence so the preceding copy kernel's peer
+// stores are ordered before it), then waits until every slot of its own array
+// has reached `epoch` (acquire).  One warp; a ~30 s clock budget traps
+// instead of hanging forever if a peer never arrives.
+__global__ void ipc_barrier_kernel(PeerFlags peers, const unsigned long long* mine, int rank, int ep,
+                                   unsigned long long epoch) {
+    const int i = threadIdx.x;
+    if (i < ep) {
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(peers.f[i] + rank), "l"(epoch) : "memory");
+        unsigned long long v;
+        const long long t0 = clock64();
+        do {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine + i) : "memory");
+            if (clock64() - t0 > (1LL << 36)) __trap();
+        } while (v < epoch);
+    }
+}
+
+void launch_ipc_barrier(const PeerFlags& peers, const unsigned long long* mine, int rank, int ep,
+                        unsigned long long epoch, cudaStream_t st) {
+    ipc_barrier_kernel<<<1, 32, 0, st>>>(peers, mine, rank, ep, epoch);
     MOE_LAUNCH_CHECK();
 }
 
