@@ -157,7 +157,7 @@ logits_kernel(const TX* __restrict__ x, const float* __restrict__ noise, const f
               float* __restrict__ out, int64_t T, int d, int k_per_split) {
     using S = LogitsSmem<E>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + 2 * S::buf);  // [2] per-buffer MMA done, [2] final
     uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
     const int tid = threadIdx.x;
@@ -287,7 +287,7 @@ dw_kernel(const TX* __restrict__ x, const float* __restrict__ noise, const float
     static_assert(sizeof(TX) == 2, "gate_tc dw: bf16 activations");
     using S = DwSmem<E>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
     uint8_t* raw = sm + 2 * S::buf;
     uint64_t* bars = reinterpret_cast<uint64_t*>(raw + kRaw * S::raw);
     uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
@@ -414,7 +414,7 @@ dx_kernel(int64_t T, int d, int K, int cap_pad, const float* __restrict__ dL, co
     static_assert(sizeof(TIO) == 2, "gate_tc dx: bf16 tensors");
     using S = DxSmem<E>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + S::steps * (S::A + S::B));
     uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
     const int tid = threadIdx.x;

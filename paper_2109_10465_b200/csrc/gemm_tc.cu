@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kThreads, 1) grouped_gemm_kernel(const __grid_
     constexpr int kEpiBufs = KCfg<KIND>::epi_bufs;
     constexpr uint32_t kEpiBytes = KCfg<KIND>::epi_bytes;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
     uint8_t* tiles = smem;
     uint8_t* cstage = smem + kStages * kStageBytes;  // [4 warps][2][4 KB]
     uint8_t* misc = cstage + kEpiBytes;
@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(kThreads, 1) grouped_gemm_kernel(const __grid_
                     __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
 #pragma unroll
                     for (int j = 0; j < 4; ++j) h2[j] = __floats2bfloat162_rn(f[q * 8 + 2 * j], f[q * 8 + 2 * j + 1]);
-                    *reinterpret_cast<uint4*>(sbuf + lane * 128 + ((q ^ (lane & 7)) << 4)) = u;
+                    sts128(smem_u32(sbuf) + lane * 128 + ((q ^ (lane & 7)) << 4), u);
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
@@ -516,7 +516,7 @@ template <int KIND>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 gemm2_kernel(const __grid_constant__ Params p) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
     uint8_t* tiles = smem;
     uint8_t* cstage = smem + kStages * kStage;
     uint8_t* misc = cstage + kEpi;
@@ -781,7 +781,7 @@ gemm2_kernel(const __grid_constant__ Params p) {
                     __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
 #pragma unroll
                     for (int j = 0; j < 4; ++j) h2[j] = __floats2bfloat162_rn(f[q * 8 + 2 * j], f[q * 8 + 2 * j + 1]);
-                    *reinterpret_cast<uint4*>(sbuf + lane * 128 + ((q ^ (lane & 7)) << 4)) = u;
+                    sts128(smem_u32(sbuf) + lane * 128 + ((q ^ (lane & 7)) << 4), u);
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
