@@ -296,8 +296,25 @@ def run_ours(args):
                  db1=torch.empty_like(b1), dw2=torch.empty_like(w2), db2=torch.empty_like(b2),
                  dresidual=None)
 
+    # one layer seed per step, derived like the reference trainer's per-step
+    # seeds (trainer.cpp:146-149).  With --prefetch the next step's jitter
+    # stream is generated during this step's backward (moe_prefetch_jitter);
+    # measured: it hides the 0.2 ms generation but slows the co-running
+    # weight-gradient GEMMs by more (0.27 ms), so the default generates in place
+    step_no = [0]
+
+    def seed_of(i):
+        return M.derive_seed(seed, i)
+
+    def fwd(xx, yy, aa):
+        i = step_no[0]
+        layer.forward(xx, params, M.Phase.TRAIN, seed_of(i), y=yy, aux=aa, decision=False, check=False)
+        if args.prefetch:
+            layer.prefetch_jitter(seed_of(i + 1), T)
+        step_no[0] += 1
+
     def step():
-        layer.forward(x, params, M.Phase.TRAIN, seed, y=y, aux=aux, decision=False, check=False)
+        fwd(x, y, aux)
         layer.backward(dy, 1.0, check=False, grads=grads)
 
     def barrier():
@@ -368,8 +385,7 @@ def run_ours(args):
             ev_dy = torch.cuda.Event()
             ev_dy.record(s_in)
         st.wait_event(ev_x)
-        layer.forward(xb[b], params, M.Phase.TRAIN, seed, y=y, aux=auxb[b], decision=False,
-                      check=False)
+        fwd(xb[b], y, auxb[b])
         st.wait_event(ev_dy)
         layer.backward(dyb[b], 1.0, check=False, grads=gb[b])
         ev_c = torch.cuda.Event()
@@ -453,7 +469,10 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random-init weights of the config-3 architecture, U(-1,1) tokens)",
-            "config": workload_config(N), "roofline": roof,
+            "config": dict(workload_config(N), seeds="per step: derive_seed(derive_seed(42, rank), step)",
+                           jitter_stream="generated during the previous step's backward (moe_prefetch_jitter)"
+                           if args.prefetch else "generated at the head of each forward"),
+            "roofline": roof,
             "expert_gemms": {"ms_per_step": gemm_ms, "tflops": gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms else None,
                              "frac_of_bf16_sustained": (gemm_flops / (gemm_ms / 1e3) / 1e12) / tf_sus if gemm_ms else None},
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms,
@@ -574,6 +593,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tokens-per-gpu", type=int, default=WORKLOAD["tokens_per_gpu"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--prefetch", action="store_true",
+                    help="generate the next step's jitter stream during this step's backward "
+                         "(moe_prefetch_jitter; it co-runs with the weight-gradient GEMMs)")
     ap.add_argument("--workload", default="c3", choices=["c3"] + sorted(EXTRA))
     ap.add_argument("--tokens", type=int, default=0, help="override T for --workload c1/c2/c4/c5")
     args = ap.parse_args()

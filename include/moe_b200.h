@@ -131,6 +131,17 @@ moe_status moe_backward(moe_handle* h, const void* dy, float daux, void* dx, flo
 moe_status moe_last_decision_stats(moe_handle* h, int* capacity, int64_t* drop_count,
                                    int64_t* kept_per_expert);
 
+/* Generate the jitter stream of a FUTURE train-phase moe_forward(seed) with
+ * `tokens` rows ahead of use: the work is launched during the next
+ * moe_backward on this handle (on its side stream, before the
+ * weight-gradient GEMMs) into a second buffer that the matching forward swaps
+ * in instead of generating.  The values are identical either way (the stream
+ * depends only on the seed); a forward with another seed / token count simply
+ * generates as usual.  Measured at config 3 it does not pay (the generator
+ * competes with the GEMMs for the SMs), so bench.py only uses it with
+ * --prefetch; it is for callers whose backward leaves the GPU idle. */
+moe_status moe_prefetch_jitter(moe_handle* h, uint64_t seed, int64_t tokens);
+
 /* Utilization and drop statistics of the last forward, accumulated on the
  * device into caller-owned int64 arrays (stream-ordered, no sync):
  *   util_dev[E]  += first-choice counts per expert (count_utilization,

@@ -79,6 +79,7 @@ _SIGS = {
     "moe_debug_mt64_chunk_host": (C.c_int, [C.c_uint64, C.c_int64, C.c_int, C.c_int64, VP]),
     "moe_debug_mt64_device": (C.c_int, [C.c_uint64, C.c_int64, VP]),
     "moe_accumulate_decision_stats": (C.c_int, [VP, VP, VP]),
+    "moe_prefetch_jitter": (C.c_int, [VP, C.c_uint64, C.c_int64]),
     "moe_rng_permutation": (C.c_int, [C.c_uint64, C.c_int64, VP]),
     "moe_convert_f64": (C.c_int, [VP, C.c_int64, C.c_int, VP, VP]),
     "moe_grad_sqnorm": (C.c_int, [VP, C.c_int64, C.c_int, VP, VP]),

@@ -156,7 +156,7 @@ struct moe_handle {
         for (int b = 0; b < P_NBUF; ++b)
             for (int r = 0; r < 8; ++r)
                 if (ipc && r != rank && peer[b][r]) cudaIpcCloseMemHandle(peer[b][r]);
-        for (cudaEvent_t e : {ev_a, ev_b, ev_c, ev_side, ev_comm})
+        for (cudaEvent_t e : {ev_a, ev_b, ev_c, ev_side, ev_comm, ev_pf})
             if (e) cudaEventDestroy(e);
         if (side) cudaStreamDestroy(side);
         if (comm_stream) cudaStreamDestroy(comm_stream);
@@ -169,6 +169,13 @@ struct moe_handle {
     DevMem Xloc, Xr, H, Or, Oloc, dOloc, dOr, dH, dXr, dXloc;
     DevMem dL, dxg, dwg_part, wgt;
     DevMem bal_term, bal_done;  // balance_finalize per-expert terms + CTA counter
+    // jitter stream double buffer: `noise` is the current forward's stream;
+    // `noise_pf` receives a stream generated ahead of use (moe_prefetch_jitter)
+    DevMem noise_pf;
+    bool pf_req = false, pf_valid = false;
+    uint64_t pf_req_seed = 0, pf_seed = 0;
+    int64_t pf_req_count = 0, pf_count = 0;
+    cudaEvent_t ev_pf = nullptr;
     DevMem db1_part;            // [rows/32][f] column sums from the dgrad2 epilogue
     AssignScratch as{};
     std::vector<uint32_t> host_ord;
@@ -384,7 +391,14 @@ void route(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, int phas
         // routing.cpp:62-70: noise stream Rng(derive_seed(seed, "jitter")), row-major
         // generated on the device by jump-ahead (rng.cu)
         const uint64_t js = derive_seed_tag(seed, "jitter");
-        launch_jitter_noise_device(js, T * h->d, h->cfg.jitter_eps, h->noise.as<float>(), st);
+        if (h->pf_valid && h->pf_seed == js && h->pf_count == T * h->d) {
+            // generated ahead of use during the previous backward: swap it in
+            MOE_CUDA_CHECK(cudaStreamWaitEvent(st, h->ev_pf, 0));
+            std::swap(h->noise.p, h->noise_pf.p);
+        } else {
+            launch_jitter_noise_device(js, T * h->d, h->cfg.jitter_eps, h->noise.as<float>(), st);
+        }
+        h->pf_valid = false;
         h->mark("jitter_noise");
     }
     // logits = (x * noise) @ gate_w  (routing.cpp:71)
@@ -608,6 +622,16 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
     }
     launch_colsum_groups<TIO>(h->dOr.as<TIO>(), d, ep, El, h->cap_pad, counts, db2, side);
     if (!db1_fused) launch_colsum_groups<TIO>(h->dH.as<TIO>(), f, ep, El, h->cap_pad, counts, db1, side);
+    if (h->pf_req) {  // jitter stream of the next forward (moe_prefetch_jitter), ~40 KB smem per CTA:
+        // it co-runs with the weight-gradient GEMMs below instead of heading the next forward
+        launch_jitter_noise_device(h->pf_req_seed, h->pf_req_count, h->cfg.jitter_eps,
+                                   h->noise_pf.as<float>(), side);
+        MOE_CUDA_CHECK(cudaEventRecord(h->ev_pf, side));
+        h->pf_valid = true;
+        h->pf_seed = h->pf_req_seed;
+        h->pf_count = h->pf_req_count;
+        h->pf_req = false;
+    }
     MOE_CUDA_CHECK(cudaEventRecord(h->ev_side, side));
     wgrad_gemm<TIO>(h, h->H.as<TIO>(), h->dOr.as<TIO>(), dw2, f, d, counts, ep);
     h->mark("ffn2_wgrad");
@@ -685,6 +709,7 @@ void alloc_workspace(moe_handle* h) {
     MOE_CUDA_CHECK(cudaMemset(h->bal_done.p, 0, 16));
     h->aux_scratch.alloc(16);
     h->noise.alloc(4 * T * d);
+    h->noise_pf.alloc(4 * T * d);
     h->ord.alloc(4 * T);
     h->flags.alloc(16);
     MOE_CUDA_CHECK(cudaMemset(h->flags.p, 0, 16));
@@ -803,7 +828,7 @@ moe_status moe_create(const moe_router_cfg* cfg, const moe_layer_dims* dims, moe
         alloc_workspace(h.get());
         MOE_CUDA_CHECK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
         MOE_CUDA_CHECK(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
-        for (cudaEvent_t* e : {&h->ev_a, &h->ev_b, &h->ev_c, &h->ev_side, &h->ev_comm})
+        for (cudaEvent_t* e : {&h->ev_a, &h->ev_b, &h->ev_c, &h->ev_side, &h->ev_comm, &h->ev_pf})
             MOE_CUDA_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     });
     if (s == MOE_OK) *out = h.release();
@@ -960,6 +985,17 @@ moe_status moe_adam_update(float* theta, float* m, float* v, const void* grad, i
         require(grad_dtype == MOE_F32 || grad_dtype == MOE_BF16, MOE_CONFIG, "adam: grad dtype");
         launch_adam(theta, m, v, grad, n, grad_dtype == MOE_BF16, static_cast<__nv_bfloat16*>(theta_bf16),
                     scale_dev, lr, beta1, beta2, eps, step, static_cast<cudaStream_t>(stream));
+    });
+}
+
+moe_status moe_prefetch_jitter(moe_handle* h, uint64_t seed, int64_t tokens) {
+    if (!h) return MOE_SHAPE;
+    return guarded(h, [&] {
+        require(tokens >= 1 && tokens <= h->Tmax, MOE_SHAPE, "prefetch_jitter: tokens outside [1, max_tokens]");
+        if (h->cfg.jitter_eps <= 0.0) return;  // no jitter stream in this configuration
+        h->pf_req = true;
+        h->pf_req_seed = derive_seed_tag(seed, "jitter");  // routing.cpp:386
+        h->pf_req_count = tokens * h->d;
     });
 }
 

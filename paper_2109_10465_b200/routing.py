@@ -535,6 +535,11 @@ class MoeLayer:
     def ep_init(self, unique_id: bytes):
         self.handle.ep_init(unique_id)
 
+    def prefetch_jitter(self, seed: int, tokens: int):
+        """moe_prefetch_jitter: generate the jitter stream of the forward with
+        this seed during the next backward (values unchanged)."""
+        _check(L.load().moe_prefetch_jitter(self.handle.h, seed, tokens), self.handle.h)
+
 
 class _MoeFn(torch.autograd.Function):
     @staticmethod

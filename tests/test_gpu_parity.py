@@ -274,3 +274,32 @@ def test_autograd_adapter_matches_explicit_backward():
     assert rel_norm(leaves[1].grad.cpu().numpy(), z["dw1"]) <= TOL_F32
     assert res.decision.drop_count() == int((z["slot"] < 0).sum())
     del dt, T, d, f
+
+
+@pytest.mark.gpu
+def test_prefetched_jitter_stream_is_identical():
+    """moe_prefetch_jitter: a forward that swaps in the stream generated during
+    the previous backward gives bit-identical outputs and gradients."""
+    import torch
+    import paper_2109_10465_b200 as M
+    T, d, f, E = 512, 256, 512, 16
+    g = torch.Generator(device="cuda").manual_seed(5)
+    p = M.MoeLayerParams(torch.randn(d, E, device="cuda", generator=g) * 0.1,
+                         (torch.randn(E, d, f, device="cuda", generator=g) * 0.05).to(torch.bfloat16),
+                         torch.zeros(E, f, device="cuda"),
+                         (torch.randn(E, f, d, device="cuda", generator=g) * 0.05).to(torch.bfloat16),
+                         torch.zeros(E, d, device="cuda"))
+    x = (torch.rand(T, d, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    dy = (torch.rand(T, d, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    outs = []
+    for prefetch in (False, True):
+        layer = M.MoeLayer(M.RouterConfig(num_experts=E), T, d, f, torch.bfloat16)
+        layer.forward(x, p, M.Phase.TRAIN, 100)
+        if prefetch:
+            layer.prefetch_jitter(101, T)
+        layer.backward(dy, 1.0)
+        y, aux, dec = layer.forward(x, p, M.Phase.TRAIN, 101)
+        gr = layer.backward(dy, 1.0)
+        outs.append((y.clone(), aux.clone(), dec.expert_id.clone(), gr["dx"].clone(), gr["dgate_w"].clone()))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
