@@ -192,6 +192,8 @@ struct PeerFlags {
 };
 void launch_ipc_barrier(const PeerFlags& peers, const unsigned long long* mine, int rank, int ep,
                         unsigned long long epoch, cudaStream_t st);
+// out = sum over ranks of src[r] (fixed rank order), n % 4 == 0
+void launch_sum_ranks(const float* const* srcs, int ep, int64_t n, float* out, cudaStream_t st);
 
 // gate2.cu: larger-tile gate GEMMs (require gate2_ok(d, E))
 bool gate2_ok(int d, int E);

@@ -145,11 +145,12 @@ struct moe_handle {
     cudaStream_t side = nullptr, comm_stream = nullptr;
     cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr, ev_side = nullptr, ev_comm = nullptr;
     // NVLink peer map (CUDA IPC) of the receive buffers: [buffer][rank]
-    enum { P_X = 0, P_O, P_DO, P_DX, P_CNT, P_FLAG, P_NBUF };
+    enum { P_X = 0, P_O, P_DO, P_DX, P_CNT, P_FLAG, P_DWG, P_NBUF };
     bool ipc = false;
     void* peer[P_NBUF][8] = {};
     DevMem bar;       // 1-int NCCL all-reduce (barrier fallback, MOE_B200_EP_BARRIER=nccl)
     DevMem flags_ipc; // [8] u64 barrier flags, written by the peers over NVLink
+    DevMem dwg_x;     // [d*E] fp32 staging of this rank's dWg for the fixed-order sum over ranks
     unsigned long long epoch = 0;
     bool nccl_barrier = false;
     ~moe_handle() {
@@ -253,7 +254,7 @@ struct XSpec {
     size_t esz;
 };
 
-void exchange(moe_handle* h, std::initializer_list<XSpec> specs) {
+void exchange(moe_handle* h, std::initializer_list<XSpec> specs, bool local_only = false) {
     if (!h->ipc) {
         NCCL_CHECK(ncclGroupStart());
         for (const XSpec& x : specs) all_to_all(h, x.send, x.recv, x.chunk_elems, x.ty, x.esz);
@@ -264,6 +265,13 @@ void exchange(moe_handle* h, std::initializer_list<XSpec> specs) {
     jobs.n = 0;
     for (const XSpec& x : specs) {
         const size_t bytes = x.chunk_elems * x.esz;
+        if (local_only) {  // publish this rank's buffer in its own exported slot, then barrier
+            jobs.src[jobs.n] = x.send;
+            jobs.dst[jobs.n] = x.recv;
+            jobs.bytes[jobs.n] = static_cast<int64_t>(bytes);
+            ++jobs.n;
+            continue;
+        }
         for (int s = 0; s < h->ep; ++s) {
             jobs.src[jobs.n] = static_cast<const char*>(x.send) + s * bytes;
             char* dst = s == h->rank ? static_cast<char*>(x.recv) : static_cast<char*>(h->peer[x.buf][s]);
@@ -287,7 +295,9 @@ void ipc_setup(moe_handle* h) {
     // export the receive buffers, all-gather the handles over NCCL, open peers'
     h->flags_ipc.alloc(8 * 16);
     MOE_CUDA_CHECK(cudaMemset(h->flags_ipc.p, 0, 8 * 16));
-    void* bufs[moe_handle::P_NBUF] = {h->Xr.p, h->Oloc.p, h->dOr.p, h->dXloc.p, h->counts_r.p, h->flags_ipc.p};
+    h->dwg_x.alloc(4 * static_cast<size_t>(h->d) * h->E);
+    void* bufs[moe_handle::P_NBUF] = {h->Xr.p,          h->Oloc.p,      h->dOr.p,    h->dXloc.p,
+                                      h->counts_r.p,    h->flags_ipc.p, h->dwg_x.p};
     const size_t hs = sizeof(cudaIpcMemHandle_t);
     std::vector<cudaIpcMemHandle_t> mine(moe_handle::P_NBUF), all(moe_handle::P_NBUF * h->ep);
     for (int b = 0; b < moe_handle::P_NBUF; ++b) MOE_CUDA_CHECK(cudaIpcGetMemHandle(&mine[b], bufs[b]));
@@ -650,10 +660,23 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
     MOE_CUDA_CHECK(cudaStreamWaitEvent(st, h->ev_side, 0));
     if (ep > 1) MOE_CUDA_CHECK(cudaStreamWaitEvent(st, h->ev_comm, 0));
     h->mark("bwd_join");
-    if (ep > 1) {
-        NCCL_CHECK(ncclAllReduce(dgate_w, dgate_w, static_cast<size_t>(d * E), ncclFloat32, ncclSum,
-                                 h->comm, st));
-        h->mark("allreduce_dgate_w");
+    if (ep > 1) {  // the gate is replicated: sum dWg over ranks on the comm stream, next to gate_dx
+        MOE_CUDA_CHECK(cudaEventRecord(h->ev_c, st));
+        MOE_CUDA_CHECK(cudaStreamWaitEvent(h->comm_stream, h->ev_c, 0));
+        if (h->ipc) {  // stage, barrier, every rank sums all ranks' copies in rank order (deterministic)
+            cudaStream_t saved = h->stream;
+            h->stream = h->comm_stream;
+            exchange(h, {{dgate_w, h->dwg_x.p, moe_handle::P_DWG, static_cast<size_t>(d * E), ncclFloat32, 4}},
+                     /*local_only=*/true);
+            h->stream = saved;
+            const float* srcs[8] = {};
+            for (int r = 0; r < ep; ++r) srcs[r] = static_cast<const float*>(h->peer[moe_handle::P_DWG][r]);
+            launch_sum_ranks(srcs, ep, d * E, dgate_w, h->comm_stream);
+        } else {
+            NCCL_CHECK(ncclAllReduce(dgate_w, dgate_w, static_cast<size_t>(d * E), ncclFloat32, ncclSum,
+                                     h->comm, h->comm_stream));
+        }
+        MOE_CUDA_CHECK(cudaEventRecord(h->ev_comm, h->comm_stream));
     }
     if (gtc) {  // dx = (dL Wg^T) * noise + dispatch bwd + residual, one tensor-core kernel
         if constexpr (std::is_same<TIO, __nv_bfloat16>::value)
@@ -676,6 +699,10 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
                                 !h->has_residual, dx, dres, st);
     }
     h->mark("gate_dx");
+    if (ep > 1) {
+        MOE_CUDA_CHECK(cudaStreamWaitEvent(st, h->ev_comm, 0));
+        h->mark("allreduce_dgate_w");
+    }
 }
 
 void alloc_workspace(moe_handle* h) {

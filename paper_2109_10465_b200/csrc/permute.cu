@@ -541,6 +541,31 @@ void launch_peer_copy(const PeerCopyJobs& jobs, cudaStream_t st) {
     MOE_LAUNCH_CHECK();
 }
 
+// out[i] = sum_r src[r][i] over the ranks' (NVLink-mapped) copies, in rank
+// order: every rank computes the identical fp32 sum.
+struct RankSrcs {
+    const float* p[8];
+};
+__global__ void sum_ranks_kernel(RankSrcs s, int ep, int64_t n, float* __restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n / 4; i += (int64_t)gridDim.x * blockDim.x) {
+        float4 acc = reinterpret_cast<const float4*>(s.p[0])[i];
+        for (int r = 1; r < ep; ++r) {
+            const float4 v = reinterpret_cast<const float4*>(s.p[r])[i];
+            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+        reinterpret_cast<float4*>(out)[i] = acc;
+    }
+}
+
+void launch_sum_ranks(const float* const* srcs, int ep, int64_t n, float* out, cudaStream_t st) {
+    if (n % 4) throw Status(1, "sum_ranks: element count must be a multiple of 4");
+    RankSrcs s{};
+    for (int r = 0; r < ep; ++r) s.p[r] = srcs[r];
+    sum_ranks_kernel<<<(unsigned)std::min<int64_t>(2 * kNumSMs, ceil_div(n / 4, (int64_t)256)), 256, 0, st>>>(
+        s, ep, n, out);
+    MOE_LAUNCH_CHECK();
+}
+
 // Device-side barrier over NVLink peer memory for the IPC exchanges: every
 // rank stores `epoch` into its slot of every peer's flag array (release,
 // system scope, after a system fence so the preceding copy kernel's peer
