@@ -25,8 +25,11 @@ namespace moe {
 constexpr int kSoftmaxWarps = 8;
 constexpr int kRowsPerPart = 2 * kSoftmaxWarps;  // token rows per CTA (2 per warp)
 
+// NL = logits per lane (E <= 32 NL), NS = split-K partial arrays: both
+// compile-time so every row's loads are issued together.
+template <int NL, int NS>
 __global__ void __launch_bounds__(kSoftmaxWarps * 32)
-softmax_topk_kernel(const float* __restrict__ logits, int nsplit, int64_t T, int E, int K,
+softmax_topk_kernel(const float* __restrict__ logits, int64_t T, int E, int K,
                     float* __restrict__ probs, int32_t* __restrict__ choice,
                     float* __restrict__ gate_prob, float* __restrict__ colsum_part,
                     int32_t* __restrict__ count_part, uint32_t* __restrict__ flags) {
@@ -43,28 +46,39 @@ softmax_topk_kernel(const float* __restrict__ logits, int nsplit, int64_t T, int
     const int64_t t0 = (int64_t)blockIdx.x * rows_per_cta;
     for (int64_t t = t0 + warp; t < min(T, t0 + rows_per_cta); t += kSoftmaxWarps) {
         const float* Lp = logits + t * E;
-        auto lg = [&](int e) {  // split-K partials summed in fixed order
-            float v = Lp[e];
-            for (int s = 1; s < nsplit; ++s) v += Lp[s * TE + e];
-            return v;
-        };
-        float L[8];  // E <= 256: at most 8 logits per lane
-        const int nl = (E + 31) / 32;
+        float part[NL][NS];  // split-K partials, loaded together, summed in fixed order
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-            if (q < nl && lane + 32 * q < E) L[q] = lg(lane + 32 * q);
+        for (int q = 0; q < NL; ++q)
+#pragma unroll
+            for (int s2 = 0; s2 < NS; ++s2)
+                part[q][s2] = lane + 32 * q < E ? __ldg(Lp + s2 * TE + lane + 32 * q) : 0.f;
+        float L[NL];
+#pragma unroll
+        for (int q = 0; q < NL; ++q) {
+            float v = part[q][0];
+#pragma unroll
+            for (int s2 = 1; s2 < NS; ++s2) v += part[q][s2];
+            L[q] = v;
+        }
         float mx = -INFINITY;
-        for (int e = lane, q = 0; e < E; e += 32, ++q) mx = fmaxf(mx, L[q]);
+#pragma unroll
+        for (int q = 0; q < NL; ++q)
+            if (lane + 32 * q < E) mx = fmaxf(mx, L[q]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         float s = 0.f;
-        for (int e = lane, q = 0; e < E; e += 32, ++q) s += expf(L[q] - mx);
+#pragma unroll
+        for (int q = 0; q < NL; ++q)
+            if (lane + 32 * q < E) s += expf(L[q] - mx);
         s = warp_sum(s);
         // best / second best over P with the reference's tie rules
         float b0 = -1.f, b1 = -1.f;
         int i0 = 0x7fffffff, i1 = 0x7fffffff;
         float psum = 0.f;
-        for (int e = lane, q = 0; e < E; e += 32, ++q) {
+#pragma unroll
+        for (int q = 0; q < NL; ++q) {
+            const int e = lane + 32 * q;
+            if (e >= E) continue;
             const float p = expf(L[q] - mx) / s;
             probs[t * E + e] = p;
             s_col[warp * E + e] += p;
@@ -187,8 +201,26 @@ void launch_softmax_topk(const float* logits, int nsplit, int64_t T, int E, int 
     if (E > 256) throw Status(2, "gate: num_experts > 256 not supported on this path");
     const int nparts = softmax_parts(T);
     const size_t smem = sizeof(float) * kSoftmaxWarps * E + sizeof(int32_t) * E;
-    softmax_topk_kernel<<<nparts, kSoftmaxWarps * 32, smem, st>>>(
-        logits, nsplit, T, E, K, probs, choice, gate_prob, colsum_part, count_part, flags);
+    const int nl = E <= 32 ? 1 : E <= 64 ? 2 : E <= 128 ? 4 : 8;
+    auto go = [&](auto kernel) {
+        kernel<<<nparts, kSoftmaxWarps * 32, smem, st>>>(logits, T, E, K, probs, choice, gate_prob,
+                                                         colsum_part, count_part, flags);
+    };
+#define MOE_SOFTMAX_NS(NLV)                                                           \
+    switch (nsplit) {                                                                 \
+        case 1: go(softmax_topk_kernel<NLV, 1>); break;                               \
+        case 2: go(softmax_topk_kernel<NLV, 2>); break;                               \
+        case 4: go(softmax_topk_kernel<NLV, 4>); break;                               \
+        case 8: go(softmax_topk_kernel<NLV, 8>); break;                               \
+        default: throw Status(2, "softmax: split-K count must be 1, 2, 4 or 8");      \
+    }
+    switch (nl) {
+        case 1: MOE_SOFTMAX_NS(1) break;
+        case 2: MOE_SOFTMAX_NS(2) break;
+        case 4: MOE_SOFTMAX_NS(4) break;
+        default: MOE_SOFTMAX_NS(8) break;
+    }
+#undef MOE_SOFTMAX_NS
     MOE_LAUNCH_CHECK();
 }
 
