@@ -200,7 +200,9 @@ dx_kernel(int64_t T, int d, int E, int K, int cap_pad, const float* __restrict__
             *reinterpret_cast<float4*>(dxg_out + t * d + j + 4) = make_float4(v[4], v[5], v[6], v[7]);
             continue;
         }
-        for (int k = 0; k < K; ++k) {
+        #pragma unroll
+        for (int k = 0; k < 2; ++k) {  // K <= 2
+            if (k >= K) break;
             const int64_t r = rows[tt][k];
             if (r < 0) continue;
             float g[8];

@@ -450,7 +450,9 @@ dx_kernel(int64_t T, int d, int K, int cap_pad, const float* __restrict__ dL, co
     int64_t rows[2] = {-1, -1};
     bool any = false;
     if (t < T) {
-        for (int k = 0; k < K; ++k) {
+        #pragma unroll
+        for (int k = 0; k < 2; ++k) {  // K <= 2
+            if (k >= K) break;
             const int32_t p = pos[t * K + k];
             if (p >= 0) {
                 rows[k] = (int64_t)choice[t * K + k] * cap_pad + p;

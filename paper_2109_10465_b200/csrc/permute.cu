@@ -37,7 +37,21 @@ dispatch_gather_kernel(const TIO* __restrict__ x, int64_t d, int E, int K, int c
     if (p < n) {
         const int64_t t = row_src[r] / K;
         const TIO* src = x + t * d;
-        for (int64_t j = (int64_t)lane * V; j < d; j += 32 * V) copy_vec<TIO, V>(dst + j, src + j);
+        if constexpr (V * sizeof(TIO) == 16) {
+            // kU 16-byte loads in flight per lane before the stores
+            constexpr int kU = 8;
+            for (int64_t j0 = (int64_t)lane * V; j0 < d; j0 += 32 * V * kU) {
+                uint4 v[kU];
+#pragma unroll
+                for (int u = 0; u < kU; ++u)
+                    if (j0 + u * 32 * V < d) v[u] = __ldg(reinterpret_cast<const uint4*>(src + j0 + u * 32 * V));
+#pragma unroll
+                for (int u = 0; u < kU; ++u)
+                    if (j0 + u * 32 * V < d) *reinterpret_cast<uint4*>(dst + j0 + u * 32 * V) = v[u];
+            }
+        } else {
+            for (int64_t j = (int64_t)lane * V; j < d; j += 32 * V) copy_vec<TIO, V>(dst + j, src + j);
+        }
     } else if (p < round_up_dev(n, kRowAlign)) {
         for (int64_t j = (int64_t)lane * V; j < d; j += 32 * V) zero_vec<TIO, V>(dst + j);
     }
@@ -73,7 +87,9 @@ combine_kernel(const TIO* __restrict__ O, int64_t T, int64_t d, int K, int cap_p
     int64_t rows[2] = {-1, -1};
     float wk[2] = {0.f, 0.f};
     bool any = false;
-    for (int k = 0; k < K; ++k) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {  // K <= 2; unrolled so rows / wk stay in registers
+        if (k >= K) break;
         const int32_t p = pos[t * K + k];
         if (p >= 0) {
             rows[k] = (int64_t)choice[t * K + k] * cap_pad + p;
@@ -87,8 +103,9 @@ combine_kernel(const TIO* __restrict__ O, int64_t T, int64_t d, int K, int cap_p
         if (any) {
 #pragma unroll
             for (int q = 0; q < V; ++q) acc[q] = 0.f;
-            for (int k = 0; k < K; ++k) {
-                if (rows[k] < 0) continue;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                if (k >= K || rows[k] < 0) continue;
                 float o[V];
                 load_f<TIO, V>(O + rows[k] * d + j, o);
 #pragma unroll
@@ -179,7 +196,9 @@ dx_assemble_kernel(int64_t T, int64_t d, int K, int cap_pad, const float* __rest
     if (t >= T) return;
     int64_t rows[2] = {-1, -1};
     bool any = false;
-    for (int k = 0; k < K; ++k) {
+    #pragma unroll
+    for (int k = 0; k < 2; ++k) {  // K <= 2
+        if (k >= K) break;
         const int32_t p = pos[t * K + k];
         if (p >= 0) {
             rows[k] = (int64_t)choice[t * K + k] * cap_pad + p;
@@ -190,7 +209,9 @@ dx_assemble_kernel(int64_t T, int64_t d, int K, int cap_pad, const float* __rest
         float acc[V];
 #pragma unroll
         for (int q = 0; q < V; ++q) acc[q] = 0.f;
-        for (int k = 0; k < K; ++k) {
+        #pragma unroll
+        for (int k = 0; k < 2; ++k) {  // K <= 2
+            if (k >= K) break;
             if (rows[k] < 0) continue;
             float v[V];
             load_f<TIO, V>(dX + rows[k] * d + j, v);
@@ -263,7 +284,9 @@ __global__ void decision_stats_kernel(int64_t T, int E, int K, const int32_t* __
          t += (int64_t)gridDim.x * blockDim.x) {
         const int c0 = choice[t * K];
         if (c0 >= 0 && c0 < E) atomicAdd(&s_cnt[c0], 1u);
-        for (int k = 0; k < K; ++k) {
+        #pragma unroll
+        for (int k = 0; k < 2; ++k) {  // K <= 2
+            if (k >= K) break;
             if (pos[t * K + k] >= 0) continue;
             const int64_t tb = t * 8 / (T > 1 ? T : 1);
             const int b = tb < 7 ? (int)tb : 7;
@@ -437,7 +460,9 @@ __global__ void combine_ref_kernel(const TIO* __restrict__ O, int64_t T, int64_t
     for (int64_t j = lane; j < d; j += 32) {
         float acc = 0.f;
         if (any) {
-            for (int k = 0; k < K; ++k) {
+            #pragma unroll
+            for (int k = 0; k < 2; ++k) {  // K <= 2
+                if (k >= K) break;
                 const int32_t s = slot[t * K + k];
                 if (s < 0) continue;
                 acc = fmaf(w[(int64_t)k * T + t], to_f(O[((int64_t)eid[t * K + k] * cap + s) * d + j]), acc);

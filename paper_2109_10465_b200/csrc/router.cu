@@ -430,7 +430,9 @@ router_bwd_kernel(int64_t T, int d, int E, int K, const TIO* __restrict__ dy,
     const int64_t t = (int64_t)blockIdx.x * 8 + warp;
     if (t >= T) return;
     float dw[2] = {0.f, 0.f};
-    for (int k = 0; k < K; ++k) {
+    #pragma unroll
+    for (int k = 0; k < 2; ++k) {  // K <= 2
+        if (k >= K) break;
         const int32_t p = pos[t * K + k];
         if (p < 0) continue;
         const int64_t row = (int64_t)choice[t * K + k] * cap_pad + p;
