@@ -915,6 +915,12 @@ moe_status moe_check(moe_handle* h, uint32_t* flags_out) {
         MOE_CUDA_CHECK(cudaStreamSynchronize(h->stream));
         MOE_CUDA_CHECK(cudaMemcpy(&fl, h->flags.p, 4, cudaMemcpyDeviceToHost));
         MOE_CUDA_CHECK(cudaMemset(h->flags.p, 0, 4));
+        if (h->comm) {  // expert-parallel communicator: surface asynchronous NCCL failures
+            ncclResult_t async = ncclSuccess;
+            NCCL_CHECK(ncclCommGetAsyncError(h->comm, &async));
+            if (async != ncclSuccess)
+                throw Status(MOE_NCCL, std::string("NCCL asynchronous error: ") + ncclGetErrorString(async));
+        }
     });
     if (flags_out) *flags_out = fl;
     if (s) return s;
