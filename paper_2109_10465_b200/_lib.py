@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmoe_b200.so")
+# MOE_B200_LIB: load a variant build instead (benchmarking scripts only)
+LIB_PATH = os.environ.get("MOE_B200_LIB") or os.path.join(HERE, "libmoe_b200.so")
 
 MOE_OK, MOE_SHAPE, MOE_CONFIG, MOE_NONFINITE, MOE_UNIFORM_SHAPE, MOE_INVALID_ARG = range(6)
 MOE_CUDA, MOE_NCCL, MOE_UNSUPPORTED = 6, 7, 8

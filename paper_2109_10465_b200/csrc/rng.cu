@@ -174,28 +174,41 @@ static const Field& field() {
 }
 
 // ---------------------------------------------------------------- device
-// One CTA per chunk, 768 threads, three phases:
+// One CTA per chunk, 768 threads (24 warps), three overlapped phases:
 //   1. base: x[1 .. BASE] regenerated from the seed in shared memory (every
-//      CTA redundantly) by the warp twister below;
-//   2. jump: the chunk's 312-word window = XOR_{i : g_c,i} x[1 + j + i], all
-//      32 warps;
+//      CTA redundantly).  The host computes the 312 init words (a serial
+//      nonlinear recurrence) and passes them as a kernel parameter; warp 0
+//      twists blocks b = 1 .. kBaseBlocks in registers and publishes each
+//      one on its own mbarrier.
+//   2. jump (warps 1..23): the chunk's 312-word window =
+//      XOR_{i : g_c,i} x[1 + j + i].  The bit range is cut into runs of
+//      kRun 10-bit groups dealt round-robin to the jump warps, so all of them
+//      advance through the base together right behind warp 0 and the base
+//      costs only its first few blocks of latency.
 //   3. generation: warp 0 runs the block recurrence (the serial critical
-//      path) entirely in registers and publishes each 312-word block into a
-//      shared-memory ring (mbarrier full/empty per slot); 18 emitter warps
-//      (those not on warp 0's SM sub-partition) temper, convert and store
-//      whole blocks, round-robin.
-constexpr int kChunkThreads = 768;
-constexpr int kJumpWarps = kChunkThreads / 32;
-// bits per warp in the jump, a multiple of kJumpR so each warp's range is
-// whole R-bit mask groups; bits >= DEG of g are zero.
-constexpr int kGroupsPerWarp = (DEG + kJumpWarps * kJumpR - 1) / (kJumpWarps * kJumpR);
-constexpr int kGroups = kJumpWarps * kGroupsPerWarp;
-// the last lane's register window reads up to kGroups*R + 32*R + R words
-constexpr int BASE = kGroups * kJumpR + 32 * kJumpR + kJumpR;
-constexpr int kBaseBlocks = (BASE + N) / N;  // x[312*b ..] blocks b = 1..kBaseBlocks
-constexpr int kEmitters = kJumpWarps / 4 * 3;  // warps w with w % 4 != 0
-constexpr int kRing = 2 * kEmitters;         // ring slots (a multiple of kEmitters)
-static_assert(kRing * N <= BASE, "ring reuses the base region after the jump");
+//      path) in registers and publishes each 312-word block into a
+//      shared-memory ring (a full mbarrier per slot; one empty mbarrier per
+//      half ring, waited once per 18 blocks); 18 emitter warps (those not on
+//      warp 0's SM sub-partition) temper, convert and store whole blocks,
+//      round-robin.
+constexpr int kJumpWarps = 23;                        // warps 1..23 run the jump
+constexpr int kChunkThreads = 32 * (kJumpWarps + 1);  // + warp 0: base producer, then twister
+constexpr int kRun = 11;                              // 10-bit groups per run
+constexpr int kRunsPerWarp = 8;
+constexpr int kGroups = kJumpWarps * kRunsPerWarp * kRun;  // bits >= DEG of g are zero
+static_assert(kGroups * kJumpR >= DEG, "jump groups cover the polynomial");
+// the last lane's register window reads up to x[(kGroups + 32) * R]
+constexpr int BASE = (kGroups + 33) * kJumpR;
+constexpr int kBaseBlocks = BASE / N;                 // block b holds x[312b .. 312b + 311]
+constexpr int kBaseAlloc = (kBaseBlocks + 2) * N;     // sb words (block stores never need a bound)
+constexpr int kEmitters = kJumpWarps - kJumpWarps / 4;  // warps w in 1..23 with w % 4 != 0
+constexpr int kRing = 2 * kEmitters;                  // ring slots: two halves of kEmitters
+constexpr int kSlot = 320;                            // words per slot: A half [0,160), B half [160,320)
+static_assert(kRing * kSlot <= BASE, "ring reuses the base region after the jump");
+
+struct InitWords {  // x[0 .. 311] of init_genrand64(seed), host-computed
+    uint64_t x[N];
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -205,19 +218,6 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        "selp.u32 %0, 1, 0, p;\n"
-        "}\n"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
@@ -230,6 +230,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ uint32_t shfl_idx0(uint32_t v) {
+    uint32_t r;
+    asm volatile("shfl.sync.idx.b32 %0, %1, 0, 0x1f, 0xffffffff;" : "=r"(r) : "r"(v));
+    return r;
+}
+__device__ __forceinline__ uint32_t shfl_down1(uint32_t v) {
+    uint32_t r;
+    asm volatile("shfl.sync.down.b32 %0, %1, 1, 0x1f, 0xffffffff;" : "=r"(r) : "r"(v));
+    return r;
+}
+__device__ __forceinline__ uint64_t join(uint32_t lo, uint32_t hi) {
+    return (static_cast<uint64_t>(hi) << 32) | lo;
+}
 
 // twist(lo, hi, mid) = mid ^ mix(lo, hi)
 __device__ __forceinline__ uint64_t mix(uint64_t lo_word, uint64_t hi_word) {
@@ -238,48 +251,67 @@ __device__ __forceinline__ uint64_t mix(uint64_t lo_word, uint64_t hi_word) {
 }
 
 // One warp advances the 312-word state by one block, in registers.  Lane l
-// holds the word pairs j = 5l + r and j + 156 (r < 5, j < 156): A[r] = o[j],
-// B[r] = o[j + 156].  Then both halves of the block twist are lane-local:
+// holds the word pairs j = 5l + r and j + 156 (r < 5): A[r] = o[j],
+// B[r] = o[j + 156] (lane 31's r >= 1, j >= 156, are padding).  Both halves
+// of the block twist are then lane-local:
 //   new[j]       = mix(o[j], o[j+1])         ^ o[j+156]   = mix(A[r], A[r+1]) ^ B[r]
 //   new[j + 156] = mix(o[j+156], o[j+157])   ^ new[j]     = mix(B[r], B[r+1]) ^ newA[r]
 // with the r+1 = 5 neighbours from lane l+1, and lane 31 (j = 155, 311 only)
-// taking o[156] and new[0] from lane 0.
-__device__ __forceinline__ void warp_twist(uint64_t (&Aw)[5], uint64_t (&Bw)[5], int lane) {
-    // all cross-lane inputs are fetched up front (one batch of shuffles):
-    // lane 31 also rebuilds new[0] = mix(o[0], o[1]) ^ o[156] from lane 0's
-    // old words instead of waiting for lane 0's result
-    const uint64_t a_next = __shfl_down_sync(0xffffffffu, Aw[0], 1);
-    const uint64_t b_next = __shfl_down_sync(0xffffffffu, Bw[0], 1);
-    const uint64_t o156 = __shfl_sync(0xffffffffu, Bw[0], 0);
-    const uint64_t o0 = __shfl_sync(0xffffffffu, Aw[0], 0);
-    const uint64_t o1 = __shfl_sync(0xffffffffu, Aw[1], 0);
-    uint64_t nA[5];
-#pragma unroll
-    for (int r = 0; r < 5; ++r) {
-        uint64_t hi = r < 4 ? Aw[r + 1] : a_next;
-        if (r == 0 && lane == 31) hi = o156;  // j = 155
-        nA[r] = mix(Aw[r], hi) ^ Bw[r];
+// taking o[156] and new[0] from lane 0 (lane 31 rebuilds new[0] =
+// mix(o[0], o[1]) ^ o[156] itself).  All cross-lane inputs are words r <= 1
+// of the OLD block, so they are shuffled as soon as those are computed, one
+// block ahead: the shuffle latency hides under the rest of the twist instead
+// of heading the serial chain.  mix(lo, hi) reads lo's top 33 bits and hi's
+// low 31, so the hi operands (a_next, b_next, o1) move only their low halves.
+struct WarpTwister {
+    uint64_t A[5], B[5];
+    uint64_t a_next, b_next, o156, o0, o1;  // cross-lane inputs of the next twist
+
+    __device__ __forceinline__ void fetch() {
+        a_next = shfl_down1(static_cast<uint32_t>(A[0]));
+        b_next = shfl_down1(static_cast<uint32_t>(B[0]));
+        o156 = join(shfl_idx0(static_cast<uint32_t>(B[0])), shfl_idx0(static_cast<uint32_t>(B[0] >> 32)));
+        o0 = join(shfl_idx0(static_cast<uint32_t>(A[0])), shfl_idx0(static_cast<uint32_t>(A[0] >> 32)));
+        o1 = shfl_idx0(static_cast<uint32_t>(A[1]));
     }
-    const uint64_t new0 = mix(o0, o1) ^ o156;
+    __device__ __forceinline__ void twist(int lane) {
+        uint64_t nA[5];
+        nA[0] = mix(A[0], lane == 31 ? o156 : A[1]) ^ B[0];  // j = 155 on lane 31
+        nA[1] = mix(A[1], A[2]) ^ B[1];
+        const uint64_t new0 = mix(o0, o1) ^ o156;
+        const uint64_t nB0 = mix(B[0], lane == 31 ? new0 : B[1]) ^ nA[0];  // j = 311 on lane 31
+        const uint64_t an = shfl_down1(static_cast<uint32_t>(nA[0]));
+        const uint64_t bn = shfl_down1(static_cast<uint32_t>(nB0));
+        const uint64_t p156 = join(shfl_idx0(static_cast<uint32_t>(nB0)), shfl_idx0(static_cast<uint32_t>(nB0 >> 32)));
+        const uint64_t p0 = join(shfl_idx0(static_cast<uint32_t>(nA[0])), shfl_idx0(static_cast<uint32_t>(nA[0] >> 32)));
+        const uint64_t p1 = shfl_idx0(static_cast<uint32_t>(nA[1]));
 #pragma unroll
-    for (int r = 0; r < 5; ++r) {
-        uint64_t hi = r < 4 ? Bw[r + 1] : b_next;
-        if (r == 0 && lane == 31) hi = new0;  // j = 311
-        Bw[r] = mix(Bw[r], hi) ^ nA[r];
-        Aw[r] = nA[r];
+        for (int r = 2; r < 5; ++r) nA[r] = mix(A[r], r < 4 ? A[r + 1] : a_next) ^ B[r];
+#pragma unroll
+        for (int r = 1; r < 5; ++r) B[r] = mix(B[r], r < 4 ? B[r + 1] : b_next) ^ nA[r];
+        B[0] = nB0;
+#pragma unroll
+        for (int r = 0; r < 5; ++r) A[r] = nA[r];
+        a_next = an;
+        b_next = bn;
+        o156 = p156;
+        o0 = p0;
+        o1 = p1;
     }
-}
+};
 
 __global__ void __launch_bounds__(kChunkThreads, 1)
-chunk_kernel(uint64_t seed, const uint16_t* __restrict__ masks, int64_t J, int64_t count,
-             double lo, double span, float* __restrict__ noise, uint64_t* __restrict__ raw_out,
-             unsigned long long* __restrict__ tdbg) {
+chunk_kernel(const __grid_constant__ InitWords init, const uint16_t* __restrict__ masks, int64_t J,
+             int64_t count, double lo, double span, float* __restrict__ noise,
+             uint64_t* __restrict__ raw_out, unsigned long long* __restrict__ tdbg) {
     extern __shared__ uint64_t sm[];
-    uint64_t* sb = sm;                                   // x[1 .. BASE]; later the ring [kRing][N]
-    uint64_t* win = sb + BASE;                           // jump result [N]
-    uint64_t* full = win + N;                            // mbarriers [kRing]
-    uint64_t* empty = full + kRing;                      // mbarriers [kRing]
-    uint16_t* sg = reinterpret_cast<uint16_t*>(empty + kRing);  // g_c masks [kGroups]
+    uint64_t* sb = sm;                                   // x[k] at sb[k-1]; later the ring [kRing][kSlot]
+    uint64_t* win = sb + kBaseAlloc;                     // jump result [N]
+    uint64_t* pad = win + N;                             // sink for lane 31's padding words [16]
+    uint64_t* bb = pad + 16;                             // base block mbarriers [kBaseBlocks + 1]
+    uint64_t* full = bb + kBaseBlocks + 1;               // ring mbarriers [kRing]
+    uint64_t* empty = full + kRing;                      // half-ring mbarriers [2]
+    uint16_t* sg = reinterpret_cast<uint16_t*>(empty + 2);  // g_c masks [kGroups]
     uint64_t* ring = sb;
     const int c = blockIdx.x;
     const int64_t q0 = static_cast<int64_t>(c) * J;
@@ -297,73 +329,82 @@ chunk_kernel(uint64_t seed, const uint16_t* __restrict__ masks, int64_t J, int64
     for (int i = t; i < kGroups; i += kChunkThreads) sg[i] = masks[static_cast<int64_t>(c) * kGroups + i];
     for (int i = t; i < N; i += kChunkThreads) win[i] = 0;
     if (t == 0) {
-        for (int i = 0; i < kRing; ++i) {
-            mbar_init(&full[i], 32);   // all twister lanes arrive
-            mbar_init(&empty[i], 32);  // all lanes of the slot's emitter arrive
-        }
-    }
-    // ---- 1. base sequence: init_genrand64 (thread 0), then warp 0 twists
-    // blocks b = 1.. in registers and writes x[312b + j] to sb[312b + j - 1].
-    if (warp == 0) {
-        if (lane == 0) {
-            uint64_t v = seed;
-            win[0] = v;  // x[0] (scratch; win is cleared again below)
-            for (int i = 1; i < N; ++i) {
-                v = 6364136223846793005ULL * (v ^ (v >> 62)) + static_cast<uint64_t>(i);
-                sb[i - 1] = v;
-            }
-        }
-        __syncwarp();
-        uint64_t Aw[5], Bw[5];
-#pragma unroll
-        for (int r = 0; r < 5; ++r) {
-            const int j = lane * 5 + r;
-            Aw[r] = j == 0 ? win[0] : (j < M ? sb[j - 1] : 0);
-            Bw[r] = j < M ? sb[j + M - 1] : 0;
-        }
-        __syncwarp();
-        if (lane == 0) win[0] = 0;
-        for (int b = 1; b <= kBaseBlocks; ++b) {
-            warp_twist(Aw, Bw, lane);
-#pragma unroll
-            for (int r = 0; r < 5; ++r) {
-                const int j = lane * 5 + r;
-                const int k = b * N + j;
-                if (j < M) {
-                    if (k <= BASE) sb[k - 1] = Aw[r];
-                    if (k + M <= BASE) sb[k + M - 1] = Bw[r];
-                }
-            }
-        }
+        for (int i = 1; i <= kBaseBlocks; ++i) mbar_init(&bb[i], 32);
+        for (int i = 0; i < kRing; ++i) mbar_init(&full[i], 32);  // all twister lanes arrive
+        mbar_init(&empty[0], 32 * kEmitters);                     // every emitter lane, once per lap
+        mbar_init(&empty[1], 32 * kEmitters);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (t == 0) stamp(1);
-    // ---- 2. jump.  Warp w takes mask groups [w*G, (w+1)*G); lane l owns
-    // R consecutive window words j = l*R + r in registers and slides a
-    // register window over the base, so each bit costs one shared load plus
-    // (if set) R XORs; the mask is warp-uniform (no divergence).  Partial
-    // windows meet in `win` via shared atomic XOR.
-    {
-        constexpr int R = kJumpR;
-        const int i0 = warp * kGroupsPerWarp * R;
+    constexpr int R = kJumpR;
+    if (warp == 0) {
+        // ---- 1. base: blocks b = 1 .. kBaseBlocks of x, each published on bb[b]
+        WarpTwister tw;
+#pragma unroll
+        for (int r = 0; r < 5; ++r) {
+            const int j = min(lane * 5 + r, M - 1);
+            tw.A[r] = init.x[j];
+            tw.B[r] = init.x[j + M];
+            if (j == lane * 5 + r) {  // block 0: x[1 .. 311] (published with block 1)
+                if (j >= 1) sb[j - 1] = tw.A[r];
+                sb[j + M - 1] = tw.B[r];
+            }
+        }
+        tw.fetch();
+        for (int b = 1; b <= kBaseBlocks; ++b) {
+            tw.twist(lane);
+            uint64_t* dst = sb + b * N - 1 + lane * 5;  // x[312b + j] at sb[312b + j - 1]
+#pragma unroll
+            for (int r = 0; r < 5; ++r) *((lane == 31 && r > 0) ? pad + r : dst + r) = tw.A[r];
+#pragma unroll
+            for (int r = 0; r < 5; ++r) *((lane == 31 && r > 0) ? pad + 8 + r : dst + r + M) = tw.B[r];
+            mbar_arrive(&bb[b]);
+        }
+        if (lane == 0) stamp(1);
+    } else {
+        // ---- 2. jump.  Lane l owns R consecutive window words j = l*R + r
+        // in registers and slides a register window over the base, so each
+        // bit costs one shared load plus (if set) R XORs; bits are taken in
+        // pairs so two set bits cost one 3-input XOR pass (acc ^ a ^ b).
+        // Masks are warp-uniform (no divergence).  Partial windows meet in
+        // `win` via shared atomic XOR.
+        const int jw = warp - 1;
         const int j0 = lane * R;
         uint64_t acc[R], wr[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            acc[r] = 0;
-            wr[r] = sb[i0 + j0 + r];
-        }
-        const uint16_t* gm = sg + warp * kGroupsPerWarp;
-        for (int g = 0; g < kGroupsPerWarp; ++g) {
-            const int i = i0 + g * R;
-            const uint32_t m = gm[g];
+        for (int r = 0; r < R; ++r) acc[r] = 0;
+        for (int run = 0; run < kRunsPerWarp; ++run) {
+            const int g0 = (run * kJumpWarps + jw) * kRun;
+            // last word this run reads: x[(g0 + kRun + 32) * R]
+            const int blk = (g0 + kRun + 32) * R / N;
+            mbar_wait(&bb[blk], 0);
 #pragma unroll
-            for (int s = 0; s < R; ++s) {
-                if (m & (1u << s)) {
+            for (int r = 0; r < R; ++r) wr[r] = sb[g0 * R + j0 + r];
+            for (int g = 0; g < kRun; ++g) {
+                const int i = (g0 + g) * R;
+                const uint32_t m = sg[g0 + g];
+                uint64_t nx[R];
 #pragma unroll
-                    for (int r = 0; r < R; ++r) acc[r] ^= wr[(s + r) % R];
+                for (int q = 0; q < R; ++q) nx[q] = sb[i + j0 + R + q];
+#pragma unroll
+                for (int s2 = 0; s2 < R; s2 += 2) {
+                    const uint32_t pr = (m >> s2) & 3u;
+                    // bit s2 reads wr[(s2+r)%R]; bit s2+1 reads wr[(s2+1+r)%R],
+                    // except r = R-1: the slot s2 refill (nx[s2])
+                    if (pr == 3u) {
+#pragma unroll
+                        for (int r = 0; r < R; ++r)
+                            acc[r] ^= wr[(s2 + r) % R] ^ (r == R - 1 ? nx[s2] : wr[(s2 + 1 + r) % R]);
+                    } else if (pr == 1u) {
+#pragma unroll
+                        for (int r = 0; r < R; ++r) acc[r] ^= wr[(s2 + r) % R];
+                    } else if (pr == 2u) {
+#pragma unroll
+                        for (int r = 0; r < R; ++r) acc[r] ^= (r == R - 1 ? nx[s2] : wr[(s2 + 1 + r) % R]);
+                    }
+                    wr[s2] = nx[s2];
+                    wr[s2 + 1] = nx[s2 + 1];
                 }
-                wr[s] = sb[i + j0 + R + s];
             }
         }
 #pragma unroll
@@ -376,52 +417,57 @@ chunk_kernel(uint64_t seed, const uint16_t* __restrict__ masks, int64_t J, int64
     const int64_t n = min(J, count - q0);
     const int nblk = static_cast<int>((n + N - 1) / N);
     if (warp == 0) {
-        uint64_t Aw[5], Bw[5];
+        WarpTwister tw;
 #pragma unroll
         for (int r = 0; r < 5; ++r) {
-            const int j = lane * 5 + r;
-            Aw[r] = j < M ? win[j] : 0;
-            Bw[r] = j < M ? win[j + M] : 0;
+            const int j = min(lane * 5 + r, M - 1);
+            tw.A[r] = win[j];
+            tw.B[r] = win[j + M];
         }
-        // Every lane arrives on full[] (count 32), one block late, so the
-        // release never waits on stores still in flight; the empty[] check
-        // for the next slot is issued before the twist so its latency hides.
-        int slot = 0, prev = -1;
+        tw.fetch();
+        int slot = 0;
         uint32_t lap = 0;
+        const long long cyc0 = clock64();
+        long long wait_cyc = 0;
         for (int b = 0; b < nblk; ++b) {
-            const bool ready = b < kRing || mbar_test(&empty[slot], lap ^ 1u);
-            if (b > 0) warp_twist(Aw, Bw, lane);
-            if (prev >= 0) mbar_arrive(&full[prev]);
-            if (!ready) mbar_wait(&empty[slot], lap ^ 1u);
-            uint64_t* dst = ring + slot * N + lane * 5;
+            if (b > 0) tw.twist(lane);
+            // slots of half h are rewritten once all emitters released them
+            if (lap > 0 && (slot == 0 || slot == kEmitters)) {
+                const long long w0 = clock64();
+                mbar_wait(&empty[slot != 0], (lap - 1) & 1);
+                wait_cyc += clock64() - w0;
+            }
+            uint64_t* dst = ring + slot * kSlot + lane * 5;  // lane 31's r > 0 hit the pads
 #pragma unroll
             for (int r = 0; r < 5; ++r) {
-                if (lane * 5 + r < M) {
-                    dst[r] = Aw[r];
-                    dst[r + M] = Bw[r];
-                }
+                dst[r] = tw.A[r];
+                dst[r + kSlot / 2] = tw.B[r];
             }
-            prev = slot;
+            mbar_arrive(&full[slot]);
             if (++slot == kRing) {
                 slot = 0;
-                lap ^= 1u;
+                ++lap;
             }
         }
-        if (prev >= 0) mbar_arrive(&full[prev]);
-        if (lane == 0) stamp(3);
-    } else if (warp & 3) {
+        if (lane == 0) {
+            stamp(3);
+            if (tdbg) tdbg[c * 8 + 6] = static_cast<unsigned long long>(clock64() - cyc0);
+            if (tdbg) tdbg[c * 8 + 7] = static_cast<unsigned long long>(wait_cyc);
+        }
+    } else if (warp & 3) {  // not on warp 0's SM sub-partition (warp w runs on SMSP w % 4)
         const int k = (warp >> 2) * 3 + (warp & 3) - 1;  // 0 .. kEmitters-1
         for (int b = k; b < nblk; b += kEmitters) {
             const int slot = b % kRing;
             mbar_wait(&full[slot], (b / kRing) & 1);
-            const uint64_t* src = ring + slot * N;
+            const uint64_t* src = ring + slot * kSlot;
             const int64_t qb = static_cast<int64_t>(b) * N;
 #pragma unroll
-            for (int it = 0; it < (N + 31) / 32; ++it) {
-                const int i = lane + 32 * it;
+            for (int it = 0; it < kSlot / 32; ++it) {
+                const int p = lane + 32 * it;  // slot position; 156..159 and 316..319 are pads
+                const int i = p < kSlot / 2 ? p : p - (kSlot / 2 - M);
                 const int64_t q = qb + i;
-                if (i < N && q < n) {
-                    const uint64_t out = temper(src[i]);
+                if ((p < M || p >= kSlot / 2) && p < kSlot / 2 + M && q < n) {
+                    const uint64_t out = temper(src[p]);
                     if (raw_out) raw_out[q0 + q] = out;
                     if (noise) {
                         // lo + (hi - lo) * u53 * 2^-53 in f64 without
@@ -431,7 +477,7 @@ chunk_kernel(uint64_t seed, const uint16_t* __restrict__ masks, int64_t J, int64
                     }
                 }
             }
-            mbar_arrive(&empty[slot]);
+            mbar_arrive(&empty[slot >= kEmitters]);
         }
         if (lane == 0 && warp == 1) stamp(4);
     }
@@ -477,7 +523,12 @@ void generate(uint64_t seed, int64_t count, double lo, double hi, float* noise, 
     const int P = static_cast<int>(std::min<int64_t>(kNumSMs, ceil_div(count, 4096)));
     const int64_t J = ceil_div(count, P);
     const Table& tab = table_for(J, P);
-    const size_t smem = sizeof(uint64_t) * (BASE + N + 2 * kRing) + sizeof(uint16_t) * kGroups;
+    const size_t smem = sizeof(uint64_t) * (kBaseAlloc + N + 16 + kBaseBlocks + 1 + kRing + 2) +
+                        sizeof(uint16_t) * kGroups;
+    InitWords init;  // init_genrand64 (rng.cpp: std::mt19937_64 seeding)
+    init.x[0] = seed;
+    for (int i = 1; i < N; ++i)
+        init.x[i] = 6364136223846793005ULL * (init.x[i - 1] ^ (init.x[i - 1] >> 62)) + static_cast<uint64_t>(i);
     static bool attr = false;
     if (!attr) {
         MOE_CUDA_CHECK(cudaFuncSetAttribute(chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -487,7 +538,10 @@ void generate(uint64_t seed, int64_t count, double lo, double hi, float* noise, 
     static unsigned long long* tdbg = nullptr;
     static const bool timing = std::getenv("MOE_B200_RNG_TIMING") != nullptr;
     if (timing && !tdbg) MOE_CUDA_CHECK(cudaMalloc(&tdbg, sizeof(unsigned long long) * 8 * kNumSMs));
-    chunk_kernel<<<P, kChunkThreads, smem, st>>>(seed, tab.dev, J, count, lo, hi - lo, noise, raw,
+    // debug (timing runs only): =1 drops the stores, timing the recurrence alone
+    static const bool null_out = timing && std::getenv("MOE_B200_RNG_NULL_OUT") != nullptr;
+    if (null_out) noise = nullptr, raw = nullptr;
+    chunk_kernel<<<P, kChunkThreads, smem, st>>>(init, tab.dev, J, count, lo, hi - lo, noise, raw,
                                                  timing ? tdbg : nullptr);
     MOE_LAUNCH_CHECK();
     if (timing) {  // debug: per-phase times averaged over CTAs (synchronises)
@@ -498,8 +552,13 @@ void generate(uint64_t seed, int64_t count, double lo, double hi, float* noise, 
         double ph[4] = {0, 0, 0, 0};
         for (int c = 0; c < P; ++c)
             for (int k = 0; k < 4; ++k) ph[k] += double(static_cast<long long>(h[c * 8 + k + 1] - h[c * 8 + k])) / P;
-        std::fprintf(stderr, "[rng] P=%d J=%lld base %.1f us, jump %.1f us, twister %.1f us, emit tail %.1f us\n",
-                     P, static_cast<long long>(J), ph[0] / 1e3, ph[1] / 1e3, ph[2] / 1e3, ph[3] / 1e3);
+        double cyc = 0;
+        double wcyc = 0;
+        for (int c = 0; c < P; ++c) cyc += double(h[c * 8 + 6]) / P, wcyc += double(h[c * 8 + 7]) / P;
+        std::fprintf(stderr, "[rng] twister empty-wait %.0f cycles/block\n", wcyc / double(ceil_div(J, (int64_t)N)));
+        std::fprintf(stderr, "[rng] P=%d J=%lld base %.1f us, jump %.1f us, twister %.1f us (%.0f cycles/block), emit tail %.1f us\n",
+                     P, static_cast<long long>(J), ph[0] / 1e3, ph[1] / 1e3, ph[2] / 1e3,
+                     cyc / double(ceil_div(J, (int64_t)N)), ph[3] / 1e3);
     }
 }
 
