@@ -473,70 +473,92 @@ dx_kernel(int64_t T, int d, int K, int cap_pad, const float* __restrict__ dL, co
     });
     mbar_wait(&bars[0], 0);
     tc_fence_after();
-    // per 32-column chunk: issue this row's global reads (noise, gathered dX
-    // rows, dy) first, then read the accumulator, then combine and store
-#pragma unroll 1
-    for (int c = 0; c < XN; c += 32) {
-        const int64_t j = j0 + c;
-        Raw4<float> nz[8];
-        uint4 gx[2][4], gy[4];
-        const bool live = t < T;
-        if (live) {
-            if (noise) {
+    // Epilogue.  tcgen05.ld hands thread i accumulator row i; the global
+    // traffic (noise, gathered dX rows, dy, dx) is row-major.  Each warp owns
+    // its 32 rows and runs its own pipeline over the 32-column chunks: the
+    // chunk's row segments are copied global -> shared with cp.async (16 B,
+    // 8 adjacent lanes per 128 B row segment, zero-filled for dropped routes)
+    // two chunks ahead, the accumulator chunk is bounced through shared
+    // memory, and the combine walks 4 rows x 8 column groups per instruction.
+    // The operand tiles are free now and hold the stages.
+    constexpr int kWS = 8192;  // bytes per warp-stage: noise [32][32] f32, g0/g1 [32][32] bf16
+    static_assert(2 * 4 * kWS + 4 * 32 * 33 * 4 + 128 * 2 * 4 <= S::steps * (S::A + S::B), "epilogue fits the operand tiles");
+    float* stile = reinterpret_cast<float*>(sm + 2 * 4 * kWS) + warp * (32 * 33);  // [32 rows][33]
+    int32_t* srows = reinterpret_cast<int32_t*>(sm + 2 * 4 * kWS + 4 * 32 * 33 * 4);  // [128][2]
+    srows[tid * 2 + 0] = t < T ? (int32_t)rows[0] : -1;
+    srows[tid * 2 + 1] = t >= T ? -1 : (any ? (int32_t)rows[1] : -2);  // -2: no route kept (residual)
+    __syncwarp();
+    const int32_t* wrows = srows + warp * 64;
+    const int64_t tw = t0 + warp * 32;  // this warp's first token
+    auto issue = [&](int c, int stage) {
+        uint8_t* base = sm + (stage * 4 + warp) * kWS;
+        const int64_t jc = j0 + c;
 #pragma unroll
-                for (int q = 0; q < 8; ++q) nz[q].load(noise + t * d + j + 4 * q);
-            }
-#pragma unroll
-            for (int k = 0; k < 2; ++k)
-                if (k < K && rows[k] >= 0) {
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) gx[k][q] = __ldg(reinterpret_cast<const uint4*>(dX + rows[k] * d + j + 8 * q));
-                }
-            if (!any) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) gy[q] = __ldg(reinterpret_cast<const uint4*>(dy + t * d + j + 8 * q));
-            }
+        for (int i = 0; i < 8; ++i) {  // noise: 32 rows x 8 x 16 B
+            const int q = lane + 32 * i, r = q >> 3, c16 = q & 7;
+            const bool ok = noise != nullptr && tw + r < T;
+            cp16(base + r * 128 + c16 * 16, ok ? noise + (tw + r) * d + jc + 4 * c16 : noise, ok);
         }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {  // dX rows of routes 0 / 1 (or dy): 32 rows x 4 x 16 B each
+            const int q = lane + 32 * i, r = q >> 2, c16 = q & 3;
+            const int32_t r0 = wrows[r * 2 + 0], r1 = wrows[r * 2 + 1];
+            cp16(base + 4096 + r * 64 + c16 * 16, r0 >= 0 ? dX + (int64_t)r0 * d + jc + 8 * c16 : dX, r0 >= 0);
+            const TIO* s1 = r1 >= 0 ? dX + (int64_t)r1 * d + jc + 8 * c16
+                                    : (r1 == -2 ? dy + (tw + r) * d + jc + 8 * c16 : dX);
+            cp16(base + 6144 + r * 64 + c16 * 16, s1, r1 != -1);
+        }
+        cp_commit();
+    };
+    const int sub = lane >> 3, cg = lane & 7;  // row within a group of 4, 4-column group
+    constexpr int NCH = XN / 32;
+    issue(0, 0);
+    issue(32, 1);
+#pragma unroll 1
+    for (int ci = 0; ci < NCH; ++ci) {
+        const int c = ci * 32, stage = ci & 1;
         uint32_t u[32];
         tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + c, u);
-        if (!live) continue;
-        float v[32];
 #pragma unroll
-        for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(u[q]);
-        if (noise) {
+        for (int q = 0; q < 32; ++q) stile[lane * 33 + q] = __uint_as_float(u[q]);
+        cp_wait<1>();  // this lane's copies of chunk ci have landed
+        __syncwarp();  // ... and everyone's; stile visible too
+        const uint8_t* base = sm + (stage * 4 + warp) * kWS;
+        const int64_t j = j0 + c + 4 * cg;
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                float n4[4];
-                nz[q].get(n4);
+        for (int it = 0; it < 8; ++it) {
+            const int rl = it * 4 + sub;
+            const int64_t tt = tw + rl;
+            if (tt >= T) continue;
+            const int32_t r1 = wrows[rl * 2 + 1];
+            const float4 n4 = noise ? *reinterpret_cast<const float4*>(base + rl * 128 + cg * 16)
+                                    : make_float4(1.f, 1.f, 1.f, 1.f);
+            const uint2 g0 = *reinterpret_cast<const uint2*>(base + 4096 + rl * 64 + cg * 8);
+            const uint2 g1 = *reinterpret_cast<const uint2*>(base + 6144 + rl * 64 + cg * 8);
+            float v[4];
 #pragma unroll
-                for (int w = 0; w < 4; ++w) v[4 * q + w] *= n4[w];
+            for (int w = 0; w < 4; ++w) v[w] = stile[rl * 33 + 4 * cg + w];
+            v[0] *= n4.x; v[1] *= n4.y; v[2] *= n4.z; v[3] *= n4.w;
+            auto add4 = [&](const uint2& g) {
+                v[0] += __uint_as_float(g.x << 16); v[1] += __uint_as_float(g.x & 0xffff0000u);
+                v[2] += __uint_as_float(g.y << 16); v[3] += __uint_as_float(g.y & 0xffff0000u);
+            };
+            add4(g0);  // zero unless route 0 kept
+            if (r1 == -2) {  // no route kept: the residual carries dy (in g1)
+                if (residual_is_x) add4(g1);
+                else if (dres) *reinterpret_cast<uint2*>(dres + tt * d + j) = g1;
+            } else {
+                add4(g1);  // zero unless route 1 kept
+                if (!residual_is_x && dres) *reinterpret_cast<uint2*>(dres + tt * d + j) = make_uint2(0u, 0u);
             }
+            const __nv_bfloat162 lo2 = __floats2bfloat162_rn(v[0], v[1]);
+            const __nv_bfloat162 hi2 = __floats2bfloat162_rn(v[2], v[3]);
+            *reinterpret_cast<uint2*>(dx + tt * d + j) =
+                make_uint2(*reinterpret_cast<const uint32_t*>(&lo2), *reinterpret_cast<const uint32_t*>(&hi2));
         }
-        auto add8 = [&](const uint4& r, int q0) {
-            const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&r);
-#pragma unroll
-            for (int w = 0; w < 8; ++w) v[q0 + w] += __bfloat162float(h[w]);
-        };
-#pragma unroll
-        for (int k = 0; k < 2; ++k)
-            if (k < K && rows[k] >= 0) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) add8(gx[k][q], 8 * q);
-            }
-        if (!any) {
-            if (residual_is_x) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) add8(gy[q], 8 * q);
-            } else if (dres) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(dres + t * d + j + 8 * q) = gy[q];
-            }
-        } else if (!residual_is_x && dres) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(dres + t * d + j + 8 * q) = make_uint4(0u, 0u, 0u, 0u);
-        }
-#pragma unroll
-        for (int q = 0; q < 32; q += 8) store_f<TIO, 8>(dx + t * d + j + q, *reinterpret_cast<float(*)[8]>(v + q));
+        __syncwarp();  // stage and stile consumed
+        if (ci + 2 < NCH) issue(c + 64, stage);
+        else cp_commit();  // keep one group per chunk so wait_group<1> stays exact
     }
     teardown(tmem, XN);
 }

@@ -53,9 +53,15 @@ enum Kind { ROW = 0, WGRAD = 1 };
 // the MMA's ~94 B/clk consumption (3 stages starved the MMA).  WGRAD (K = the
 // expert's rows, ~128 on one GPU) is bound by its dW stores: 3 stages and a
 // double-buffered epilogue.
+#ifndef MOE_WG_STAGES
+#define MOE_WG_STAGES 3
+#endif
+#ifndef MOE_WG_EPIBUFS
+#define MOE_WG_EPIBUFS 2
+#endif
 template <int KIND> struct KCfg {
-    static constexpr int stages = KIND == ROW ? 4 : 3;
-    static constexpr int epi_bufs = KIND == ROW ? 1 : 2;
+    static constexpr int stages = KIND == ROW ? 4 : MOE_WG_STAGES;
+    static constexpr int epi_bufs = KIND == ROW ? 1 : MOE_WG_EPIBUFS;
     static constexpr uint32_t epi_bytes = 4 * epi_bufs * kStageCBytes;
     static constexpr size_t smem = 1024 /*align slack*/ + stages * kStageBytes + epi_bytes +
                                    1024 /*barriers*/ + 4 * (kMaxSegs + 3 * kMaxGroups + 8);
@@ -378,12 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1) grouped_gemm_kernel(const __grid_
                 // stage the warp's 32 x 64 bf16 block (128B-swizzled rows) and
                 // hand it to the TMA engine; two buffers alternate per warp
                 uint8_t* sbuf = cstage + ((quarter * kEpiBufs + (cbuf % kEpiBufs)) * kStageCBytes);
-                if (lane == 0) {
-                    if constexpr (kEpiBufs == 1)
-                        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                    else
-                        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-                }
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kEpiBufs - 1) : "memory");
                 __syncwarp();
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
