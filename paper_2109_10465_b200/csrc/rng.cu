@@ -10,7 +10,7 @@
 //    with g = t^e mod phi.
 //  * Chunk c of the stream starts at raw word o_c = 312 + c*J.  Its 312-word
 //    window is XOR_{i: g_c,i = 1} base[j + i] with g_c = t^(o_c - 1) mod phi
-//    and base = x[1 .. 20249) generated once per call from the seed.
+//    and base = x[1 .. BASE] generated once per call from the seed.
 //  * From its window each CTA regenerates its J outputs with the ordinary
 //    block twist (shift-invariant) and tempering, producing the reference's
 //    noise bit-for-bit (noise = lo + (hi - lo) * ((out >> 11) * 2^-53), the
