@@ -27,7 +27,7 @@ def test_jump_ahead_host_matches_sequential_stream(seed, J, c, n):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("count", [1, 311, 312, 5000, 2_000_003, 16_777_216])
+@pytest.mark.parametrize("count", [1, 311, 312, 313, 4097, 5000, 606_209, 2_000_003, 16_777_216])
 def test_device_stream_matches_reference(count):
     import torch
     from paper_2109_10465_b200 import _lib
