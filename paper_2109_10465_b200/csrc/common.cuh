@@ -35,6 +35,33 @@ uint64_t count_launch();
         ::moe::count_launch();                    \
     } while (0)
 
+// Programmatic dependent launch (PDL).  Kernels of the layer's main path are
+// launched with programmatic stream serialisation, so a kernel's CTAs are
+// scheduled (and run their independent prologue: barrier init, TMEM
+// allocation, table loads) while the previous kernel drains.  Every kernel
+// calls pdl_wait() before touching anything an earlier kernel wrote (it
+// returns once the predecessor grid has completed and its writes are
+// visible; a no-op for ordinary launches) and pdl_trigger() to let its own
+// successor be scheduled.  MOE_B200_PDL=0 turns the attribute off.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+bool pdl_on();
+template <class... P, class... A>
+inline void launch_pdl(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A&&... args) {
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    MOE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, static_cast<P>(args)...));
+    ::moe::count_launch();
+}
+
 inline int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 inline int64_t ceil_div(int64_t v, int64_t a) { return (v + a - 1) / a; }
 

@@ -49,6 +49,8 @@ __global__ void __launch_bounds__(NT)
 logits_kernel(const TX* __restrict__ x, const float* __restrict__ noise,
               const float* __restrict__ wg, float* __restrict__ logits, int64_t T, int d, int E,
               int k_per_split) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ __align__(16) float Xs[BK][BT + 4];
     __shared__ __align__(16) float Ws[BK][BE + 4];
     const int tid = threadIdx.x;
@@ -122,6 +124,8 @@ dx_kernel(int64_t T, int d, int E, int K, int cap_pad, const float* __restrict__
           const int32_t* __restrict__ choice, const int32_t* __restrict__ pos,
           const TIO* __restrict__ dy, bool residual_is_x, TIO* __restrict__ dx,
           TIO* __restrict__ dres) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ __align__(16) float Ls[MAXE][BT + 4];
     __shared__ __align__(16) float Wt[MAXE][DJ + 4];
     __shared__ int64_t rows[BT][2];
@@ -214,6 +218,8 @@ __global__ void __launch_bounds__(NT)
 dw_kernel(const TX* __restrict__ x, const float* __restrict__ noise,
           const float* __restrict__ dL, float* __restrict__ part, int64_t T, int d, int E,
           int64_t t_per_split) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ __align__(16) float As[BK][BT + 4];  // [token][j]
     __shared__ __align__(16) float Bs[BK][BE + 4];  // [token][e]
     const int tid = threadIdx.x;

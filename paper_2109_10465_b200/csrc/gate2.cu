@@ -22,6 +22,8 @@ __global__ void __launch_bounds__(NT)
 logits_kernel(const TX* __restrict__ x, const float* __restrict__ noise,
               const float* __restrict__ wg, float* __restrict__ logits, int64_t T, int d, int E,
               int k_per_split) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ __align__(16) float Xs[LK][LT + 4];
     __shared__ __align__(16) float Ws[LK][LE + 4];
     const int tid = threadIdx.x;
@@ -96,6 +98,8 @@ logits_kernel(const TX* __restrict__ x, const float* __restrict__ noise,
 
 // ---- WgT = Wg^T ([E][d]) so the dx kernel stages contiguous rows.
 __global__ void transpose_kernel(const float* __restrict__ wg, float* __restrict__ wgt, int d, int E) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ float tile[32][33];
     const int j0 = blockIdx.x * 32, e0 = blockIdx.y * 32;
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {
@@ -123,6 +127,8 @@ dx_kernel(int64_t T, int d, int E, int K, int cap_pad, const float* __restrict__
           const TIO* __restrict__ dX, const int32_t* __restrict__ choice,
           const int32_t* __restrict__ pos, const TIO* __restrict__ dy, bool residual_is_x,
           TIO* __restrict__ dx, TIO* __restrict__ dres, float* __restrict__ dxg_out) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ __align__(16) float Ls[DT][MAXE + 1];
     __shared__ __align__(16) float Ws[DE][DJ + 4];
     __shared__ int64_t rows[DT][2];
@@ -253,14 +259,12 @@ template <class TX>
 void launch_gate2_logits(const TX* x, const float* noise, const float* wg, float* logits, int64_t T,
                          int d, int E, int splits, cudaStream_t st) {
     dim3 grid((unsigned)ceil_div(T, gate2::LT), (unsigned)ceil_div(E, gate2::LE), (unsigned)splits);
-    gate2::logits_kernel<TX><<<grid, gate2::NT, 0, st>>>(x, noise, wg, logits, T, d, E, d / splits);
-    MOE_LAUNCH_CHECK();
+    launch_pdl(gate2::logits_kernel<TX>, dim3(grid), dim3(gate2::NT), 0, st, x, noise, wg, logits, T, d, E, d / splits);
 }
 
 void launch_gate2_transpose(const float* wg, float* wgt, int d, int E, cudaStream_t st) {
     dim3 grid((unsigned)ceil_div(d, 32), (unsigned)ceil_div(E, 32));
-    gate2::transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(wg, wgt, d, E);
-    MOE_LAUNCH_CHECK();
+    launch_pdl(gate2::transpose_kernel, dim3(grid), dim3(dim3(32, 8)), 0, st, wg, wgt, d, E);
 }
 
 template <class TIO>
@@ -268,17 +272,15 @@ void launch_gate2_dx(int64_t T, int d, int E, int K, int cap_pad, const float* d
                      const float* noise, const TIO* dX, const int32_t* choice, const int32_t* pos,
                      const TIO* dy, bool residual_is_x, TIO* dx, TIO* dres, cudaStream_t st) {
     dim3 grid((unsigned)ceil_div(T, gate2::DT), (unsigned)(d / gate2::DJ));
-    gate2::dx_kernel<TIO><<<grid, gate2::NT, 0, st>>>(T, d, E, K, cap_pad, dL, wgt, noise, dX, choice,
+    launch_pdl(gate2::dx_kernel<TIO>, dim3(grid), dim3(gate2::NT), 0, st, T, d, E, K, cap_pad, dL, wgt, noise, dX, choice,
                                                        pos, dy, residual_is_x, dx, dres, nullptr);
-    MOE_LAUNCH_CHECK();
 }
 
 void launch_gate2_dxg(int64_t T, int d, int E, const float* dL, const float* wgt, const float* noise,
                       float* dxg, cudaStream_t st) {
     dim3 grid((unsigned)ceil_div(T, gate2::DT), (unsigned)(d / gate2::DJ));
-    gate2::dx_kernel<float><<<grid, gate2::NT, 0, st>>>(T, d, E, 1, 0, dL, wgt, noise, nullptr, nullptr,
+    launch_pdl(gate2::dx_kernel<float>, dim3(grid), dim3(gate2::NT), 0, st, T, d, E, 1, 0, dL, wgt, noise, nullptr, nullptr,
                                                          nullptr, nullptr, false, nullptr, nullptr, dxg);
-    MOE_LAUNCH_CHECK();
 }
 
 int gate2_logit_splits(int64_t T, int d, int E) {

@@ -166,6 +166,8 @@ logits_kernel(const TX* __restrict__ x, const float* __restrict__ noise, const f
     const int nsteps = k_per_split / BK;
     out += (int64_t)blockIdx.y * T * E;
     const uint32_t tmem = setup(bars, 3, tslot, kNAcc * E);
+    pdl_wait();  // barriers and TMEM are set up; now the predecessor's data
+    pdl_trigger();
 
     // producer mapping: A: chunk c = tid % 8 (4 k), rows tid/8 + 16 i (i < 8)
     //                   B: chunk c = tid % 8, rows e = tid/8 + 16 i (i < E/16)
@@ -298,6 +300,8 @@ dw_kernel(const TX* __restrict__ x, const float* __restrict__ noise, const float
     const int nsteps = te > tb ? (int)((te - tb + BK - 1) / BK) : 0;
     part += (int64_t)blockIdx.y * d * E;
     const uint32_t tmem = setup(bars, 3, tslot, E < 32 ? 32 : E);
+    pdl_wait();  // barriers and TMEM are set up; now the predecessor's data
+    pdl_trigger();
 
     auto issue = [&](int step) {
         if (step < nsteps) {
@@ -421,6 +425,8 @@ dx_kernel(int64_t T, int d, int K, int cap_pad, const float* __restrict__ dL, co
     const int64_t t0 = (int64_t)blockIdx.x * BM;
     const int j0 = blockIdx.y * XN;
     const uint32_t tmem = setup(bars, 1, tslot, XN);
+    pdl_wait();  // barriers and TMEM are set up; now the predecessor's data
+    pdl_trigger();
     // stage all K steps: A 8 chunks / thread / step, B 16 chunks / thread / step
 #pragma unroll
     for (int s = 0; s < S::steps; ++s) {
@@ -590,8 +596,7 @@ void launch_gate_tc_logits(const TX* x, const float* noise, const float* wgt, fl
     static bool attr = false;
     if (!attr) { gtc::set_smem(k, gtc::LogitsSmem<kE>::bytes); attr = true; }
     dim3 grid((unsigned)ceil_div(T, (int64_t)gtc::BM), (unsigned)splits);
-    k<<<grid, gtc::NT, gtc::LogitsSmem<kE>::bytes, st>>>(x, noise, wgt, logits, T, d, d / splits);
-    MOE_LAUNCH_CHECK();
+    launch_pdl(k, dim3(grid), dim3(gtc::NT), gtc::LogitsSmem<kE>::bytes, st, x, noise, wgt, logits, T, d, d / splits);
 }
 
 template <class TX>
@@ -604,8 +609,7 @@ void launch_gate_tc_dw(const TX* x, const float* noise, const float* dL, float* 
     if (!attr) { gtc::set_smem(k, gtc::DwSmem<kE>::bytes); attr = true; }
     const int64_t tps = round_up(ceil_div(T, (int64_t)splits), (int64_t)gtc::BK);
     dim3 grid((unsigned)(d / gtc::BM), (unsigned)splits);
-    k<<<grid, gtc::NTS, gtc::DwSmem<kE>::bytes, st>>>(x, noise, dL, part, T, d, tps);
-    MOE_LAUNCH_CHECK();
+    launch_pdl(k, dim3(grid), dim3(gtc::NTS), gtc::DwSmem<kE>::bytes, st, x, noise, dL, part, T, d, tps);
 }
 
 template <class TIO>
@@ -618,9 +622,8 @@ void launch_gate_tc_dx(int64_t T, int d, int E, int K, int cap_pad, const float*
     static bool attr = false;
     if (!attr) { gtc::set_smem(k, gtc::DxSmem<kE>::bytes); attr = true; }
     dim3 grid((unsigned)ceil_div(T, (int64_t)gtc::BM), (unsigned)(d / gtc::XN));
-    k<<<grid, gtc::NT, gtc::DxSmem<kE>::bytes, st>>>(T, d, K, cap_pad, dL, wg, noise, dX, choice, pos, dy,
+    launch_pdl(k, dim3(grid), dim3(gtc::NT), gtc::DxSmem<kE>::bytes, st, T, d, K, cap_pad, dL, wg, noise, dX, choice, pos, dy,
                                                      residual_is_x, dx, dres);
-    MOE_LAUNCH_CHECK();
 }
 
 #define INST(T)                                                                                         \

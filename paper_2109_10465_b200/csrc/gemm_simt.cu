@@ -44,6 +44,8 @@ gemm_dense_kernel(const TA* __restrict__ A, int64_t lda_m, int64_t lda_k,
                   const float* __restrict__ S, const float* __restrict__ B, int64_t ldb_k,
                   int64_t ldb_n, float* __restrict__ C, int64_t M, int64_t N, int64_t K,
                   int64_t k_per_split) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ __align__(16) float As[BK][BM + 4];
     __shared__ __align__(16) float Bs[BK][BN + 4];
     const int tid = threadIdx.x;
@@ -98,13 +100,14 @@ void launch_gemm_dense(const TA* A, int64_t lda_m, int64_t lda_k, const float* S
     if (M == 0 || N == 0) return;
     const int64_t kps = round_up(ceil_div(K, split_k), BK);
     dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)split_k);
-    gemm_dense_kernel<TA><<<grid, NT, 0, st>>>(A, lda_m, lda_k, S, B, ldb_k, ldb_n, C, M, N, K,
+    launch_pdl(gemm_dense_kernel<TA>, dim3(grid), dim3(NT), 0, st, A, lda_m, lda_k, S, B, ldb_k, ldb_n, C, M, N, K,
                                                kps);
-    MOE_LAUNCH_CHECK();
 }
 
 __global__ void splitk_reduce_kernel(const float* __restrict__ part, int split_k, int64_t MN,
                                      float* __restrict__ out) {
+    pdl_wait();
+    pdl_trigger();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= MN) return;
     float acc = 0.f;
@@ -114,8 +117,7 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ part, int split_k
 
 void launch_splitk_reduce(const float* part, int split_k, int64_t MN, float* out,
                           cudaStream_t st) {
-    splitk_reduce_kernel<<<(unsigned)ceil_div(MN, 256), 256, 0, st>>>(part, split_k, MN, out);
-    MOE_LAUNCH_CHECK();
+    launch_pdl(splitk_reduce_kernel, dim3((unsigned)ceil_div(MN, 256)), dim3(256), 0, st, part, split_k, MN, out);
 }
 
 template void launch_gemm_dense<float>(const float*, int64_t, int64_t, const float*,
@@ -132,6 +134,8 @@ template void launch_gemm_dense<__nv_bfloat16>(const __nv_bfloat16*, int64_t, in
 template <class T>
 __global__ void __launch_bounds__(NT)
 row_gemm_simt_kernel(RowGemmArgs a) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ __align__(16) float As[BK][BM + 4];
     __shared__ __align__(16) float Bs[BK][BN + 4];
     const int seg = blockIdx.z;             // r * El + le
@@ -198,8 +202,7 @@ row_gemm_simt_kernel(RowGemmArgs a) {
 template <class T>
 void launch_row_gemm_simt(const RowGemmArgs& a, cudaStream_t st) {
     dim3 grid((unsigned)ceil_div(a.N, BN), (unsigned)ceil_div(a.cap_pad, BM), (unsigned)(a.ep * a.El));
-    row_gemm_simt_kernel<T><<<grid, NT, 0, st>>>(a);
-    MOE_LAUNCH_CHECK();
+    launch_pdl(row_gemm_simt_kernel<T>, dim3(grid), dim3(NT), 0, st, a);
 }
 
 // ---------------------------------------------------------------------------
@@ -208,6 +211,8 @@ void launch_row_gemm_simt(const RowGemmArgs& a, cudaStream_t st) {
 template <class T>
 __global__ void __launch_bounds__(NT)
 wgrad_gemm_simt_kernel(WgradGemmArgs a) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ __align__(16) float As[BK][BM + 4];
     __shared__ __align__(16) float Bs[BK][BN + 4];
     const int g = blockIdx.z;
@@ -250,8 +255,7 @@ wgrad_gemm_simt_kernel(WgradGemmArgs a) {
 template <class T>
 void launch_wgrad_gemm_simt(const WgradGemmArgs& a, cudaStream_t st) {
     dim3 grid((unsigned)ceil_div(a.N, BN), (unsigned)ceil_div(a.M, BM), (unsigned)a.El);
-    wgrad_gemm_simt_kernel<T><<<grid, NT, 0, st>>>(a);
-    MOE_LAUNCH_CHECK();
+    launch_pdl(wgrad_gemm_simt_kernel<T>, dim3(grid), dim3(NT), 0, st, a);
 }
 
 template void launch_row_gemm_simt<float>(const RowGemmArgs&, cudaStream_t);

@@ -170,6 +170,8 @@ __global__ void __launch_bounds__(kThreads, 1) grouped_gemm_kernel(const __grid_
                      "r"(512));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
+    pdl_wait();  // barriers, TMEM and tensor maps are set up; now the predecessor's data
+    pdl_trigger();
     for (int i = threadIdx.x; i < nseg; i += blockDim.x) seg_cnt[i] = p.counts[i];
     __syncthreads();
     Sched s{seg_cnt, grp_mt, grp_base, 0};
@@ -556,6 +558,8 @@ gemm2_kernel(const __grid_constant__ Params p) {
                      "r"(512));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     }
+    pdl_wait();  // barriers, TMEM and tensor maps are set up; now the predecessor's data
+    pdl_trigger();
     for (int i = threadIdx.x; i < nseg; i += blockDim.x) seg_cnt[i] = p.counts[i];
     __syncthreads();
     Sched s{seg_cnt, grp_mt, grp_base, 0};
@@ -865,8 +869,7 @@ void launch(const Params& p, int64_t max_tiles, cudaStream_t st) {
         attr = true;
     }
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms(), max_tiles)));
-    grouped_gemm_kernel<KIND><<<grid, kThreads, KCfg<KIND>::smem, st>>>(p);
-    MOE_LAUNCH_CHECK();
+    launch_pdl(grouped_gemm_kernel<KIND>, dim3(grid), dim3(kThreads), KCfg<KIND>::smem, st, p);
 }
 
 
@@ -880,8 +883,7 @@ void launch_pair(const Params& p, int64_t max_pair_tiles, cudaStream_t st) {
         attr = true;
     }
     const int npairs = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms() / 2, max_pair_tiles)));
-    pair::gemm2_kernel<KIND><<<2 * npairs, kThreads, pair::kSmem, st>>>(p);
-    MOE_LAUNCH_CHECK();
+    launch_pdl(pair::gemm2_kernel<KIND>, dim3(2 * npairs), dim3(kThreads), pair::kSmem, st, p);
 }
 
 // 2-CTA pairs pay off when the MMA is the bottleneck: every expert has >= 2

@@ -75,6 +75,13 @@ int capacity_of(int64_t tokens, const moe_router_cfg* c, int phase) {
 namespace moe {
 static std::atomic<uint64_t> g_launches{0};
 uint64_t count_launch() { return g_launches.fetch_add(1, std::memory_order_relaxed) + 1; }
+bool pdl_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("MOE_B200_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 }  // namespace moe
 
 namespace {

@@ -33,6 +33,8 @@ __device__ __forceinline__ double gval(const T* g, int64_t i) {
 template <class T>
 __global__ void __launch_bounds__(kNormThreads)
 sqnorm_partials_kernel(const T* __restrict__ g, int64_t n, double* __restrict__ partials) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ double s[kNormThreads];
     double acc = 0.0;
     for (int64_t i = (int64_t)blockIdx.x * kNormThreads + threadIdx.x; i < n;
@@ -51,6 +53,8 @@ sqnorm_partials_kernel(const T* __restrict__ g, int64_t n, double* __restrict__ 
 
 __global__ void __launch_bounds__(kNormThreads)
 sqnorm_finalize_kernel(const double* __restrict__ partials, double* __restrict__ acc) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ double s[kNormThreads];
     double a = 0.0;
     for (int i = threadIdx.x; i < kNormBlocks; i += kNormThreads) a += partials[i];
@@ -64,6 +68,8 @@ sqnorm_finalize_kernel(const double* __restrict__ partials, double* __restrict__
 }
 
 __global__ void clip_scale_kernel(const double* __restrict__ sq, double clip, double* __restrict__ scale) {
+    pdl_wait();
+    pdl_trigger();
     // optim.cpp:26-37: scale = clip / ||g|| when clip > 0 and ||g|| > clip
     const double norm = sqrt(*sq);
     *scale = (clip > 0.0 && norm > clip) ? clip / norm : 1.0;
@@ -75,6 +81,8 @@ adam_kernel(float* __restrict__ theta, float* __restrict__ m, float* __restrict_
             const G* __restrict__ g, int64_t n, __nv_bfloat16* __restrict__ shadow,
             const double* __restrict__ scale_p, double lr, double b1, double b2, double eps,
             double bc1, double bc2) {
+    pdl_wait();
+    pdl_trigger();
     const double scale = scale_p ? *scale_p : 1.0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {

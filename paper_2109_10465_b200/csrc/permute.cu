@@ -27,6 +27,8 @@ __global__ void __launch_bounds__(kRowWarps * 32)
 dispatch_gather_kernel(const TIO* __restrict__ x, int64_t d, int E, int K, int cap_pad,
                        const int32_t* __restrict__ row_src, const int32_t* __restrict__ kept,
                        TIO* __restrict__ buf) {
+    pdl_wait();
+    pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t r = (int64_t)blockIdx.x * kRowWarps + warp;
     if (r >= (int64_t)E * cap_pad) return;
@@ -65,12 +67,11 @@ void launch_dispatch_gather(const TIO* x, int64_t d, int E, int K, int cap_pad,
     const int64_t rows = (int64_t)E * cap_pad;
     const unsigned grid = (unsigned)ceil_div(rows, kRowWarps);
     if (vec_width<TIO>(d) > 1)
-        dispatch_gather_kernel<TIO, 16 / sizeof(TIO)><<<grid, kRowWarps * 32, 0, st>>>(
+        launch_pdl(dispatch_gather_kernel<TIO, 16 / sizeof(TIO)>, dim3(grid), dim3(kRowWarps * 32), 0, st, 
             x, d, E, K, cap_pad, row_src, kept, buf);
     else
-        dispatch_gather_kernel<TIO, 1><<<grid, kRowWarps * 32, 0, st>>>(x, d, E, K, cap_pad,
+        launch_pdl(dispatch_gather_kernel<TIO, 1>, dim3(grid), dim3(kRowWarps * 32), 0, st, x, d, E, K, cap_pad,
                                                                          row_src, kept, buf);
-    MOE_LAUNCH_CHECK();
 }
 
 // y[t] = sum_{k kept} w[t*K+k] * O[row_k]  (accumulated from 0 in k order,
@@ -81,6 +82,8 @@ combine_kernel(const TIO* __restrict__ O, int64_t T, int64_t d, int K, int cap_p
                const int32_t* __restrict__ choice, const int32_t* __restrict__ pos,
                const float* __restrict__ w, const TIO* __restrict__ residual, TIO* __restrict__ y,
                uint32_t* __restrict__ flags) {
+    pdl_wait();
+    pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t t = (int64_t)blockIdx.x * kRowWarps + warp;
     if (t >= T) return;
@@ -128,12 +131,11 @@ void launch_combine(const TIO* O, int64_t T, int64_t d, int E, int K, int cap_pa
     (void)E;
     const unsigned grid = (unsigned)ceil_div(T, kRowWarps);
     if (vec_width<TIO>(d) > 1)
-        combine_kernel<TIO, 16 / sizeof(TIO)><<<grid, kRowWarps * 32, 0, st>>>(
+        launch_pdl(combine_kernel<TIO, 16 / sizeof(TIO)>, dim3(grid), dim3(kRowWarps * 32), 0, st, 
             O, T, d, K, cap_pad, choice, pos, w, residual, y, flags);
     else
-        combine_kernel<TIO, 1><<<grid, kRowWarps * 32, 0, st>>>(O, T, d, K, cap_pad, choice, pos,
+        launch_pdl(combine_kernel<TIO, 1>, dim3(grid), dim3(kRowWarps * 32), 0, st, O, T, d, K, cap_pad, choice, pos,
                                                                 w, residual, y, flags);
-    MOE_LAUNCH_CHECK();
 }
 
 // dO[r] = w[src] * dy[t(src)] for occupied rows; zero tail up to 128 rows.
@@ -142,6 +144,8 @@ __global__ void __launch_bounds__(kRowWarps * 32)
 combine_bwd_gather_kernel(const TIO* __restrict__ dy, int64_t d, int K, int cap_pad,
                           const int32_t* __restrict__ row_src, const int32_t* __restrict__ kept,
                           const float* __restrict__ w, TIO* __restrict__ dO, int64_t rows) {
+    pdl_wait();
+    pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t r = (int64_t)blockIdx.x * kRowWarps + warp;
     if (r >= rows) return;
@@ -172,12 +176,11 @@ void launch_combine_bwd_gather(const TIO* dy, int64_t d, int E, int K, int cap_p
     const int64_t rows = (int64_t)E * cap_pad;
     const unsigned grid = (unsigned)ceil_div(rows, kRowWarps);
     if (vec_width<TIO>(d) > 1)
-        combine_bwd_gather_kernel<TIO, 16 / sizeof(TIO)><<<grid, kRowWarps * 32, 0, st>>>(
+        launch_pdl(combine_bwd_gather_kernel<TIO, 16 / sizeof(TIO)>, dim3(grid), dim3(kRowWarps * 32), 0, st, 
             dy, d, K, cap_pad, row_src, kept, w, dO, rows);
     else
-        combine_bwd_gather_kernel<TIO, 1><<<grid, kRowWarps * 32, 0, st>>>(dy, d, K, cap_pad,
+        launch_pdl(combine_bwd_gather_kernel<TIO, 1>, dim3(grid), dim3(kRowWarps * 32), 0, st, dy, d, K, cap_pad,
                                                                            row_src, kept, w, dO, rows);
-    MOE_LAUNCH_CHECK();
 }
 
 // dx[t] = dxg[t] * noise[t] + sum_{k kept} dX[row_k] (+ dy[t] if no route kept
@@ -191,6 +194,8 @@ dx_assemble_kernel(int64_t T, int64_t d, int K, int cap_pad, const float* __rest
                    const int32_t* __restrict__ choice, const int32_t* __restrict__ pos,
                    const TIO* __restrict__ dy, bool residual_is_x, TIO* __restrict__ dx,
                    TIO* __restrict__ dres) {
+    pdl_wait();
+    pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t t = (int64_t)blockIdx.x * kRowWarps + warp;
     if (t >= T) return;
@@ -260,12 +265,11 @@ void launch_dx_assemble(int64_t T, int64_t d, int E, int K, int cap_pad, const f
     (void)E;
     const unsigned grid = (unsigned)ceil_div(T, kRowWarps);
     if (vec_width<TIO>(d) > 1)
-        dx_assemble_kernel<TIO, 16 / sizeof(TIO)><<<grid, kRowWarps * 32, 0, st>>>(
+        launch_pdl(dx_assemble_kernel<TIO, 16 / sizeof(TIO)>, dim3(grid), dim3(kRowWarps * 32), 0, st, 
             T, d, K, cap_pad, dxg, noise, dX, choice, pos, dy, residual_is_x, dx, dres);
     else
-        dx_assemble_kernel<TIO, 1><<<grid, kRowWarps * 32, 0, st>>>(
+        launch_pdl(dx_assemble_kernel<TIO, 1>, dim3(grid), dim3(kRowWarps * 32), 0, st, 
             T, d, K, cap_pad, dxg, noise, dX, choice, pos, dy, residual_is_x, dx, dres);
-    MOE_LAUNCH_CHECK();
 }
 
 // Utilization + drop statistics of one routing decision, accumulated into
@@ -277,6 +281,8 @@ __global__ void decision_stats_kernel(int64_t T, int E, int K, const int32_t* __
                                       const int32_t* __restrict__ pos,
                                       unsigned long long* __restrict__ util,
                                       unsigned long long* __restrict__ hist) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ unsigned int s_cnt[];  // [E] + [9]
     for (int i = threadIdx.x; i < E + 9; i += blockDim.x) s_cnt[i] = 0;
     __syncthreads();
@@ -307,14 +313,15 @@ __global__ void decision_stats_kernel(int64_t T, int E, int K, const int32_t* __
 void launch_decision_stats(int64_t T, int E, int K, const int32_t* choice, const int32_t* pos,
                            int64_t* util, int64_t* hist, cudaStream_t st) {
     const int blocks = (int)std::min<int64_t>(kNumSMs, ceil_div(T, (int64_t)256));
-    decision_stats_kernel<<<blocks, 256, sizeof(unsigned int) * (E + 9), st>>>(
+    launch_pdl(decision_stats_kernel, dim3(blocks), dim3(256), sizeof(unsigned int) * (E + 9), st, 
         T, E, K, choice, pos, reinterpret_cast<unsigned long long*>(util),
         reinterpret_cast<unsigned long long*>(hist));
-    MOE_LAUNCH_CHECK();
 }
 
 __global__ void combine_weights_kernel(int64_t T, int E, int K, const float* __restrict__ gp,
                                        float* __restrict__ w) {
+    pdl_wait();
+    pdl_trigger();
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= T) return;
     if (K == 1) {
@@ -329,8 +336,7 @@ __global__ void combine_weights_kernel(int64_t T, int E, int K, const float* __r
 
 void launch_combine_weights(int64_t T, int E, int K, const float* gate_prob, float* w,
                             cudaStream_t st) {
-    combine_weights_kernel<<<(unsigned)ceil_div(T, 256), 256, 0, st>>>(T, E, K, gate_prob, w);
-    MOE_LAUNCH_CHECK();
+    launch_pdl(combine_weights_kernel, dim3((unsigned)ceil_div(T, 256)), dim3(256), 0, st, T, E, K, gate_prob, w);
 }
 
 // db[g][n] = sum_{r, i < count(r,g)} src[(r*El+g)*cap_pad + i][n], fixed order.
@@ -343,6 +349,8 @@ template <class TIO>
 __global__ void __launch_bounds__(128 * kColsumRG)
 colsum_groups_kernel(const TIO* __restrict__ src, int64_t N, int ep, int El, int cap_pad,
                      const int32_t* __restrict__ counts, float* __restrict__ db) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ float part[kColsumRG][128];
     const int c = threadIdx.x & 127, rg = threadIdx.x >> 7;
     const int64_t nblk = (N + 127) / 128;
@@ -374,14 +382,15 @@ template <class TIO>
 void launch_colsum_groups(const TIO* src, int64_t N, int ep, int El, int cap_pad,
                           const int32_t* counts, float* db, cudaStream_t st) {
     const int64_t items = ceil_div(N, (int64_t)128) * El;
-    colsum_groups_kernel<TIO><<<(unsigned)std::min<int64_t>(items, kNumSMs), 128 * kColsumRG, 0, st>>>(
+    launch_pdl(colsum_groups_kernel<TIO>, dim3((unsigned)std::min<int64_t>(items, kNumSMs)), dim3(128 * kColsumRG), 0, st, 
         src, N, ep, El, cap_pad, counts, db);
-    MOE_LAUNCH_CHECK();
 }
 
 __global__ void colsum_parts_kernel(const float* __restrict__ part, int64_t N, int ep, int El,
                                     int cap_pad, const int32_t* __restrict__ counts,
                                     float* __restrict__ db) {
+    pdl_wait();
+    pdl_trigger();
     const int g = blockIdx.y;
     const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= N) return;
@@ -399,11 +408,12 @@ __global__ void colsum_parts_kernel(const float* __restrict__ part, int64_t N, i
 void launch_colsum_parts(const float* part, int64_t N, int ep, int El, int cap_pad,
                          const int32_t* counts, float* db, cudaStream_t st) {
     dim3 grid((unsigned)ceil_div(N, 128), El);
-    colsum_parts_kernel<<<grid, 128, 0, st>>>(part, N, ep, El, cap_pad, counts, db);
-    MOE_LAUNCH_CHECK();
+    launch_pdl(colsum_parts_kernel, dim3(grid), dim3(128), 0, st, part, N, ep, El, cap_pad, counts, db);
 }
 
 __global__ void convert_f64_kernel(const double* __restrict__ src, int64_t n, bool bf16, void* dst) {
+    pdl_wait();
+    pdl_trigger();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         if (bf16) static_cast<__nv_bfloat16*>(dst)[i] = __double2bfloat16(src[i]);
@@ -413,9 +423,8 @@ __global__ void convert_f64_kernel(const double* __restrict__ src, int64_t n, bo
 
 void launch_convert_f64(const double* src, int64_t n, bool bf16, void* dst, cudaStream_t st) {
     if (n <= 0) return;
-    convert_f64_kernel<<<(unsigned)std::min<int64_t>(8 * kNumSMs, ceil_div(n, (int64_t)256)), 256, 0, st>>>(
+    launch_pdl(convert_f64_kernel, dim3((unsigned)std::min<int64_t>(8 * kNumSMs, ceil_div(n, (int64_t)256))), dim3(256), 0, st, 
         src, n, bf16, dst);
-    MOE_LAUNCH_CHECK();
 }
 
 // ---- reference-layout per-stage kernels ------------------------------------
@@ -424,6 +433,8 @@ __global__ void dispatch_ref_kernel(const TIO* __restrict__ x, int64_t T, int64_
                                     int cap, const int32_t* __restrict__ eid,
                                     const int32_t* __restrict__ slot, TIO* __restrict__ buf,
                                     uint8_t* __restrict__ occ) {
+    pdl_wait();
+    pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t i = (int64_t)blockIdx.x * kRowWarps + warp;  // route index
     if (i >= T * K) return;
@@ -442,9 +453,8 @@ void launch_dispatch_ref(const TIO* x, int64_t T, int64_t d, int E, int K, int c
     MOE_CUDA_CHECK(cudaMemsetAsync(buf, 0, sizeof(TIO) * (size_t)E * cap * d, st));
     if (occ) MOE_CUDA_CHECK(cudaMemsetAsync(occ, 0, (size_t)E * cap, st));
     if (T * K == 0) return;
-    dispatch_ref_kernel<TIO><<<(unsigned)ceil_div(T * K, kRowWarps), kRowWarps * 32, 0, st>>>(
+    launch_pdl(dispatch_ref_kernel<TIO>, dim3((unsigned)ceil_div(T * K, kRowWarps)), dim3(kRowWarps * 32), 0, st, 
         x, T, d, K, cap, expert_id, slot, buf, occ);
-    MOE_LAUNCH_CHECK();
 }
 
 template <class TIO>
@@ -452,6 +462,8 @@ __global__ void combine_ref_kernel(const TIO* __restrict__ O, int64_t T, int64_t
                                    int cap, const int32_t* __restrict__ eid,
                                    const int32_t* __restrict__ slot, const float* __restrict__ w,
                                    const TIO* __restrict__ residual, TIO* __restrict__ y) {
+    pdl_wait();
+    pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t t = (int64_t)blockIdx.x * kRowWarps + warp;
     if (t >= T) return;
@@ -479,12 +491,13 @@ void launch_combine_ref(const TIO* O, int64_t T, int64_t d, int E, int K, int ca
                         const int32_t* expert_id, const int32_t* slot, const float* w,
                         const TIO* residual, TIO* y, cudaStream_t st) {
     (void)E;
-    combine_ref_kernel<TIO><<<(unsigned)ceil_div(T, kRowWarps), kRowWarps * 32, 0, st>>>(
+    launch_pdl(combine_ref_kernel<TIO>, dim3((unsigned)ceil_div(T, kRowWarps)), dim3(kRowWarps * 32), 0, st, 
         O, T, d, K, cap, expert_id, slot, w, residual, y);
-    MOE_LAUNCH_CHECK();
 }
 
 __global__ void check_finite_kernel(const float* __restrict__ p, int64_t n, uint32_t* flags) {
+    pdl_wait();
+    pdl_trigger();
     bool bad = false;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -494,9 +507,8 @@ __global__ void check_finite_kernel(const float* __restrict__ p, int64_t n, uint
 
 void launch_check_finite_f32(const float* p, int64_t n, uint32_t* flags, cudaStream_t st) {
     if (n <= 0) return;
-    check_finite_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 4 * kNumSMs), 256, 0, st>>>(
+    launch_pdl(check_finite_kernel, dim3((unsigned)std::min<int64_t>(ceil_div(n, 256), 4 * kNumSMs)), dim3(256), 0, st, 
         p, n, flags);
-    MOE_LAUNCH_CHECK();
 }
 
 #define INST(T)                                                                                  \
@@ -534,6 +546,8 @@ namespace moe {
 // proportion to its size; a CTA streams 16-byte vectors, 8 per thread in
 // flight, from local HBM to the (local or NVLink peer) destination.
 __global__ void __launch_bounds__(256) peer_copy_kernel(PeerCopyJobs jobs, int ctas_per_job) {
+    pdl_wait();
+    pdl_trigger();
     const int j = blockIdx.x / ctas_per_job;
     if (j >= jobs.n) return;
     const int64_t nv = jobs.bytes[j] >> 4;
@@ -562,8 +576,7 @@ void launch_peer_copy(const PeerCopyJobs& jobs, cudaStream_t st) {
     }
     if (maxv == 0 || jobs.n == 0) return;
     const int per = (int)std::max<int64_t>(1, std::min<int64_t>(4 * kNumSMs / jobs.n, ceil_div(maxv, (int64_t)256 * 8)));
-    peer_copy_kernel<<<per * jobs.n, 256, 0, st>>>(jobs, per);
-    MOE_LAUNCH_CHECK();
+    launch_pdl(peer_copy_kernel, dim3(per * jobs.n), dim3(256), 0, st, jobs, per);
 }
 
 // out[i] = sum_r src[r][i] over the ranks' (NVLink-mapped) copies, in rank
@@ -572,6 +585,8 @@ struct RankSrcs {
     const float* p[8];
 };
 __global__ void sum_ranks_kernel(RankSrcs s, int ep, int64_t n, float* __restrict__ out) {
+    pdl_wait();
+    pdl_trigger();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n / 4; i += (int64_t)gridDim.x * blockDim.x) {
         float4 acc = reinterpret_cast<const float4*>(s.p[0])[i];
         for (int r = 1; r < ep; ++r) {
@@ -586,9 +601,8 @@ void launch_sum_ranks(const float* const* srcs, int ep, int64_t n, float* out, c
     if (n % 4) throw Status(1, "sum_ranks: element count must be a multiple of 4");
     RankSrcs s{};
     for (int r = 0; r < ep; ++r) s.p[r] = srcs[r];
-    sum_ranks_kernel<<<(unsigned)std::min<int64_t>(2 * kNumSMs, ceil_div(n / 4, (int64_t)256)), 256, 0, st>>>(
+    launch_pdl(sum_ranks_kernel, dim3((unsigned)std::min<int64_t>(2 * kNumSMs, ceil_div(n / 4, (int64_t)256))), dim3(256), 0, st, 
         s, ep, n, out);
-    MOE_LAUNCH_CHECK();
 }
 
 // Device-side barrier over NVLink peer memory for the IPC exchanges: every
@@ -599,6 +613,8 @@ void launch_sum_ranks(const float* const* srcs, int ep, int64_t n, float* out, c
 // instead of hanging forever if a peer never arrives.
 __global__ void ipc_barrier_kernel(PeerFlags peers, const unsigned long long* mine, int rank, int ep,
                                    unsigned long long epoch) {
+    pdl_wait();
+    pdl_trigger();
     const int i = threadIdx.x;
     if (i < ep) {
         __threadfence_system();
@@ -614,8 +630,7 @@ __global__ void ipc_barrier_kernel(PeerFlags peers, const unsigned long long* mi
 
 void launch_ipc_barrier(const PeerFlags& peers, const unsigned long long* mine, int rank, int ep,
                         unsigned long long epoch, cudaStream_t st) {
-    ipc_barrier_kernel<<<1, 32, 0, st>>>(peers, mine, rank, ep, epoch);
-    MOE_LAUNCH_CHECK();
+    launch_pdl(ipc_barrier_kernel, dim3(1), dim3(32), 0, st, peers, mine, rank, ep, epoch);
 }
 
 }  // namespace moe

@@ -335,6 +335,8 @@ chunk_kernel(const __grid_constant__ InitWords init, const uint16_t* __restrict_
         mbar_init(&empty[1], 32 * kEmitters);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    pdl_wait();  // the noise buffer may still be read by the previous kernels
+    pdl_trigger();
     __syncthreads();
     constexpr int R = kJumpR;
     if (warp == 0) {
@@ -541,9 +543,8 @@ void generate(uint64_t seed, int64_t count, double lo, double hi, float* noise, 
     // debug (timing runs only): =1 drops the stores, timing the recurrence alone
     static const bool null_out = timing && std::getenv("MOE_B200_RNG_NULL_OUT") != nullptr;
     if (null_out) noise = nullptr, raw = nullptr;
-    chunk_kernel<<<P, kChunkThreads, smem, st>>>(init, tab.dev, J, count, lo, hi - lo, noise, raw,
-                                                 timing ? tdbg : nullptr);
-    MOE_LAUNCH_CHECK();
+    launch_pdl(chunk_kernel, dim3(P), dim3(kChunkThreads), smem, st, init, tab.dev, J, count, lo, hi - lo,
+               noise, raw, timing ? tdbg : nullptr);
     if (timing) {  // debug: per-phase times averaged over CTAs (synchronises)
         std::vector<unsigned long long> h(8 * static_cast<size_t>(P));
         MOE_CUDA_CHECK(cudaStreamSynchronize(st));

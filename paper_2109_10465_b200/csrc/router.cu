@@ -33,6 +33,8 @@ softmax_topk_kernel(const float* __restrict__ logits, int64_t T, int E, int K,
                     float* __restrict__ probs, int32_t* __restrict__ choice,
                     float* __restrict__ gate_prob, float* __restrict__ colsum_part,
                     int32_t* __restrict__ count_part, uint32_t* __restrict__ flags) {
+    pdl_wait();
+    pdl_trigger();
     const int64_t TE = T * E;
     extern __shared__ float sm[];
     float* s_col = sm;                                   // [warps][E]
@@ -157,6 +159,8 @@ balance_finalize_kernel(const float* __restrict__ colsum_part, const int32_t* __
                         int nparts, int64_t T, int E, double alpha, float* __restrict__ aux,
                         float* __restrict__ fcoef, int32_t* __restrict__ counts,
                         double* __restrict__ term, unsigned* __restrict__ done) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ double s_cs[256];
     __shared__ long long s_cnt[256];
     __shared__ bool last;
@@ -203,7 +207,7 @@ void launch_softmax_topk(const float* logits, int nsplit, int64_t T, int E, int 
     const size_t smem = sizeof(float) * kSoftmaxWarps * E + sizeof(int32_t) * E;
     const int nl = E <= 32 ? 1 : E <= 64 ? 2 : E <= 128 ? 4 : 8;
     auto go = [&](auto kernel) {
-        kernel<<<nparts, kSoftmaxWarps * 32, smem, st>>>(logits, T, E, K, probs, choice, gate_prob,
+        launch_pdl(kernel, dim3(nparts), dim3(kSoftmaxWarps * 32), smem, st, logits, T, E, K, probs, choice, gate_prob,
                                                          colsum_part, count_part, flags);
     };
 #define MOE_SOFTMAX_NS(NLV)                                                           \
@@ -229,9 +233,8 @@ int softmax_parts(int64_t T) { return (int)ceil_div(T, (int64_t)kRowsPerPart); }
 void launch_balance_finalize(const float* colsum_part, const int32_t* count_part, int nparts,
                              int64_t T, int E, double alpha, float* aux, float* fcoef,
                              int32_t* counts, double* term, unsigned* done, cudaStream_t st) {
-    balance_finalize_kernel<<<E, 256, 0, st>>>(colsum_part, count_part, nparts, T, E, alpha, aux,
+    launch_pdl(balance_finalize_kernel, dim3(E), dim3(256), 0, st, colsum_part, count_part, nparts, T, E, alpha, aux,
                                                fcoef, counts, term, done);
-    MOE_LAUNCH_CHECK();
 }
 
 // ---------------------------------------------------------------------------
@@ -276,6 +279,8 @@ __global__ void __launch_bounds__(kChunk)
 assign_count_kernel(ScanGeom g, const int32_t* __restrict__ choice,
                     const uint32_t* __restrict__ ord, int32_t* __restrict__ hist,
                     uint32_t* __restrict__ flags) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ int32_t s_h[];  // [K][E]
     for (int i = threadIdx.x; i < g.K * g.E; i += blockDim.x) s_h[i] = 0;
     __syncthreads();
@@ -306,6 +311,8 @@ assign_count_kernel(ScanGeom g, const int32_t* __restrict__ choice,
 __global__ void assign_scan_kernel(ScanGeom g, const int32_t* __restrict__ hist,
                                    int32_t* __restrict__ base, int32_t* __restrict__ gkept,
                                    int32_t* __restrict__ kept) {
+    pdl_wait();
+    pdl_trigger();
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= g.E) return;
     int32_t run_compact = 0;
@@ -339,6 +346,8 @@ assign_rank_kernel(ScanGeom g, const int32_t* __restrict__ choice,
                    const uint32_t* __restrict__ ord, const int32_t* __restrict__ base,
                    const int32_t* __restrict__ gkept, int cap_pad, int32_t* __restrict__ slot,
                    int32_t* __restrict__ pos, int32_t* __restrict__ row_src) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ int32_t s_w[];  // [32 warps][E]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int64_t b, e;
@@ -396,14 +405,11 @@ void launch_assign(int64_t T, int E, int K, int cap, int mode, int G, const int3
     const int nchunks = g.G * g.cpg;
     if (nchunks > s.max_chunks || g.G > s.max_groups)
         throw Status(1, "assign: scratch too small");
-    assign_count_kernel<<<nchunks, kChunk, sizeof(int32_t) * K * E, st>>>(g, choice, ord, s.hist,
+    launch_pdl(assign_count_kernel, dim3(nchunks), dim3(kChunk), sizeof(int32_t) * K * E, st, g, choice, ord, s.hist,
                                                                            flags);
-    MOE_LAUNCH_CHECK();
-    assign_scan_kernel<<<(int)ceil_div(E, 128), 128, 0, st>>>(g, s.hist, s.base, s.gkept, kept);
-    MOE_LAUNCH_CHECK();
-    assign_rank_kernel<<<nchunks, kChunk, sizeof(int32_t) * 32 * E, st>>>(
+    launch_pdl(assign_scan_kernel, dim3((int)ceil_div(E, 128)), dim3(128), 0, st, g, s.hist, s.base, s.gkept, kept);
+    launch_pdl(assign_rank_kernel, dim3(nchunks), dim3(kChunk), sizeof(int32_t) * 32 * E, st, 
         g, choice, ord, s.base, s.gkept, cap_pad, slot, pos, row_src);
-    MOE_LAUNCH_CHECK();
 }
 
 size_t assign_scratch_ints(int64_t T, int E, int K, int G) {
@@ -426,6 +432,8 @@ router_bwd_kernel(int64_t T, int d, int E, int K, const TIO* __restrict__ dy,
                   const int32_t* __restrict__ pos, const float* __restrict__ gate_prob,
                   const float* __restrict__ probs, const float* __restrict__ fcoef, float daux,
                   float* __restrict__ dL) {
+    pdl_wait();
+    pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t t = (int64_t)blockIdx.x * 8 + warp;
     if (t >= T) return;
@@ -481,12 +489,11 @@ void launch_router_bwd(int64_t T, int d, int E, int K, const TIO* dy, const TIO*
                        const float* probs, const float* fcoef, float daux, float* dL,
                        cudaStream_t st) {
     if (vec_width<TIO>(d) > 1)
-        router_bwd_kernel<TIO, 16 / sizeof(TIO)><<<(int)ceil_div(T, 8), 256, 0, st>>>(
+        launch_pdl(router_bwd_kernel<TIO, 16 / sizeof(TIO)>, dim3((int)ceil_div(T, 8)), dim3(256), 0, st, 
             T, d, E, K, dy, O, cap_pad, choice, pos, gate_prob, probs, fcoef, daux, dL);
     else
-        router_bwd_kernel<TIO, 1><<<(int)ceil_div(T, 8), 256, 0, st>>>(
+        launch_pdl(router_bwd_kernel<TIO, 1>, dim3((int)ceil_div(T, 8)), dim3(256), 0, st, 
             T, d, E, K, dy, O, cap_pad, choice, pos, gate_prob, probs, fcoef, daux, dL);
-    MOE_LAUNCH_CHECK();
 }
 
 template void launch_router_bwd<float>(int64_t, int, int, int, const float*, const float*, int,
@@ -507,6 +514,8 @@ __global__ void __launch_bounds__(256)
 balance_partials_kernel(const float* __restrict__ probs, int64_t T, int E, int K,
                         const int32_t* __restrict__ eid, float* __restrict__ colsum_part,
                         int32_t* __restrict__ count_part, uint32_t* __restrict__ flags) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ float sm[];
     float* s_col = sm;
     int32_t* s_cnt = reinterpret_cast<int32_t*>(sm + 8 * E);
@@ -545,9 +554,8 @@ void launch_balance_from_probs(const float* probs, int64_t T, int E, int K,
                                float* colsum_part, int32_t* count_part, uint32_t* flags,
                                double* term, unsigned* done, cudaStream_t st) {
     const int nparts = softmax_parts(T);
-    balance_partials_kernel<<<nparts, 256, sizeof(float) * 8 * E + sizeof(int32_t) * E, st>>>(
+    launch_pdl(balance_partials_kernel, dim3(nparts), dim3(256), sizeof(float) * 8 * E + sizeof(int32_t) * E, st, 
         probs, T, E, K, expert_id, colsum_part, count_part, flags);
-    MOE_LAUNCH_CHECK();
     launch_balance_finalize(colsum_part, count_part, nparts, T, E, alpha, loss, nullptr, nullptr,
                             term, done, st);
 }
