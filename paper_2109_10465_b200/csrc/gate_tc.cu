@@ -151,8 +151,9 @@ struct LogitsSmem {
     static constexpr uint32_t bytes = 1024 + 2 * buf + 256;
 };
 
+constexpr int NTL = 256;  // logits: 8 warps stage / transform, 2 CTAs per SM
 template <class TX, int E>
-__global__ void __launch_bounds__(NT, 2)
+__global__ void __launch_bounds__(NTL, 2)
 logits_kernel(const TX* __restrict__ x, const float* __restrict__ noise, const float* __restrict__ wgt,
               float* __restrict__ out, int64_t T, int d, int k_per_split) {
     using S = LogitsSmem<E>;
@@ -169,17 +170,20 @@ logits_kernel(const TX* __restrict__ x, const float* __restrict__ noise, const f
     pdl_wait();  // barriers and TMEM are set up; now the predecessor's data
     pdl_trigger();
 
-    // producer mapping: A: chunk c = tid % 8 (4 k), rows tid/8 + 16 i (i < 8)
-    //                   B: chunk c = tid % 8, rows e = tid/8 + 16 i (i < E/16)
+    // producer mapping: A: chunk c = tid % 8 (4 k), rows tid/8 + 32 i (i < 4)
+    //                   B: chunk c = tid % 8, rows e = tid/8 + 32 i (i < E/32)
+    // The raw loads run two K steps ahead in two register slots, so ~2 steps
+    // of x / noise are in flight per CTA while the tensor core works.
     const int ac = tid & 7, ar = tid >> 3;
-    constexpr int NB = E / 16;
-    Raw4<TX> xa[8];
-    Raw4<float> na[8], wb[NB];
-    auto load = [&](int step) {
+    constexpr int NA = BM / 32, NB = E / 32;
+    Raw4<TX> xa0[NA], xa1[NA];
+    Raw4<float> na0[NA], na1[NA], wb0[NB], wb1[NB];
+    auto load = [&](int step, Raw4<TX> (&xa)[NA], Raw4<float> (&na)[NA], Raw4<float> (&wb)[NB]) {
+        if (step >= nsteps) return;
         const int k0 = kb + step * BK;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int64_t t = t0 + ar + 16 * i;
+        for (int i = 0; i < NA; ++i) {
+            const int64_t t = t0 + ar + 32 * i;
             if (t < T) {
                 xa[i].load(x + t * d + k0 + 4 * ac);
                 if (noise) na[i].load(noise + t * d + k0 + 4 * ac);
@@ -188,21 +192,22 @@ logits_kernel(const TX* __restrict__ x, const float* __restrict__ noise, const f
             }
         }
 #pragma unroll
-        for (int i = 0; i < NB; ++i) wb[i].load(wgt + (int64_t)(ar + 16 * i) * d + k0 + 4 * ac);
+        for (int i = 0; i < NB; ++i) wb[i].load(wgt + (int64_t)(ar + 32 * i) * d + k0 + 4 * ac);
     };
-    auto store = [&](uint8_t* buf) {
+    auto store = [&](uint8_t* buf, const Raw4<TX> (&xa)[NA], const Raw4<float> (&na)[NA],
+                     const Raw4<float> (&wb)[NB]) {
         uint8_t* ahi = buf;
         uint8_t* alo = buf + S::A;
         uint8_t* bhi = buf + 2 * S::A;
         uint8_t* blo = bhi + S::B;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < NA; ++i) {
             float xv[4], nv[4] = {1.f, 1.f, 1.f, 1.f}, h[4], l[4];
             xa[i].get(xv);
             if (noise) na[i].get(nv);
 #pragma unroll
             for (int q = 0; q < 4; ++q) split_tf32(noise ? xv[q] * nv[q] : xv[q], h[q], l[q]);
-            const uint32_t off = swz(ar + 16 * i, ac);
+            const uint32_t off = swz(ar + 32 * i, ac);
             st4(ahi, off, h[0], h[1], h[2], h[3]);
             st4(alo, off, l[0], l[1], l[2], l[3]);
         }
@@ -212,19 +217,18 @@ logits_kernel(const TX* __restrict__ x, const float* __restrict__ noise, const f
             wb[i].get(wv);
 #pragma unroll
             for (int j = 0; j < 4; ++j) split_tf32(wv[j], h[j], l[j]);
-            const uint32_t off = swz(ar + 16 * i, ac);
+            const uint32_t off = swz(ar + 32 * i, ac);
             st4(bhi, off, h[0], h[1], h[2], h[3]);
             st4(blo, off, l[0], l[1], l[2], l[3]);
         }
     };
     constexpr uint32_t idesc = make_idesc_tf32(BM, E, 0, 0);
-    load(0);
-    for (int s = 0; s < nsteps; ++s) {
+    auto step = [&](int s, Raw4<TX> (&xa)[NA], Raw4<float> (&na)[NA], Raw4<float> (&wb)[NB]) {
         const int b = s & 1;
         uint8_t* buf = sm + b * S::buf;
         if (s >= 2) mbar_wait(&bars[b], ((s - 2) >> 1) & 1);
-        store(buf);
-        if (s + 1 < nsteps) load(s + 1);  // in flight during this step's MMAs
+        store(buf, xa, na, wb);
+        load(s + 2, xa, na, wb);  // two steps ahead, in flight during the MMAs
         publish_and_issue(&bars[b], [&] {
             const uint32_t a = smem_u32(buf), bb = a + 2 * S::A;
 #pragma unroll
@@ -239,28 +243,34 @@ logits_kernel(const TX* __restrict__ x, const float* __restrict__ noise, const f
                 tc_mma_tf32(acc, al, bh, idesc, 1u);
             }
         });
+    };
+    load(0, xa0, na0, wb0);
+    load(1, xa1, na1, wb1);
+    for (int s = 0; s < nsteps; s += 2) {
+        step(s, xa0, na0, wb0);
+        if (s + 1 < nsteps) step(s + 1, xa1, na1, wb1);
     }
     if (tid == 0) tc_commit(&bars[2]);
     mbar_wait(&bars[2], 0);
     tc_fence_after();
+    // epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31, columns half w / 4
     const int warp = tid >> 5, lane = tid & 31;
-    const int64_t t = t0 + warp * 32 + lane;
+    const int64_t t = t0 + (warp & 3) * 32 + lane;
+    const int c = (warp >> 2) * 32;
+    static_assert(E == 64, "logits epilogue: two 32-column halves");
+    float sum[32];
 #pragma unroll
-    for (int c = 0; c < E; c += 32) {
-        float sum[32];
+    for (int q = 0; q < kNAcc; ++q) {  // the accumulators, summed in fixed order
+        uint32_t v[32];
+        tmem_ld32(tmem + ((uint32_t)((warp & 3) * 32) << 16) + q * E + c, v);
 #pragma unroll
-        for (int q = 0; q < kNAcc; ++q) {  // the accumulators, summed in fixed order
-            uint32_t v[32];
-            tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + q * E + c, v);
+        for (int j = 0; j < 32; ++j) sum[j] = q ? sum[j] + __uint_as_float(v[j]) : __uint_as_float(v[j]);
+    }
+    if (t < T) {
+        float* o = out + t * E + c;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) sum[j] = q ? sum[j] + __uint_as_float(v[j]) : __uint_as_float(v[j]);
-        }
-        if (t < T) {
-            float* o = out + t * E + c;
-#pragma unroll
-            for (int j = 0; j < 32; j += 4)
-                *reinterpret_cast<float4*>(o + j) = make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]);
-        }
+        for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4*>(o + j) = make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]);
     }
     teardown(tmem, kNAcc * E);
 }
@@ -596,7 +606,7 @@ void launch_gate_tc_logits(const TX* x, const float* noise, const float* wgt, fl
     static bool attr = false;
     if (!attr) { gtc::set_smem(k, gtc::LogitsSmem<kE>::bytes); attr = true; }
     dim3 grid((unsigned)ceil_div(T, (int64_t)gtc::BM), (unsigned)splits);
-    launch_pdl(k, dim3(grid), dim3(gtc::NT), gtc::LogitsSmem<kE>::bytes, st, x, noise, wgt, logits, T, d, d / splits);
+    launch_pdl(k, dim3(grid), dim3(gtc::NTL), gtc::LogitsSmem<kE>::bytes, st, x, noise, wgt, logits, T, d, d / splits);
 }
 
 template <class TX>
