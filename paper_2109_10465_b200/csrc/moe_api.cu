@@ -270,6 +270,8 @@ void exchange(moe_handle* h, std::initializer_list<XSpec> specs, bool local_only
     }
     PeerCopyJobs jobs{};
     jobs.n = 0;
+    require(specs.size() * static_cast<size_t>(local_only ? 1 : h->ep) <= static_cast<size_t>(kMaxCopies),
+            MOE_UNSUPPORTED, "exchange: too many peer copies for one launch");
     for (const XSpec& x : specs) {
         const size_t bytes = x.chunk_elems * x.esz;
         if (local_only) {  // publish this rank's buffer in its own exported slot, then barrier
