@@ -82,6 +82,8 @@ struct __align__(64) Params {
     int epi;
     int b_mn;        // ROW: 1 if W is N-major
     float* colsum;   // ROW: optional per-32-row-block column sums of C
+    int c_peer;      // ROW: store origin rank r's rows through tmC_peer[r]
+    CUtensorMap tmC_peer[8];  // [El*cap_pad, N] slices in the origin ranks' buffers
 };
 
 // Instruction descriptor, kind::f16: bf16 A/B, fp32 D, M=128, N=256.
@@ -338,6 +340,11 @@ __global__ void __launch_bounds__(kThreads, 1) grouped_gemm_kernel(const __grid_
             tc_fence_after();
             const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16);
             const int32_t box_row = static_cast<int32_t>(crow - lane);  // this warp's 32 rows
+            // expert parallelism: origin rank r's rows go straight to its buffer
+            const int32_t slice_rows = p.El * p.cap_pad;
+            const int peer_r = (KIND == ROW && p.c_peer) ? box_row / slice_rows : -1;
+            const CUtensorMap* out_map = peer_r >= 0 ? &p.tmC_peer[peer_r] : &p.tmC;
+            const int32_t out_row = peer_r >= 0 ? box_row - peer_r * slice_rows : box_row;
 #pragma unroll 1
             for (int c = 0; c < BN; c += 64) {
                 float f[64];
@@ -401,8 +408,8 @@ __global__ void __launch_bounds__(kThreads, 1) grouped_gemm_kernel(const __grid_
                 if (lane == 0) {
                     asm volatile(
                         "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                            reinterpret_cast<uint64_t>(&p.tmC)),
-                        "r"(smem_u32(sbuf)), "r"(static_cast<int32_t>(ncol0 + c)), "r"(box_row)
+                            reinterpret_cast<uint64_t>(out_map)),
+                        "r"(smem_u32(sbuf)), "r"(static_cast<int32_t>(ncol0 + c)), "r"(out_row)
                         : "memory");
                     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 }
@@ -731,6 +738,10 @@ gemm2_kernel(const __grid_constant__ Params p) {
             const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16);
             const bool store = crow >= 0;
             const int32_t box_row = static_cast<int32_t>(crow - lane);
+            const int32_t slice_rows = p.El * p.cap_pad;
+            const int peer_r = (KIND == ROW && p.c_peer) ? box_row / slice_rows : -1;
+            const CUtensorMap* out_map = peer_r >= 0 ? &p.tmC_peer[peer_r] : &p.tmC;
+            const int32_t out_row = peer_r >= 0 ? box_row - peer_r * slice_rows : box_row;
 #pragma unroll 1
             for (int c = 0; c < BN; c += 64) {
                 float f[64];
@@ -793,8 +804,8 @@ gemm2_kernel(const __grid_constant__ Params p) {
                 if (lane == 0) {
                     asm volatile(
                         "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                            reinterpret_cast<uint64_t>(&p.tmC)),
-                        "r"(smem_u32(sbuf)), "r"(static_cast<int32_t>(ncol0 + c)), "r"(box_row)
+                            reinterpret_cast<uint64_t>(out_map)),
+                        "r"(smem_u32(sbuf)), "r"(static_cast<int32_t>(ncol0 + c)), "r"(out_row)
                         : "memory");
                     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 }
@@ -934,6 +945,13 @@ void launch_row_gemm_tc(const RowGemmArgs& a, cudaStream_t st) {
     p.epi = a.epi;
     p.b_mn = a.w_nmajor ? 1 : 0;
     p.colsum = a.epi == EPI_RELU_MASK ? a.colsum : nullptr;
+    p.c_peer = 0;
+    if (a.c_peer) {
+        if (a.ep > 8) throw Status(8, "row gemm: peer stores support at most 8 ranks");
+        for (int r = 0; r < a.ep; ++r)
+            p.tmC_peer[r] = tc::make_map(a.c_peer[r], static_cast<int64_t>(a.El) * a.cap_pad, a.N, 64, 32);
+        p.c_peer = 1;
+    }
     const int64_t max_tiles = rows / tc::BM * (a.N / tc::BN);
     const int ov = tc::pair_override();
     const bool use_pair = ov >= 0 ? ov == 1 : static_cast<int64_t>(a.ep) * a.cap_pad >= 2 * tc::BM;

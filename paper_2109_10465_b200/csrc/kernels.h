@@ -133,6 +133,11 @@ struct RowGemmArgs {
     // optional (tensor-core path, EPI_RELU_MASK): per-32-row-block column sums
     // of the stored C, [rows/32][N]; reduce with launch_colsum_parts
     float* colsum = nullptr;
+    // optional (tensor-core path, expert parallelism): store each origin rank
+    // r's rows straight into c_peer[r] (rank r's receive buffer slice for this
+    // rank, [El * cap_pad][N], NVLink-mapped), row (seg % El) * cap_pad + m,
+    // instead of C — the combine exchange's copy folded into the epilogue
+    void* const* c_peer = nullptr;
 };
 template <class T>
 void launch_row_gemm_simt(const RowGemmArgs& a, cudaStream_t st);

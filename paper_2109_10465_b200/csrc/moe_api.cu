@@ -157,6 +157,7 @@ struct moe_handle {
     void* peer[P_NBUF][8] = {};
     DevMem bar;       // 1-int NCCL all-reduce (barrier fallback, MOE_B200_EP_BARRIER=nccl)
     DevMem flags_ipc; // [8] u64 barrier flags, written by the peers over NVLink
+    bool no_peer_epi = std::getenv("MOE_B200_PEER_EPI") && std::getenv("MOE_B200_PEER_EPI")[0] == '0';
     DevMem dwg_x;     // [d*E] fp32 staging of this rank's dWg for the fixed-order sum over ranks
     unsigned long long epoch = 0;
     bool nccl_barrier = false;
@@ -261,6 +262,7 @@ struct XSpec {
     size_t esz;
 };
 
+void peer_barrier(moe_handle* h);
 void exchange(moe_handle* h, std::initializer_list<XSpec> specs, bool local_only = false) {
     if (!h->ipc) {
         NCCL_CHECK(ncclGroupStart());
@@ -291,6 +293,12 @@ void exchange(moe_handle* h, std::initializer_list<XSpec> specs, bool local_only
     }
     launch_peer_copy(jobs, h->stream);
     if (std::getenv("MOE_B200_PROFILE_BARRIER")) h->mark("xchg_copy");
+    peer_barrier(h);
+}
+
+// All ranks' stores into each other's receive buffers (peer copies or GEMM
+// epilogues storing over NVLink) complete before any rank reads its own.
+void peer_barrier(moe_handle* h) {
     if (h->nccl_barrier) {
         NCCL_CHECK(ncclAllReduce(h->bar.p, h->bar.p, 1, ncclInt32, ncclSum, h->comm, h->stream));
     } else {
@@ -342,7 +350,8 @@ void ipc_setup(moe_handle* h) {
 template <class TIO>
 bool row_gemm(moe_handle* h, const TIO* A, const TIO* W, TIO* C, const float* bias,
               const TIO* mask, const int32_t* counts, int64_t N, int64_t K, bool w_nmajor,
-              int epi, int nseg_ep, float* colsum = nullptr) {
+              int epi, int nseg_ep, float* colsum = nullptr, void* const* c_peer = nullptr,
+              bool* peered = nullptr) {
     RowGemmArgs a;
     a.A = A;
     a.W = W;
@@ -360,6 +369,8 @@ bool row_gemm(moe_handle* h, const TIO* A, const TIO* W, TIO* C, const float* bi
     a.colsum = colsum;
     if constexpr (std::is_same<TIO, __nv_bfloat16>::value) {
         if (tc_row_gemm_supported(a)) {
+            a.c_peer = c_peer;
+            if (peered) *peered = c_peer != nullptr;
             launch_row_gemm_tc(a, h->stream);
             return colsum != nullptr;
         }
@@ -523,11 +534,24 @@ void forward_impl(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, c
     row_gemm<TIO>(h, h->Xr.as<TIO>(), w1, h->H.as<TIO>(), b1, nullptr, counts, h->f, h->d, true,
                   EPI_BIAS_RELU, ep);
     h->mark("ffn1_fwd");
+    // under EP with NVLink-mapped buffers the fwd2 epilogue stores each origin
+    // rank's rows straight into that rank's O receive buffer (no copy pass)
+    void* opeer[8] = {};
+    const bool want_peer = ep > 1 && h->ipc && !h->no_peer_epi;
+    if (want_peer)
+        for (int r = 0; r < ep; ++r)
+            opeer[r] = static_cast<char*>(h->peer[moe_handle::P_O][r]) +
+                       static_cast<size_t>(h->rank) * El * h->cap_pad * h->d * h->esz;
+    bool peered = false;
     row_gemm<TIO>(h, h->H.as<TIO>(), w2, h->Or.as<TIO>(), b2, nullptr, counts, h->d, h->f, true,
-                  EPI_BIAS, ep);
+                  EPI_BIAS, ep, nullptr, want_peer ? opeer : nullptr, &peered);
     h->mark("ffn2_fwd");
     TIO* Oloc = h->Or.as<TIO>();
-    if (ep > 1) {
+    if (peered) {
+        peer_barrier(h);
+        Oloc = h->Oloc.as<TIO>();
+        h->mark("a2a_combine");
+    } else if (ep > 1) {
         exchange(h, {{h->Or.p, h->Oloc.p, moe_handle::P_O, static_cast<size_t>(El) * h->cap_pad * h->d,
                       nccl_type(h->esz), h->esz}});
         Oloc = h->Oloc.as<TIO>();
