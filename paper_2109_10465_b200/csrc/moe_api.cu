@@ -622,8 +622,17 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
                                          h->db1_part.as<float>());
     h->mark("ffn2_dgrad");
     if (db1_fused) launch_colsum_parts(h->db1_part.as<float>(), f, ep, El, h->cap_pad, counts, db1, st);
+    // under EP with NVLink-mapped buffers the dgrad1 epilogue returns dX rows
+    // straight into the origin ranks' dX buffers (no copy pass)
+    void* xpeer[8] = {};
+    const bool want_peer = ep > 1 && h->ipc && !h->no_peer_epi;
+    if (want_peer)
+        for (int r = 0; r < ep; ++r)
+            xpeer[r] = static_cast<char*>(h->peer[moe_handle::P_DX][r]) +
+                       static_cast<size_t>(h->rank) * El * h->cap_pad * d * h->esz;
+    bool dx_peered = false;
     row_gemm<TIO>(h, h->dH.as<TIO>(), w1, h->dXr.as<TIO>(), nullptr, nullptr, counts, d, f, false,
-                  EPI_NONE, ep);
+                  EPI_NONE, ep, nullptr, want_peer ? xpeer : nullptr, &dx_peered);
     h->mark("ffn1_dgrad");
     TIO* dXloc = h->dXr.as<TIO>();
     if (ep > 1) {  // return dX to its origin ranks while the weight gradients compute
@@ -631,8 +640,11 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
         MOE_CUDA_CHECK(cudaStreamWaitEvent(h->comm_stream, h->ev_c, 0));
         cudaStream_t saved = h->stream;
         h->stream = h->comm_stream;
-        exchange(h, {{h->dXr.p, h->dXloc.p, moe_handle::P_DX, static_cast<size_t>(El) * h->cap_pad * d,
-                      nccl_type(h->esz), h->esz}});
+        if (dx_peered)
+            peer_barrier(h);
+        else
+            exchange(h, {{h->dXr.p, h->dXloc.p, moe_handle::P_DX, static_cast<size_t>(El) * h->cap_pad * d,
+                          nccl_type(h->esz), h->esz}});
         h->stream = saved;
         MOE_CUDA_CHECK(cudaEventRecord(h->ev_comm, h->comm_stream));
         dXloc = h->dXloc.as<TIO>();
