@@ -445,6 +445,7 @@ router_bwd_kernel(int64_t T, int d, int E, int K, const TIO* __restrict__ dy,
         if (p < 0) continue;
         const int64_t row = (int64_t)choice[t * K + k] * cap_pad + p;
         float acc = 0.f;
+#pragma unroll 4
         for (int j = lane * V; j < d; j += 32 * V) {
             float a[V], b[V];
             load_f<TIO, V>(dy + t * d + j, a);
