@@ -593,22 +593,31 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
     const TIO* w2 = static_cast<const TIO*>(h->w2);
     const TIO* Oloc = ep > 1 ? h->Oloc.as<TIO>() : h->Or.as<TIO>();
     h->mark("begin");
-    // routing weights / balance loss / softmax backward -> dL
-    launch_router_bwd<TIO>(T, static_cast<int>(d), E, K, dy, Oloc, h->cap_pad,
-                           h->choice.as<int32_t>(), h->pos.as<int32_t>(),
-                           h->gate_prob.as<float>(), h->probs.as<float>(), h->fcoef.as<float>(),
-                           daux, h->dL.as<float>(), st);
-    h->mark("router_bwd");
     // combine backward: dO rows = w * dy[t]
     TIO* dOloc = static_cast<TIO*>(h->loc(h->dOr, h->dOloc));
     launch_combine_bwd_gather<TIO>(dy, d, E, K, h->cap_pad, h->row_src.as<int32_t>(),
                                    h->kept.as<int32_t>(), h->wts.as<float>(), dOloc, st);
     h->mark("combine_bwd");
     const int32_t* counts = h->kept.as<int32_t>();
-    if (ep > 1) {
+    if (ep > 1) {  // dO to the expert owners on the comm stream, next to the router backward
+        MOE_CUDA_CHECK(cudaEventRecord(h->ev_c, st));
+        MOE_CUDA_CHECK(cudaStreamWaitEvent(h->comm_stream, h->ev_c, 0));
+        cudaStream_t saved = h->stream;
+        h->stream = h->comm_stream;
         exchange(h, {{dOloc, h->dOr.p, moe_handle::P_DO, static_cast<size_t>(El) * h->cap_pad * d,
                       nccl_type(h->esz), h->esz}});
+        h->stream = saved;
+        MOE_CUDA_CHECK(cudaEventRecord(h->ev_comm, h->comm_stream));
         counts = h->counts_r.as<int32_t>();
+    }
+    // routing weights / balance loss / softmax backward -> dL
+    launch_router_bwd<TIO>(T, static_cast<int>(d), E, K, dy, Oloc, h->cap_pad,
+                           h->choice.as<int32_t>(), h->pos.as<int32_t>(),
+                           h->gate_prob.as<float>(), h->probs.as<float>(), h->fcoef.as<float>(),
+                           daux, h->dL.as<float>(), st);
+    h->mark("router_bwd");
+    if (ep > 1) {
+        MOE_CUDA_CHECK(cudaStreamWaitEvent(st, h->ev_comm, 0));
         h->mark("a2a_dO");
     }
     const float* noise = h->jitter_on ? h->noise.as<float>() : nullptr;
