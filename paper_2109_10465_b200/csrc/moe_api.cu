@@ -161,6 +161,7 @@ struct moe_handle {
     DevMem dwg_x;     // [d*E] fp32 staging of this rank's dWg for the fixed-order sum over ranks
     unsigned long long epoch = 0;
     bool nccl_barrier = false;
+    bool defer_balance = false;  // forward under EP: the balance loss runs next to the dispatch exchange
     ~moe_handle() {
         for (int b = 0; b < P_NBUF; ++b)
             for (int r = 0; r < 8; ++r)
@@ -411,6 +412,7 @@ bool use_gate_tc(const moe_handle* h) {
 // ---------------------------------------------------------------------------
 // router: gate -> softmax/top-k -> balance loss -> assignment
 // ---------------------------------------------------------------------------
+void balance_finalize(moe_handle* h, int64_t T, float* aux);
 template <class TIO>
 void route(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, int phase, uint64_t seed,
            float* aux) {
@@ -458,13 +460,18 @@ void route(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, int phas
                         h->colsum_part.as<float>(), h->count_part.as<int32_t>(),
                         h->flags.as<uint32_t>(), st);
     h->mark("softmax_topk");
+    if (!h->defer_balance) balance_finalize(h, T, aux);
+    h->jitter_on = jitter;
+}
+
+// aux loss and the per-expert gradient coefficients (routing.cpp:348-374)
+void balance_finalize(moe_handle* h, int64_t T, float* aux) {
     launch_balance_finalize(h->colsum_part.as<float>(), h->count_part.as<int32_t>(),
-                            softmax_parts(T), T, E, h->cfg.balance_coeff,
+                            softmax_parts(T), T, h->E, h->cfg.balance_coeff,
                             aux ? aux : h->aux_scratch.as<float>(), h->fcoef.as<float>(),
                             h->fcount.as<int32_t>(), h->bal_term.as<double>(),
-                            h->bal_done.as<unsigned>(), st);
+                            h->bal_done.as<unsigned>(), h->stream);
     h->mark("balance_loss");
-    h->jitter_on = jitter;
 }
 
 void assign(moe_handle* h, int64_t T, const int32_t* choice, int cap, int mode, uint64_t aseed,
@@ -508,11 +515,13 @@ void forward_impl(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, c
     set_geometry(h, T, phase, mode);
     h->fwd_valid = false;
     h->mark("begin");
+    h->defer_balance = ep > 1;
     route<TIO>(h, T, x, gate_w, phase, seed, aux);
+    h->defer_balance = false;
     assign(h, T, h->choice.as<int32_t>(), h->cap, mode, derive_seed_tag(seed, "assign"),
            h->slot.as<int32_t>());
     h->mark("assign");
-    launch_combine_weights(T, E, K, h->gate_prob.as<float>(), h->wts.as<float>(), st);
+    if (ep == 1) launch_combine_weights(T, E, K, h->gate_prob.as<float>(), h->wts.as<float>(), st);
     // dispatch (routing.cpp:396): un-jittered x into [E, cap_pad, d]
     TIO* Xloc = static_cast<TIO*>(h->loc(h->Xr, h->Xloc));
     launch_dispatch_gather<TIO>(x, h->d, E, K, h->cap_pad, h->row_src.as<int32_t>(),
@@ -520,10 +529,20 @@ void forward_impl(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, c
     h->mark("dispatch");
     const int32_t* counts = h->kept.as<int32_t>();
     if (ep > 1) {
-        // forward all-to-all: counts then rows (fixed-shape [E_local, cap_pad, d] slices)
+        // forward all-to-all: counts then rows (fixed-shape [E_local, cap_pad, d] slices), on
+        // the comm stream while the balance loss and the combine weights compute
+        MOE_CUDA_CHECK(cudaEventRecord(h->ev_c, st));
+        MOE_CUDA_CHECK(cudaStreamWaitEvent(h->comm_stream, h->ev_c, 0));
+        cudaStream_t saved = h->stream;
+        h->stream = h->comm_stream;
         exchange(h, {{h->kept.p, h->counts_r.p, moe_handle::P_CNT, static_cast<size_t>(El), ncclInt32, 4},
                      {Xloc, h->Xr.p, moe_handle::P_X, static_cast<size_t>(El) * h->cap_pad * h->d,
                       nccl_type(h->esz), h->esz}});
+        h->stream = saved;
+        MOE_CUDA_CHECK(cudaEventRecord(h->ev_comm, h->comm_stream));
+        balance_finalize(h, T, aux);
+        launch_combine_weights(T, E, K, h->gate_prob.as<float>(), h->wts.as<float>(), st);
+        MOE_CUDA_CHECK(cudaStreamWaitEvent(st, h->ev_comm, 0));
         counts = h->counts_r.as<int32_t>();
         const double slice = static_cast<double>(El) * h->cap * h->d;
         h->last_logical_traffic = 2.0 * slice * 8.0 * (ep - 1);
