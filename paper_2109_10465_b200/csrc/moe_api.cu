@@ -419,6 +419,13 @@ void route(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, int phas
     const int E = h->E, K = h->K;
     cudaStream_t st = h->stream;
     const bool jitter = phase == MOE_TRAIN && h->cfg.jitter_eps > 0.0;
+    const bool gtc = use_gate_tc<TIO>(h);
+    if (gtc) {  // Wg^T for the logits' B operand, on the side stream next to the jitter generator
+        MOE_CUDA_CHECK(cudaEventRecord(h->ev_a, st));
+        MOE_CUDA_CHECK(cudaStreamWaitEvent(h->side, h->ev_a, 0));
+        launch_gate2_transpose(gate_w, h->wgt.as<float>(), static_cast<int>(h->d), E, h->side);
+        MOE_CUDA_CHECK(cudaEventRecord(h->ev_b, h->side));
+    }
     if (jitter) {
         // routing.cpp:62-70: noise stream Rng(derive_seed(seed, "jitter")), row-major
         // generated on the device by jump-ahead (rng.cu)
@@ -435,10 +442,10 @@ void route(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, int phas
     }
     // logits = (x * noise) @ gate_w  (routing.cpp:71)
     int nsplit = 1;
-    if (use_gate_tc<TIO>(h)) {
+    if (gtc) {
         if constexpr (std::is_same<TIO, __nv_bfloat16>::value) {
             nsplit = gate_tc_logit_splits(T, static_cast<int>(h->d));
-            launch_gate2_transpose(gate_w, h->wgt.as<float>(), static_cast<int>(h->d), E, st);
+            MOE_CUDA_CHECK(cudaStreamWaitEvent(st, h->ev_b, 0));
             launch_gate_tc_logits<TIO>(x, jitter ? h->noise.as<float>() : nullptr, h->wgt.as<float>(),
                                        h->logits.as<float>(), T, static_cast<int>(h->d), E, nsplit, st);
         }
