@@ -249,6 +249,21 @@ __device__ __forceinline__ uint64_t mix(uint64_t lo_word, uint64_t hi_word) {
     const uint64_t y = (lo_word & UM) | (hi_word & LM);
     return (y >> 1) ^ ((y & 1ULL) ? A : 0ULL);
 }
+// twist3(lo, hi, mid) = mix(lo, hi) ^ mid on 32-bit halves: y's high half is
+// lo's, the low half merges lo's top bit with hi's low 31; one funnel shift,
+// and the conditional A is a 32-bit sign-spread mask shared by both halves
+// (9 ALU operations instead of the 64-bit form's ~12).
+__device__ __forceinline__ uint64_t twist3(uint64_t lo_word, uint64_t hi_word, uint64_t mid) {
+    const uint32_t lo_l = static_cast<uint32_t>(lo_word), lo_h = static_cast<uint32_t>(lo_word >> 32);
+    const uint32_t hi_l = static_cast<uint32_t>(hi_word);
+    const uint32_t y_l = (lo_l & 0x80000000u) | (hi_l & 0x7fffffffu);
+    const uint32_t r_l = __funnelshift_r(y_l, lo_h, 1);
+    const uint32_t r_h = lo_h >> 1;
+    const uint32_t m = static_cast<uint32_t>(static_cast<int32_t>(hi_l << 31) >> 31);
+    const uint32_t o_l = (r_l ^ static_cast<uint32_t>(mid)) ^ (static_cast<uint32_t>(A) & m);
+    const uint32_t o_h = (r_h ^ static_cast<uint32_t>(mid >> 32)) ^ (static_cast<uint32_t>(A >> 32) & m);
+    return (static_cast<uint64_t>(o_h) << 32) | o_l;
+}
 
 // One warp advances the 312-word state by one block, in registers.  Lane l
 // holds the word pairs j = 5l + r and j + 156 (r < 5): A[r] = o[j],
@@ -276,19 +291,19 @@ struct WarpTwister {
     }
     __device__ __forceinline__ void twist(int lane) {
         uint64_t nA[5];
-        nA[0] = mix(A[0], lane == 31 ? o156 : A[1]) ^ B[0];  // j = 155 on lane 31
-        nA[1] = mix(A[1], A[2]) ^ B[1];
-        const uint64_t new0 = mix(o0, o1) ^ o156;
-        const uint64_t nB0 = mix(B[0], lane == 31 ? new0 : B[1]) ^ nA[0];  // j = 311 on lane 31
+        nA[0] = twist3(A[0], lane == 31 ? o156 : A[1], B[0]);  // j = 155 on lane 31
+        nA[1] = twist3(A[1], A[2], B[1]);
+        const uint64_t new0 = twist3(o0, o1, o156);
+        const uint64_t nB0 = twist3(B[0], lane == 31 ? new0 : B[1], nA[0]);  // j = 311 on lane 31
         const uint64_t an = shfl_down1(static_cast<uint32_t>(nA[0]));
         const uint64_t bn = shfl_down1(static_cast<uint32_t>(nB0));
         const uint64_t p156 = join(shfl_idx0(static_cast<uint32_t>(nB0)), shfl_idx0(static_cast<uint32_t>(nB0 >> 32)));
         const uint64_t p0 = join(shfl_idx0(static_cast<uint32_t>(nA[0])), shfl_idx0(static_cast<uint32_t>(nA[0] >> 32)));
         const uint64_t p1 = shfl_idx0(static_cast<uint32_t>(nA[1]));
 #pragma unroll
-        for (int r = 2; r < 5; ++r) nA[r] = mix(A[r], r < 4 ? A[r + 1] : a_next) ^ B[r];
+        for (int r = 2; r < 5; ++r) nA[r] = twist3(A[r], r < 4 ? A[r + 1] : a_next, B[r]);
 #pragma unroll
-        for (int r = 1; r < 5; ++r) B[r] = mix(B[r], r < 4 ? B[r + 1] : b_next) ^ nA[r];
+        for (int r = 1; r < 5; ++r) B[r] = twist3(B[r], r < 4 ? B[r + 1] : b_next, nA[r]);
         B[0] = nB0;
 #pragma unroll
         for (int r = 0; r < 5; ++r) A[r] = nA[r];
