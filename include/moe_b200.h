@@ -90,6 +90,7 @@ typedef struct moe_handle moe_handle;
 #define MOE_FLAG_NONFINITE 0x1u
 #define MOE_FLAG_PROB_ROWS 0x2u /* balance_loss: probs rows must sum to 1 */
 #define MOE_FLAG_CHOICE_RANGE 0x4u
+#define MOE_FLAG_UNIFORM_SHAPE 0x8u /* expert parallelism: ranks passed different T */
 
 void moe_router_cfg_default(moe_router_cfg* cfg);                    /* routing.hpp:17-27 */
 moe_status moe_router_cfg_validate(const moe_router_cfg* cfg);       /* routing.cpp:13-23 */
@@ -125,6 +126,14 @@ moe_status moe_forward(moe_handle* h, int64_t T, const void* x, const float* gat
  * to the forward (else ignored; its gradient then flows into dx). */
 moe_status moe_backward(moe_handle* h, const void* dy, float daux, void* dx, float* dgate_w,
                         void* dw1, float* db1, void* dw2, float* db2, void* dresidual);
+
+/* Which kernel family runs this handle's expert GEMMs.  bf16 layers use the
+ * tcgen05/TMEM kernels when d_model and d_ff are multiples of 256, else the
+ * fp32-accumulating SIMT kernels (logged to stderr at moe_create unless
+ * MOE_B200_QUIET=1; MOE_B200_REQUIRE_TC=1 makes moe_create fail with
+ * MOE_UNSUPPORTED instead).  fp32 layers always use SIMT (the parity path). */
+typedef enum { MOE_GEMM_SIMT = 0, MOE_GEMM_TCGEN05 = 1 } moe_gemm_kind;
+moe_status moe_gemm_path(const moe_handle* h, int* path_out);
 
 /* Capacity and kept/dropped statistics of the last forward (host copy;
  * synchronises).  kept_per_expert may be NULL, else [E] int64. */
@@ -205,6 +214,24 @@ moe_status moe_ep_get_unique_id(void* id_out);
  * are those E/ep experts.  Each rank gates its own tokens; moe_forward's
  * seed is the rank's seed (derive_seed(seed, r), parallel.cpp:272). */
 moe_status moe_ep_init(moe_handle* h, const void* unique_id);
+/* NCCL-free bootstrap of the NVLink peer map (ranks on one node; ranks may
+ * share a GPU, which NCCL refuses).  Each rank writes its blob
+ * (moe_ep_blob_size() bytes: its layer dims and the CUDA-IPC handles of its
+ * receive buffers) with moe_ep_export, the caller all-gathers the blobs in
+ * rank order by any means (MPI, torch.distributed gloo, a file), every rank
+ * passes the gathered array to moe_ep_import, and the caller then runs one
+ * barrier before the first forward.  Exchanges are then NVLink / peer-memory
+ * stores closed by the device flag barrier; dgate_w is summed over ranks from
+ * peer-mapped staging.  Ranks that built different layers fail with
+ * MOE_CONFIG; different max_tokens with MOE_UNIFORM_SHAPE.  Needs ep <= 8
+ * and E/ep % 4 == 0 (else MOE_UNSUPPORTED: use moe_ep_init). */
+size_t moe_ep_blob_size(void);
+moe_status moe_ep_export(moe_handle* h, void* blob_out);
+moe_status moe_ep_import(moe_handle* h, const void* all_blobs);
+/* Per-forward shape contract (parallel.cpp:245-253): every rank must pass
+ * the same T to moe_forward.  The dispatch exchange compares the ranks' T on
+ * the device; a mismatch latches MOE_FLAG_UNIFORM_SHAPE (no expert rows are
+ * computed) and the next moe_check returns MOE_UNIFORM_SHAPE. */
 /* Fixed-shape A2A accounting of the last forward (A2ATrafficLog,
  * parallel.hpp:83-91): bytes [ep, ep] in the reference's f64 units, and the
  * bytes actually moved by this rank. */

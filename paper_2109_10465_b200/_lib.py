@@ -72,6 +72,10 @@ _SIGS = {
     "moe_ep_get_unique_id": (C.c_int, [VP]),
     "moe_ep_init": (C.c_int, [H, VP]),
     "moe_ep_traffic": (C.c_int, [H, VP, C.POINTER(C.c_double)]),
+    "moe_ep_blob_size": (C.c_size_t, []),
+    "moe_gemm_path": (C.c_int, [H, C.POINTER(C.c_int)]),
+    "moe_ep_export": (C.c_int, [H, VP]),
+    "moe_ep_import": (C.c_int, [H, VP]),
     "moe_profile_enable": (C.c_int, [H, C.c_int]),
     "moe_profile_read": (C.c_int, [H, C.c_int, C.c_char_p, C.POINTER(C.c_double),
                                    C.POINTER(C.c_int64), C.POINTER(C.c_int)]),

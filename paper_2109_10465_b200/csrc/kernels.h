@@ -11,6 +11,7 @@ namespace moe {
 constexpr uint32_t MOE_FLAG_NONFINITE_DEV = 0x1u;
 constexpr uint32_t MOE_FLAG_PROB_ROWS_DEV = 0x2u;
 constexpr uint32_t MOE_FLAG_CHOICE_RANGE_DEV = 0x4u;
+constexpr uint32_t MOE_FLAG_UNIFORM_SHAPE_DEV = 0x8u;
 // fp32 probabilities: |sum_e P - 1| bound used in place of the reference's
 // f64 1e-9 (routing.cpp:360-361).
 constexpr float kProbRowTol = 1e-4f;
@@ -195,8 +196,18 @@ void launch_peer_copy(const PeerCopyJobs& jobs, cudaStream_t st);
 struct PeerFlags {
     unsigned long long* f[8];  // each rank's flag array, mapped into this process
 };
+// Per-rank token-count agreement carried by an exchange barrier (tokens < 0:
+// no check).  On mismatch: flags |= MOE_FLAG_UNIFORM_SHAPE, counts[0..n) = 0.
+struct ShapeCheck {
+    long long tokens;
+    uint32_t* flags;
+    int32_t* counts;
+    int ncounts;
+};
 void launch_ipc_barrier(const PeerFlags& peers, const unsigned long long* mine, int rank, int ep,
-                        unsigned long long epoch, cudaStream_t st);
+                        unsigned long long epoch, cudaStream_t st, const ShapeCheck* sc = nullptr);
+void launch_fill_i64(long long* p, long long v, cudaStream_t st);
+void launch_ep_shape_check(const long long* all_t, int ep, const ShapeCheck& sc, cudaStream_t st);
 // out = sum over ranks of src[r] (fixed rank order), n % 4 == 0
 void launch_sum_ranks(const float* const* srcs, int ep, int64_t n, float* out, cudaStream_t st);
 

@@ -11,6 +11,7 @@
 #include <atomic>
 #include <cmath>
 #include <map>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -158,10 +159,12 @@ struct moe_handle {
     DevMem bar;       // 1-int NCCL all-reduce (barrier fallback, MOE_B200_EP_BARRIER=nccl)
     DevMem flags_ipc; // [8] u64 barrier flags, written by the peers over NVLink
     bool no_peer_epi = std::getenv("MOE_B200_PEER_EPI") && std::getenv("MOE_B200_PEER_EPI")[0] == '0';
+    DevMem shape_all; // [ep + 1] i64: all-gathered per-rank token counts (NCCL transport)
     DevMem dwg_x;     // [d*E] fp32 staging of this rank's dWg for the fixed-order sum over ranks
     unsigned long long epoch = 0;
     bool nccl_barrier = false;
-    bool defer_balance = false;  // forward under EP: the balance loss runs next to the dispatch exchange
+    bool defer_balance = false;
+    bool gemm_tc = false;        // bf16 expert GEMMs on tcgen05 (decided at create)  // forward under EP: the balance loss runs next to the dispatch exchange
     ~moe_handle() {
         for (int b = 0; b < P_NBUF; ++b)
             for (int r = 0; r < 8; ++r)
@@ -263,12 +266,21 @@ struct XSpec {
     size_t esz;
 };
 
-void peer_barrier(moe_handle* h);
-void exchange(moe_handle* h, std::initializer_list<XSpec> specs, bool local_only = false) {
+void peer_barrier(moe_handle* h, const ShapeCheck* sc = nullptr);
+// sc: also verify that every rank passed the same token count (the dispatch
+// exchange; parallel.cpp:245-253), see ShapeCheck in kernels.h.
+void exchange(moe_handle* h, std::initializer_list<XSpec> specs, bool local_only = false,
+              const ShapeCheck* sc = nullptr) {
     if (!h->ipc) {
         NCCL_CHECK(ncclGroupStart());
         for (const XSpec& x : specs) all_to_all(h, x.send, x.recv, x.chunk_elems, x.ty, x.esz);
         NCCL_CHECK(ncclGroupEnd());
+        if (sc) {
+            long long* all = h->shape_all.as<long long>();
+            launch_fill_i64(all + h->ep, sc->tokens, h->stream);
+            NCCL_CHECK(ncclAllGather(all + h->ep, all, 1, ncclInt64, h->comm, h->stream));
+            launch_ep_shape_check(all, h->ep, *sc, h->stream);
+        }
         return;
     }
     PeerCopyJobs jobs{};
@@ -294,57 +306,105 @@ void exchange(moe_handle* h, std::initializer_list<XSpec> specs, bool local_only
     }
     launch_peer_copy(jobs, h->stream);
     if (std::getenv("MOE_B200_PROFILE_BARRIER")) h->mark("xchg_copy");
-    peer_barrier(h);
+    peer_barrier(h, sc);
 }
 
 // All ranks' stores into each other's receive buffers (peer copies or GEMM
 // epilogues storing over NVLink) complete before any rank reads its own.
-void peer_barrier(moe_handle* h) {
+void peer_barrier(moe_handle* h, const ShapeCheck* sc) {
     if (h->nccl_barrier) {
         NCCL_CHECK(ncclAllReduce(h->bar.p, h->bar.p, 1, ncclInt32, ncclSum, h->comm, h->stream));
+        if (sc) {
+            long long* all = h->shape_all.as<long long>();
+            launch_fill_i64(all + h->ep, sc->tokens, h->stream);
+            NCCL_CHECK(ncclAllGather(all + h->ep, all, 1, ncclInt64, h->comm, h->stream));
+            launch_ep_shape_check(all, h->ep, *sc, h->stream);
+        }
     } else {
         PeerFlags pf{};
         for (int r = 0; r < h->ep; ++r) pf.f[r] = static_cast<unsigned long long*>(h->peer[moe_handle::P_FLAG][r]);
-        launch_ipc_barrier(pf, h->flags_ipc.as<unsigned long long>(), h->rank, h->ep, ++h->epoch, h->stream);
+        launch_ipc_barrier(pf, h->flags_ipc.as<unsigned long long>(), h->rank, h->ep, ++h->epoch, h->stream, sc);
     }
 }
 
-void ipc_setup(moe_handle* h) {
-    // export the receive buffers, all-gather the handles over NCCL, open peers'
-    h->flags_ipc.alloc(8 * 16);
+// Bootstrap blob of one rank for the NVLink peer map: its dims (checked for
+// agreement) and the CUDA-IPC handles of its receive buffers.
+struct EpBlob {
+    int64_t max_tokens, d, f;
+    int32_t E, K, dtype, ep, rank, pad;
+    cudaIpcMemHandle_t mem[moe_handle::P_NBUF];
+};
+
+// Export: allocate the flag / dWg staging buffers, zero the flags (before any
+// peer can see them) and describe this rank's receive buffers.
+void ipc_export(moe_handle* h, EpBlob* out) {
+    if (!h->flags_ipc.p) {
+        h->flags_ipc.alloc(8 * 16);
+        h->dwg_x.alloc(4 * static_cast<size_t>(h->d) * h->E);
+    }
     MOE_CUDA_CHECK(cudaMemset(h->flags_ipc.p, 0, 8 * 16));
-    h->dwg_x.alloc(4 * static_cast<size_t>(h->d) * h->E);
+    h->epoch = 0;
     void* bufs[moe_handle::P_NBUF] = {h->Xr.p,          h->Oloc.p,      h->dOr.p,    h->dXloc.p,
                                       h->counts_r.p,    h->flags_ipc.p, h->dwg_x.p};
-    const size_t hs = sizeof(cudaIpcMemHandle_t);
-    std::vector<cudaIpcMemHandle_t> mine(moe_handle::P_NBUF), all(moe_handle::P_NBUF * h->ep);
-    for (int b = 0; b < moe_handle::P_NBUF; ++b) MOE_CUDA_CHECK(cudaIpcGetMemHandle(&mine[b], bufs[b]));
-    DevMem dev;
-    dev.alloc(hs * moe_handle::P_NBUF * h->ep);
-    char* base = static_cast<char*>(dev.p);
-    MOE_CUDA_CHECK(cudaMemcpy(base + h->rank * hs * moe_handle::P_NBUF, mine.data(),
-                              hs * moe_handle::P_NBUF, cudaMemcpyHostToDevice));
-    NCCL_CHECK(ncclAllGather(base + h->rank * hs * moe_handle::P_NBUF, base, hs * moe_handle::P_NBUF,
-                             ncclUint8, h->comm, h->stream));
-    MOE_CUDA_CHECK(cudaStreamSynchronize(h->stream));
-    MOE_CUDA_CHECK(cudaMemcpy(all.data(), base, hs * moe_handle::P_NBUF * h->ep, cudaMemcpyDeviceToHost));
+    std::memset(out, 0, sizeof(EpBlob));
+    out->max_tokens = h->Tmax;
+    out->d = h->d;
+    out->f = h->f;
+    out->E = h->E;
+    out->K = h->K;
+    out->dtype = h->esz == 2 ? MOE_BF16 : MOE_F32;
+    out->ep = h->ep;
+    out->rank = h->rank;
+    for (int b = 0; b < moe_handle::P_NBUF; ++b) MOE_CUDA_CHECK(cudaIpcGetMemHandle(&out->mem[b], bufs[b]));
+    MOE_CUDA_CHECK(cudaDeviceSynchronize());
+}
+
+// Import: check that every rank built the same layer, then open the peers'
+// receive buffers (rank order).  Ranks may share a device.
+void ipc_import(moe_handle* h, const EpBlob* all) {
+    for (int r = 0; r < h->ep; ++r) {
+        const EpBlob& b = all[r];
+        require(b.ep == h->ep && b.rank == r, MOE_CONFIG, "moe_ep_import: blobs must be all ranks in rank order");
+        require(b.E == h->E && b.K == h->K && b.d == h->d && b.f == h->f && b.dtype == all[h->rank].dtype,
+                MOE_CONFIG, "moe_ep_import: ranks built different layers");
+        // parallel.cpp:245-253: the fixed-shape exchange needs the same token geometry everywhere
+        require(b.max_tokens == h->Tmax, MOE_UNIFORM_SHAPE,
+                "simulate: per-rank token counts must be identical (All-to-All requires the same "
+                "tensor shape on every rank)");
+    }
+    void* bufs[moe_handle::P_NBUF] = {h->Xr.p,          h->Oloc.p,      h->dOr.p,    h->dXloc.p,
+                                      h->counts_r.p,    h->flags_ipc.p, h->dwg_x.p};
     for (int r = 0; r < h->ep; ++r)
         for (int b = 0; b < moe_handle::P_NBUF; ++b) {
             if (r == h->rank) {
                 h->peer[b][r] = bufs[b];
                 continue;
             }
-            MOE_CUDA_CHECK(cudaIpcOpenMemHandle(&h->peer[b][r], all[r * moe_handle::P_NBUF + b],
+            MOE_CUDA_CHECK(cudaIpcOpenMemHandle(&h->peer[b][r], all[r].mem[b],
                                                 cudaIpcMemLazyEnablePeerAccess));
         }
-    h->bar.alloc(16);
-    MOE_CUDA_CHECK(cudaMemset(h->bar.p, 0, 16));
+    h->ipc = true;
+}
+
+void ipc_setup(moe_handle* h) {
+    // export the receive buffers, all-gather the blobs over NCCL, open peers'
+    std::vector<EpBlob> all(static_cast<size_t>(h->ep));
+    EpBlob mine;
+    ipc_export(h, &mine);
+    DevMem dev;
+    dev.alloc(sizeof(EpBlob) * h->ep);
+    char* base = static_cast<char*>(dev.p);
+    MOE_CUDA_CHECK(cudaMemcpy(base + h->rank * sizeof(EpBlob), &mine, sizeof(EpBlob), cudaMemcpyHostToDevice));
+    NCCL_CHECK(ncclAllGather(base + h->rank * sizeof(EpBlob), base, sizeof(EpBlob), ncclUint8, h->comm,
+                             h->stream));
+    MOE_CUDA_CHECK(cudaStreamSynchronize(h->stream));
+    MOE_CUDA_CHECK(cudaMemcpy(all.data(), base, sizeof(EpBlob) * h->ep, cudaMemcpyDeviceToHost));
+    ipc_import(h, all.data());
     const char* bt = std::getenv("MOE_B200_EP_BARRIER");
     h->nccl_barrier = bt && std::string(bt) == "nccl";
     MOE_CUDA_CHECK(cudaDeviceSynchronize());  // flags zeroed everywhere before first use
     NCCL_CHECK(ncclAllReduce(h->bar.p, h->bar.p, 1, ncclInt32, ncclSum, h->comm, h->stream));
     MOE_CUDA_CHECK(cudaStreamSynchronize(h->stream));
-    h->ipc = true;
 }
 
 // Returns true iff the GEMM also produced the per-block column sums `colsum`.
@@ -542,9 +602,12 @@ void forward_impl(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, c
         MOE_CUDA_CHECK(cudaStreamWaitEvent(h->comm_stream, h->ev_c, 0));
         cudaStream_t saved = h->stream;
         h->stream = h->comm_stream;
+        // the exchange also checks that every rank passed the same T (else
+        // MOE_FLAG_UNIFORM_SHAPE and zero received counts)
+        const ShapeCheck sc{static_cast<long long>(T), h->flags.as<uint32_t>(), h->counts_r.as<int32_t>(), E};
         exchange(h, {{h->kept.p, h->counts_r.p, moe_handle::P_CNT, static_cast<size_t>(El), ncclInt32, 4},
                      {Xloc, h->Xr.p, moe_handle::P_X, static_cast<size_t>(El) * h->cap_pad * h->d,
-                      nccl_type(h->esz), h->esz}});
+                      nccl_type(h->esz), h->esz}}, false, &sc);
         h->stream = saved;
         MOE_CUDA_CHECK(cudaEventRecord(h->ev_comm, h->comm_stream));
         balance_finalize(h, T, aux);
@@ -837,6 +900,9 @@ void alloc_workspace(moe_handle* h) {
     h->dXr.alloc(es * R * d);
     if (es == 2) h->db1_part.alloc(4 * static_cast<size_t>(R / 32 + 1) * f);
     if (h->ep > 1) {
+        h->bar.alloc(16);
+        MOE_CUDA_CHECK(cudaMemset(h->bar.p, 0, 16));
+        h->shape_all.alloc(8 * (static_cast<size_t>(h->ep) + 1));
         h->Xloc.alloc(es * R * d);
         h->Oloc.alloc(es * R * d);
         h->dOloc.alloc(es * R * d);
@@ -933,6 +999,45 @@ moe_status moe_create(const moe_router_cfg* cfg, const moe_layer_dims* dims, moe
         h->f = dims->d_ff;
         h->esz = dims->dtype == MOE_BF16 ? 2 : 4;
         alloc_workspace(h.get());
+        if (h->esz == 2) {
+            // The bf16 path's expert GEMMs run on tcgen05 when the shape tiles
+            // (d, f multiples of 256); otherwise they run on the fp32-accumulating
+            // SIMT kernels, ~20x slower.  That choice is explicit: logged once
+            // here, reported by moe_gemm_path, and an error under MOE_B200_REQUIRE_TC=1.
+            RowGemmArgs ra{};
+            ra.N = h->f;
+            ra.K = h->d;
+            ra.ep = h->ep;
+            ra.El = h->El;
+            ra.cap_pad = kRowAlign;
+            RowGemmArgs rb = ra;
+            rb.N = h->d;
+            rb.K = h->f;
+            WgradGemmArgs wa{};
+            wa.M = h->f;
+            wa.N = h->d;
+            wa.ep = h->ep;
+            wa.El = h->El;
+            wa.cap_pad = kRowAlign;
+            WgradGemmArgs wb = wa;
+            wb.M = h->d;
+            wb.N = h->f;
+            h->gemm_tc = tc_row_gemm_supported(ra) && tc_row_gemm_supported(rb) &&
+                         tc_wgrad_gemm_supported(wa) && tc_wgrad_gemm_supported(wb);
+            if (!h->gemm_tc) {
+                const char* req = std::getenv("MOE_B200_REQUIRE_TC");
+                if (req && req[0] == '1')
+                    throw Status(MOE_UNSUPPORTED,
+                                 "moe_create: bf16 expert GEMMs need d_model and d_ff multiples of 256 "
+                                 "for tcgen05 (MOE_B200_REQUIRE_TC=1)");
+                const char* q = std::getenv("MOE_B200_QUIET");
+                if (!(q && q[0] == '1'))
+                    std::fprintf(stderr,
+                                 "[moe_b200] bf16 layer d_model=%lld d_ff=%lld: expert GEMMs use the SIMT "
+                                 "kernels (tcgen05 tiles need multiples of 256)\n",
+                                 static_cast<long long>(h->d), static_cast<long long>(h->f));
+            }
+        }
         MOE_CUDA_CHECK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
         MOE_CUDA_CHECK(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
         for (cudaEvent_t* e : {&h->ev_a, &h->ev_b, &h->ev_c, &h->ev_side, &h->ev_comm, &h->ev_pf})
@@ -1011,6 +1116,11 @@ moe_status moe_check(moe_handle* h, uint32_t* flags_out) {
     if (fl & MOE_FLAG_CHOICE_RANGE) {
         h->err = "assignment: choice out of expert range";
         return MOE_CONFIG;
+    }
+    if (fl & MOE_FLAG_UNIFORM_SHAPE) {  // parallel.cpp:245-253
+        h->err = "simulate: per-rank token counts must be identical (All-to-All requires the same "
+                 "tensor shape on every rank)";
+        return MOE_UNIFORM_SHAPE;
     }
     if (fl & MOE_FLAG_PROB_ROWS) {
         h->err = "balance_loss: probs rows must sum to 1";
@@ -1127,6 +1237,7 @@ moe_status moe_gate(moe_handle* h, int64_t T, const void* x, const float* gate_w
     if (!h) return MOE_SHAPE;
     return guarded(h, [&] {
         require(T >= 1 && T <= h->Tmax, MOE_SHAPE, "gate_forward: x [T,d] and gate_w [d,E] required");
+        h->fwd_valid = false;  // the per-stage gate reuses the forward's noise / logits scratch
         cudaStream_t st = h->stream;
         const int E = h->E, K = h->K;
         const bool jitter = phase == MOE_TRAIN && h->cfg.jitter_eps > 0.0;
@@ -1252,6 +1363,35 @@ moe_status moe_ep_init(moe_handle* h, const void* unique_id) {
         const char* tr = std::getenv("MOE_B200_EP_TRANSPORT");
         const bool want_ipc = !(tr && std::string(tr) == "nccl");
         if (want_ipc && h->ep <= 8 && (h->El * 4) % 16 == 0) ipc_setup(h);
+    });
+}
+
+moe_status moe_gemm_path(const moe_handle* h, int* path_out) {
+    if (!h || !path_out) return MOE_SHAPE;
+    *path_out = h->esz == 2 && h->gemm_tc && tc_enabled() ? MOE_GEMM_TCGEN05 : MOE_GEMM_SIMT;
+    return MOE_OK;
+}
+
+size_t moe_ep_blob_size(void) { return sizeof(EpBlob); }
+
+moe_status moe_ep_export(moe_handle* h, void* blob_out) {
+    if (!h) return MOE_SHAPE;
+    return guarded(h, [&] {
+        require(h->ep > 1, MOE_CONFIG, "moe_ep_export: ep_size must be > 1");
+        require(blob_out, MOE_SHAPE, "moe_ep_export: blob required");
+        require(h->ep <= 8 && (h->El * 4) % 16 == 0, MOE_UNSUPPORTED,
+                "moe_ep_export: the NVLink peer map needs ep <= 8 and experts per rank % 4 == 0");
+        require(!h->ipc && !h->comm, MOE_CONFIG, "moe_ep_export: handle already bound");
+        ipc_export(h, static_cast<EpBlob*>(blob_out));
+    });
+}
+
+moe_status moe_ep_import(moe_handle* h, const void* all_blobs) {
+    if (!h) return MOE_SHAPE;
+    return guarded(h, [&] {
+        require(h->flags_ipc.p && !h->ipc, MOE_CONFIG, "moe_ep_import: call moe_ep_export first");
+        require(all_blobs, MOE_SHAPE, "moe_ep_import: blobs required");
+        ipc_import(h, static_cast<const EpBlob*>(all_blobs));
     });
 }
 

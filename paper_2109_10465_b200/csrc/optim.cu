@@ -14,6 +14,7 @@
 // partials over a fixed grid, then one block), accumulated tensor by tensor in
 // stream order into a device double: deterministic.
 #include <cmath>
+#include <map>
 #include <mutex>
 
 #include "common.cuh"
@@ -97,28 +98,31 @@ adam_kernel(float* __restrict__ theta, float* __restrict__ m, float* __restrict_
     }
 }
 
+// Partial-sum scratch per (device, stream): concurrent norms on different
+// streams (two optimizers, per-layer optimizers on side streams) never share
+// a buffer; calls on one stream are ordered by the stream itself.
 struct Scratch {
-    double* partials[16] = {};
+    std::map<std::pair<int, cudaStream_t>, double*> partials;
     std::mutex mu;
 };
 static Scratch& scratch() {
     static Scratch s;
     return s;
 }
-static double* partials_for_device() {
+static double* partials_for(cudaStream_t st) {
     int dev = 0;
     MOE_CUDA_CHECK(cudaGetDevice(&dev));
     Scratch& s = scratch();
     std::lock_guard<std::mutex> lk(s.mu);
-    if (dev < 0 || dev >= 16) throw Status(6, "optim: device index out of range");
-    if (!s.partials[dev]) MOE_CUDA_CHECK(cudaMalloc(&s.partials[dev], sizeof(double) * kNormBlocks));
-    return s.partials[dev];
+    double*& p = s.partials[{dev, st}];
+    if (!p) MOE_CUDA_CHECK(cudaMalloc(&p, sizeof(double) * kNormBlocks));
+    return p;
 }
 
 }  // namespace opt
 
 void launch_grad_sqnorm(const void* g, int64_t n, bool bf16, double* acc, cudaStream_t st) {
-    double* part = opt::partials_for_device();
+    double* part = opt::partials_for(st);
     if (bf16)
         opt::sqnorm_partials_kernel<__nv_bfloat16><<<opt::kNormBlocks, opt::kNormThreads, 0, st>>>(
             static_cast<const __nv_bfloat16*>(g), n, part);

@@ -611,12 +611,25 @@ void launch_sum_ranks(const float* const* srcs, int ep, int64_t n, float* out, c
 // stores are ordered before it), then waits until every slot of its own array
 // has reached `epoch` (acquire).  One warp; a ~30 s clock budget traps
 // instead of hanging forever if a peer never arrives.
+//
+// With a ShapeCheck the barrier also carries each rank's token count: rank r
+// stores T_r into slot kShapeSlot + r of every peer's array before its epoch
+// (same release), and after the acquire compares every rank's T with its own.
+// Unequal per-rank T is the reference's UniformShapeError
+// (parallel.cpp:245-253): the flag latches MOE_FLAG_UNIFORM_SHAPE and the
+// received per-expert counts are zeroed so no expert GEMM touches rows laid
+// out for another rank's capacity.
+constexpr int kShapeSlot = 8;
 __global__ void ipc_barrier_kernel(PeerFlags peers, const unsigned long long* mine, int rank, int ep,
-                                   unsigned long long epoch) {
+                                   unsigned long long epoch, ShapeCheck sc) {
     pdl_wait();
     pdl_trigger();
     const int i = threadIdx.x;
+    bool bad = false;
     if (i < ep) {
+        if (sc.tokens >= 0)
+            asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(peers.f[i] + kShapeSlot + rank),
+                         "l"((unsigned long long)sc.tokens) : "memory");
         __threadfence_system();
         asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(peers.f[i] + rank), "l"(epoch) : "memory");
         unsigned long long v;
@@ -625,12 +638,46 @@ __global__ void ipc_barrier_kernel(PeerFlags peers, const unsigned long long* mi
             asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine + i) : "memory");
             if (clock64() - t0 > (1LL << 36)) __trap();
         } while (v < epoch);
+        if (sc.tokens >= 0) {
+            unsigned long long t;
+            asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(t) : "l"(mine + kShapeSlot + i) : "memory");
+            bad = t != (unsigned long long)sc.tokens;
+        }
+    }
+    if (__any_sync(0xffffffffu, bad)) {
+        for (int c = i; c < sc.ncounts; c += 32) sc.counts[c] = 0;
+        if (i == 0) atomicOr(sc.flags, MOE_FLAG_UNIFORM_SHAPE_DEV);
     }
 }
 
 void launch_ipc_barrier(const PeerFlags& peers, const unsigned long long* mine, int rank, int ep,
-                        unsigned long long epoch, cudaStream_t st) {
-    launch_pdl(ipc_barrier_kernel, dim3(1), dim3(32), 0, st, peers, mine, rank, ep, epoch);
+                        unsigned long long epoch, cudaStream_t st, const ShapeCheck* sc) {
+    ShapeCheck none{};
+    none.tokens = -1;
+    launch_pdl(ipc_barrier_kernel, dim3(1), dim3(32), 0, st, peers, mine, rank, ep, epoch, sc ? *sc : none);
+}
+
+// NCCL transport: `all_t` holds every rank's token count (all-gathered).
+__global__ void ep_shape_check_kernel(const long long* all_t, int ep, ShapeCheck sc) {
+    pdl_wait();
+    pdl_trigger();
+    const int i = threadIdx.x;
+    const bool bad = i < ep && all_t[i] != sc.tokens;
+    if (__any_sync(0xffffffffu, bad)) {
+        for (int c = i; c < sc.ncounts; c += 32) sc.counts[c] = 0;
+        if (i == 0) atomicOr(sc.flags, MOE_FLAG_UNIFORM_SHAPE_DEV);
+    }
+}
+__global__ void fill_i64_kernel(long long* p, long long v) {
+    pdl_wait();
+    pdl_trigger();
+    if (threadIdx.x == 0) *p = v;
+}
+void launch_fill_i64(long long* p, long long v, cudaStream_t st) {
+    launch_pdl(fill_i64_kernel, dim3(1), dim3(32), 0, st, p, v);
+}
+void launch_ep_shape_check(const long long* all_t, int ep, const ShapeCheck& sc, cudaStream_t st) {
+    launch_pdl(ep_shape_check_kernel, dim3(1), dim3(32), 0, st, all_t, ep, sc);
 }
 
 }  // namespace moe

@@ -160,6 +160,15 @@ def _p(t):
     return None if t is None else C.c_void_p(t.data_ptr())
 
 
+def _dense(t: torch.Tensor, device, name: str) -> None:
+    """The kernels read raw row-major device memory: reject views and tensors
+    on another device instead of reading them wrongly."""
+    if not t.is_cuda or t.device != torch.device(device):
+        raise ShapeError(f"moe_layer_forward: {name} must be on {device}")
+    if not t.is_contiguous():
+        raise ShapeError(f"moe_layer_forward: {name} must be contiguous")
+
+
 # --- handles -------------------------------------------------------------------
 class MoeHandle:
     """One moe_handle: workspace + saved forward context + stream binding."""
@@ -200,6 +209,28 @@ class MoeHandle:
     def ep_init(self, unique_id: bytes):
         buf = C.create_string_buffer(unique_id, len(unique_id))
         _check(L.load().moe_ep_init(self.h, buf), self.h)
+
+    def ep_bootstrap(self, all_gather, barrier):
+        """NCCL-free binding of the NVLink peer map (moe_ep_export/import):
+        ``all_gather(bytes) -> list[bytes]`` returns every rank's blob in rank
+        order, ``barrier()`` synchronises the ranks (e.g. torch.distributed
+        over gloo).  Ranks may share a GPU."""
+        lib = L.load()
+        n = lib.moe_ep_blob_size()
+        mine = C.create_string_buffer(n)
+        _check(lib.moe_ep_export(self.h, mine), self.h)
+        blobs = all_gather(mine.raw)
+        if len(blobs) != self.dims[4] or any(len(b) != n for b in blobs):
+            raise ConfigError("ep_bootstrap: one blob per rank required")
+        allb = C.create_string_buffer(b"".join(blobs), n * len(blobs))
+        _check(lib.moe_ep_import(self.h, allb), self.h)
+        barrier()
+
+    def gemm_path(self) -> str:
+        """'tcgen05' or 'simt': the kernel family of this handle's expert GEMMs."""
+        v = C.c_int()
+        _check(L.load().moe_gemm_path(self.h, C.byref(v)), self.h)
+        return "tcgen05" if v.value == 1 else "simt"
 
     def profile(self, on: bool):
         """Enable the per-stage CUDA-event timeline (resets accumulators)."""
@@ -464,8 +495,11 @@ class MoeLayer:
         self.d_model, self.d_ff = d_model, d_ff
         self.ep_size, self.ep_rank = ep_size, ep_rank
         self.n_local = cfg.num_experts // ep_size
+        # forward generation: the handle keeps ONE saved context, so an
+        # autograd node may only run backward for the latest forward
+        self._gen = 0
 
-    def _check_params(self, p: MoeLayerParams):
+    def _check_params(self, p: MoeLayerParams, device):
         E, El, d, f = self.cfg.num_experts, self.n_local, self.d_model, self.d_ff
         if tuple(p.gate_w.shape) != (d, E) or tuple(p.w1.shape) != (El, d, f) or \
                 tuple(p.w2.shape) != (El, f, d) or tuple(p.b1.shape) != (El, f) or \
@@ -473,12 +507,25 @@ class MoeLayer:
             raise ShapeError("moe_layer_forward: expert count does not match config")
         if p.w1.dtype != self.dtype or p.w2.dtype != self.dtype:
             raise ShapeError("moe_layer_forward: expert weight dtype does not match the layer")
+        for name in ("gate_w", "b1", "b2"):
+            if getattr(p, name).dtype != torch.float32:
+                raise ShapeError(f"moe_layer_forward: {name} must be float32")
+        for name in ("gate_w", "w1", "b1", "w2", "b2"):
+            _dense(getattr(p, name), device, name)
 
     def forward(self, x, params: MoeLayerParams, phase: Phase, seed: int, residual=None,
                 y=None, aux=None, decision: bool = True, check: bool = True):
-        self._check_params(params)
         if x.dim() != 2 or x.shape[1] != self.d_model or x.dtype != self.dtype:
             raise ShapeError("moe_layer_forward: x must be [T, d_model] of the layer dtype")
+        _dense(x, x.device, "x")
+        self._check_params(params, x.device)
+        if residual is not None:
+            if tuple(residual.shape) != tuple(x.shape) or residual.dtype != self.dtype:
+                raise ShapeError("moe_layer_forward: residual must be [T, d_model] of the layer dtype")
+            _dense(residual, x.device, "residual")
+        for name, t in (("y", y), ("aux", aux)):
+            if t is not None:
+                _dense(t, x.device, name)
         T = x.shape[0]
         K = self.cfg.top_k
         dev = x.device
@@ -506,10 +553,13 @@ class MoeLayer:
         # keep every tensor the saved context points at alive until backward
         # (the reference tape keeps its parents alive the same way, tensor.cpp:140-152)
         self._saved = (params, residual is not None, x, residual)
+        self._gen += 1
         return y, aux, dec
 
     def backward(self, dy, daux: float = 1.0, check: bool = True, grads=None):
-        params, has_res = self._saved[:2]
+        params, has_res, x = self._saved[:3]
+        if tuple(dy.shape) != tuple(x.shape) or dy.dtype != self.dtype:
+            raise ShapeError("moe_layer_backward: dy must be [T, d_model] of the layer dtype")
         El, d, f = self.n_local, self.d_model, self.d_ff
         dev = dy.device
         if grads is None:
@@ -535,6 +585,9 @@ class MoeLayer:
     def ep_init(self, unique_id: bytes):
         self.handle.ep_init(unique_id)
 
+    def ep_bootstrap(self, all_gather, barrier):
+        self.handle.ep_bootstrap(all_gather, barrier)
+
     def prefetch_jitter(self, seed: int, tokens: int):
         """moe_prefetch_jitter: generate the jitter stream of the forward with
         this seed during the next backward (values unchanged)."""
@@ -546,12 +599,17 @@ class _MoeFn(torch.autograd.Function):
     def forward(ctx, layer, params, phase, seed, x, gate_w, w1, b1, w2, b2, residual):
         y, aux, dec = layer.forward(x, params, phase, seed, residual)
         ctx.layer = layer
+        ctx.gen = layer._gen
         ctx.has_res = residual is not None
         layer._last_dec = dec
         return y, aux[0]
 
     @staticmethod
     def backward(ctx, dy, daux):
+        if ctx.layer._gen != ctx.gen:
+            raise MoeError("moe_layer_forward: this MoeLayer ran another forward before this "
+                           "node's backward; its handle keeps only the latest forward context "
+                           "(use one MoeLayer per in-flight forward)")
         daux_v = 0.0 if daux is None else float(daux)
         g = ctx.layer.backward(dy.to(ctx.layer.dtype).contiguous(), daux_v)
         return (None, None, None, None, g["dx"], g["dgate_w"], g["dw1"], g["db1"], g["dw2"],

@@ -1,4 +1,4 @@
-"""Multi-GPU expert-parallel parity check (run under torchrun, one rank per GPU).
+"""Expert-parallel parity check (run under torchrun, one process per rank).
 
 Contract (parallel.hpp:100-109, test_parallel.cpp:194-265): rank r gates its own
 tokens with seed derive_seed(seed, r); its output equals the single-rank layer
@@ -6,9 +6,22 @@ on x_r with that seed.  The reference's EP step is forward-only; the backward
 is pinned by composition: dx_r is rank-local, dWg is the sum over ranks, and an
 owned expert's grads are the sum over origin ranks of the single-rank grads.
 
-  torchrun --nproc-per-node N tests/ep_check.py [fp32|bf16]
-Prints 'EP_OK <max errors>' on rank 0 and exits non-zero on mismatch.
+  torchrun --nproc-per-node N tests/ep_check.py MODE [options]
+    MODE          fp32 | bf16
+    --shape       small (E = 4/rank, T=256, d=256, f=512; full oracle composition)
+                  c3    (config 3 widths: E=64 sharded, d=2048, f=8192, T_r=512,
+                         bf16; every element of y, dx, dWg and all owned experts'
+                         dW1/db1/dW2/db2 within the derived bf16 bound of an f64
+                         recomputation from the oracle's per-rank decisions)
+    --bootstrap   nccl (moe_ep_init: NCCL communicator + IPC map)
+                  ipc  (moe_ep_export/import over a gloo all-gather; no NCCL)
+    --same-gpu    every rank on cuda:0 (two processes sharing one GPU; needs
+                  --bootstrap ipc, NCCL refuses duplicate GPUs)
+    --uneven      rank 1 passes one token fewer: every rank must raise
+                  UniformShapeError (parallel.cpp:245-253, test_parallel.cpp:226-235)
+Prints 'EP_OK ...' on rank 0 and exits non-zero on mismatch.
 """
+import argparse
 import os
 import sys
 
@@ -22,24 +35,49 @@ sys.path.insert(0, ROOT)
 import oracle as O  # noqa: E402
 import paper_2109_10465_b200 as M  # noqa: E402
 from oracle.margin import margin_guard  # noqa: E402
+from tests import ref_f64 as R  # noqa: E402
 
 
-def main():
-    mode = sys.argv[1] if len(sys.argv) > 1 else "fp32"
-    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+def bf16_rnd(a):
+    return torch.from_numpy(np.asarray(a, np.float32)).to(torch.bfloat16).float().numpy().astype(np.float64)
+
+
+def f32_rnd(a):
+    return np.asarray(a, np.float64).astype(np.float32).astype(np.float64)
+
+
+def bind(layer, args, rank, world):
+    if args.bootstrap == "nccl":
+        uid = [M.ep_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        layer.ep_init(uid[0])
+    else:
+        def all_gather(b):
+            out = [None] * world
+            dist.all_gather_object(out, b)
+            return out
+        layer.ep_bootstrap(all_gather, dist.barrier)
+
+
+def rel(a, b):  # element-wise, max(1,|ref|) normalisation
+    a = a.float().cpu().numpy().astype(np.float64)
+    return float(np.max(np.abs(a - b) / np.maximum(1.0, np.abs(b))))
+
+
+def reln(a, b):  # norm-wise for token-reduced gradients
+    a = a.float().cpu().numpy().astype(np.float64)
+    return float(np.max(np.abs(a - b)) / max(1.0, float(np.max(np.abs(b)))))
+
+
+def check_small(args, rank, world, dev):
     E, El = 4 * world, 4
     T, d, f = 256, 256, 512
     seed = 77
-    dt = torch.float32 if mode == "fp32" else torch.bfloat16
+    dt = torch.float32 if args.mode == "fp32" else torch.bfloat16
     o = O.restatement()
     x_all, gw, w1, b1, w2, b2, dy_all = O.layer_inputs(T * world, d, f, E, seed=5)
     cfg_o = O.make_cfg(num_experts=E, capacity_factor_train=1.0)
-    rnd = (lambda a: a.astype(np.float32).astype(np.float64)) if mode == "fp32" else \
-        (lambda a: torch.from_numpy(np.asarray(a, np.float32)).to(torch.bfloat16).float().numpy().astype(np.float64))
+    rnd = f32_rnd if args.mode == "fp32" else bf16_rnd
     xs, dys = [], []
     for r in range(world):
         xr = rnd(x_all[r * T:(r + 1) * T])
@@ -47,7 +85,7 @@ def main():
         xs.append(xr)
         dys.append(rnd(dy_all[r * T:(r + 1) * T]))
     w1r, w2r = rnd(w1), rnd(w2)
-    gwr, b1r, b2r = [a.astype(np.float32).astype(np.float64) for a in (gw, b1, b2)]
+    gwr, b1r, b2r = [f32_rnd(a) for a in (gw, b1, b2)]
     refs = [o.moe_layer(xs[r], gwr, w1r, b1r, w2r, b2r, cfg_o, O.TRAIN, o.derive_seed(seed, r),
                         dy=dys[r], daux=1.0) for r in range(world)]
 
@@ -56,21 +94,12 @@ def main():
     params = M.MoeLayerParams(to(gwr), to(w1r[lo:hi], dt), to(b1r[lo:hi]), to(w2r[lo:hi], dt),
                               to(b2r[lo:hi]))
     layer = M.MoeLayer(M.RouterConfig(num_experts=E), T, d, f, dt, ep_size=world, ep_rank=rank)
-    uid = [M.ep_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(uid, src=0)
-    layer.ep_init(uid[0])
+    bind(layer, args, rank, world)
+    if args.uneven:
+        return check_uneven(layer, params, to(xs[rank], dt), rank, seed)
     y, aux, dec = layer.forward(to(xs[rank], dt), params, M.Phase.TRAIN, M.derive_seed(seed, rank))
     g = layer.backward(to(dys[rank], dt), 1.0)
     torch.cuda.synchronize()
-
-    def rel(a, b):  # element-wise, max(1,|ref|) normalisation
-        a = a.float().cpu().numpy().astype(np.float64)
-        return float(np.max(np.abs(a - b) / np.maximum(1.0, np.abs(b))))
-
-    def reln(a, b):  # norm-wise for token-reduced gradients
-        a = a.float().cpu().numpy().astype(np.float64)
-        return float(np.max(np.abs(a - b)) / max(1.0, float(np.max(np.abs(b)))))
-
     ref = refs[rank]
     ok = np.array_equal(dec.expert_id.cpu().numpy(), ref.expert_id) and \
         np.array_equal(dec.slot.cpu().numpy(), ref.slot)
@@ -82,17 +111,136 @@ def main():
     # fp32: element-wise 1e-5.  bf16: norm-wise like test_gpu_bf16 —
     # element-wise maxima over 4 ranks of bf16-rounded chains (dH, dX, y all
     # rounded to 2^-8) sit at the 2e-2 line by chance alone
-    ew = rel if mode == "fp32" else reln
+    ew = rel if args.mode == "fp32" else reln
     errs = dict(y=ew(y, ref.y), dx=ew(g["dx"], ref.dx), aux=abs(aux.item() - ref.aux),
                 dgate_w=reln(g["dgate_w"], dwg), dw1=reln(g["dw1"], dw1), dw2=reln(g["dw2"], dw2),
                 db1=reln(g["db1"], db1), db2=reln(g["db2"], db2))
-    tol = 1e-5 if mode == "fp32" else 2e-2
-    bad = torch.tensor([0 if ok and all(v <= tol for v in errs.values()) else 1], device=dev)
+    tol = 1e-5 if args.mode == "fp32" else 2e-2
+    good = ok and all(v <= tol for v in errs.values())
+    print(f"rank {rank} decisions_ok={ok} errs={ {k: f'{v:.2e}' for k, v in errs.items()} }", flush=True)
+    return good
+
+
+def check_c3(args, rank, world, dev):
+    """Config-3 widths under EP: per-rank decisions from the f64 oracle,
+    outputs / gradients vs the f64 recomputation composed over ranks."""
+    E, d, f, T = 64, 2048, 8192, args.tokens
+    El = E // world
+    seed = 91
+    o = O.restatement()
+    cfg_o = O.make_cfg(num_experts=E, capacity_factor_train=1.0)
+    _, gw, *_ = O.layer_inputs(8, d, 8, E, seed=seed)
+    gw = f32_rnd(gw)
+    xs, dec_o = [], []
+    for r in range(world):
+        xr = bf16_rnd(O.uniform(o.derive_seed(o.derive_seed(seed, "x"), r), T * d, -1.0, 1.0).reshape(T, d))
+        rs = o.derive_seed(seed, r)
+        xr = margin_guard(xr, gw, cfg_o, O.TRAIN, rs, round_fn=bf16_rnd)
+        xs.append(xr)
+        probs, ch, gp, noise = o.gate_forward(xr, gw, cfg_o, O.TRAIN, o.derive_seed(rs, "jitter"))
+        slot, cap = o.assign(ch, E, o.capacity(T, cfg_o, O.TRAIN), 1, O.PLAIN, 1, 0)
+        dec_o.append((probs, ch, gp, noise, slot, cap))
+    # expert weights: one generator stream for all E experts (identical on every rank)
+    g = torch.Generator(device=dev).manual_seed(seed)
+    s1 = float(np.sqrt(6.0 / (d + f)))
+    w1 = ((torch.rand(E, d, f, device=dev, generator=g) * 2 - 1) * s1).to(torch.bfloat16)
+    w2 = ((torch.rand(E, f, d, device=dev, generator=g) * 2 - 1) * s1).to(torch.bfloat16)
+    b1 = (torch.rand(E, f, device=dev, generator=g) * 2 - 1) * 0.01
+    b2 = (torch.rand(E, d, device=dev, generator=g) * 2 - 1) * 0.01
+    dys = [(torch.rand(T, d, device=dev, generator=g) * 2 - 1).to(torch.bfloat16) for _ in range(world)]
+    lo, hi = rank * El, (rank + 1) * El
+    params = M.MoeLayerParams(torch.from_numpy(gw.astype(np.float32)).to(dev), w1[lo:hi].contiguous(),
+                              b1[lo:hi].contiguous(), w2[lo:hi].contiguous(), b2[lo:hi].contiguous())
+    layer = M.MoeLayer(M.RouterConfig(num_experts=E), T, d, f, torch.bfloat16, ep_size=world,
+                       ep_rank=rank)
+    assert layer.handle.gemm_path() == "tcgen05"
+    bind(layer, args, rank, world)
+    xd = torch.from_numpy(xs[rank].astype(np.float32)).to(dev).to(torch.bfloat16)
+    y, aux, dec = layer.forward(xd, params, M.Phase.TRAIN, M.derive_seed(seed, rank))
+    gr = layer.backward(dys[rank], 1.0)
+    torch.cuda.synchronize()
+    probs, ch, gp, noise, slot, cap = dec_o[rank]
+    ok = dec.capacity == cap and np.array_equal(dec.expert_id.cpu().numpy(), ch) and \
+        np.array_equal(dec.slot.cpu().numpy(), slot)
+    sums = {}
+
+    def sink(e, parts):
+        for k, (ref, var) in parts.items():
+            if (k, e) in sums:
+                sums[(k, e)] = (sums[(k, e)][0] + ref, sums[(k, e)][1] + var)
+            else:
+                sums[(k, e)] = (ref, var)
+
+    dwg = None
+    res = None
+    for r in range(world):
+        probs, ch, gp, noise, slot, cap = dec_o[r]
+        out = dict(y=y, aux=aux[0], dx=gr["dx"], dgate_w=gr["dgate_w"]) if r == rank else None
+        rr = R.check_layer(dev, out, xs[r], gw, w1, b1, w2, b2,
+                           dys[r].float().cpu().numpy().astype(np.float64), probs=probs, noise=noise,
+                           expert_id=ch, slot=slot, gate_prob=gp, E=E, K=1, alpha=0.01, daux=1.0,
+                           experts=range(lo, hi), expert_sink=sink)
+        dwg = rr["_dgate_w"] if dwg is None else (dwg[0] + rr["_dgate_w"][0], dwg[1] + rr["_dgate_w"][1])
+        if r == rank:
+            res = {k: v for k, v in rr.items() if k in ("y", "dx", "aux")}
+    st = {k: R.Stat() for k in ("dgate_w", "dw1", "dw2", "db1", "db2")}
+    st["dgate_w"].add(gr["dgate_w"], dwg[0], dwg[1])
+    for e in range(lo, hi):
+        for k in ("dw1", "dw2", "db1", "db2"):
+            if (k, e) not in sums:
+                continue
+            ref, var = sums[(k, e)]
+            det = R.U * ref.abs() if k in ("dw1", "dw2") else None   # bf16 return
+            st[k].add(gr[k][e - lo], ref, var, det)
+    res.update(st)
+    print(f"rank {rank} decisions_ok={ok} " + " ".join(f"{k}: {v}" for k, v in res.items()), flush=True)
+    try:
+        R.assert_within(res, f"rank {rank}")
+        good = ok
+    except AssertionError as ex:
+        print(ex, flush=True)
+        good = False
+    return good
+
+
+def check_uneven(layer, params, x, rank, seed):
+    T = x.shape[0] - (1 if rank == 1 else 0)
+    try:
+        layer.forward(x[:T].contiguous(), params, M.Phase.TRAIN, M.derive_seed(seed, rank))
+    except M.UniformShapeError as ex:
+        print(f"rank {rank} UniformShapeError: {ex}", flush=True)
+        # the handle stays usable: a matching forward afterwards succeeds
+        layer.forward(x, params, M.Phase.TRAIN, M.derive_seed(seed, rank))
+        return True
+    print(f"rank {rank}: no UniformShapeError for T={T}", flush=True)
+    return False
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("mode", nargs="?", default="fp32", choices=["fp32", "bf16"])
+    ap.add_argument("--shape", default="small", choices=["small", "c3"])
+    ap.add_argument("--bootstrap", default="nccl", choices=["nccl", "ipc"])
+    ap.add_argument("--same-gpu", action="store_true")
+    ap.add_argument("--uneven", action="store_true")
+    ap.add_argument("--tokens", type=int, default=512)
+    args = ap.parse_args()
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = 0 if args.same_gpu else int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if args.bootstrap == "ipc":
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
+    good = check_c3(args, rank, world, dev) if args.shape == "c3" else check_small(args, rank, world, dev)
+    bad = torch.tensor([0 if good else 1])
+    if args.bootstrap == "nccl":
+        bad = bad.to(dev)
     dist.all_reduce(bad)
-    print(f"rank {rank} decisions_ok={ok} errs={ {k: f'{v:.2e}' for k, v in errs.items()} }",
-          flush=True)
     if rank == 0:
-        print("EP_OK" if bad.item() == 0 else "EP_FAIL", world, mode, flush=True)
+        print("EP_OK" if bad.item() == 0 else "EP_FAIL", world, args.mode, args.shape, args.bootstrap,
+              "same-gpu" if args.same_gpu else "", "uneven" if args.uneven else "", flush=True)
     dist.destroy_process_group()
     sys.exit(0 if bad.item() == 0 else 1)
 
