@@ -92,7 +92,7 @@ def test_bf16_tcgen05_vs_oracle(name, cfgk, T, d, f, E):
     probs, ch, gp, noise = o.gate_forward(arrs[0], arrs[1], ocfg, O.TRAIN, o.derive_seed(seed, "jitter"))
     assert np.array_equal(ch, ref.expert_id)
     tt = lambda a, dt=torch.float32: torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dt)  # noqa
-    dout = {k: tt(v) for k, v in out.items() if k not in ("expert_id", "slot")}
+    dout = {k: tt(v) for k, v in out.items() if k not in ("expert_id", "slot") and v is not None}
     res = R.check_layer("cuda", dout, arrs[0], arrs[1], tt(arrs[2]), tt(arrs[3]), tt(arrs[4]),
                         tt(arrs[5]), arrs[6], probs=probs, noise=noise, expert_id=ch,
                         slot=ref.slot, gate_prob=gp, E=E, K=K, alpha=0.01, daux=1.0)
