@@ -168,27 +168,37 @@ def run_reference_arm(args):
     secs = sorted(times)[len(times) // 2]
     T = 128
     value = T * threads / secs
-    sample = (f"per step: {threads} concurrent replicas of one config-3 expert (d=2048, f=8192, "
-              f"cap=128, 128 tokens, train, jitter on) fwd+bwd; median of {args.steps} steps")
+    sample = (f"per step: {threads} concurrent replicas (one per host thread, {os.cpu_count()} host cores) "
+              f"of one expert's share of the config-3 layer: E'=1, d=2048, f=8192, cap=128, 128 tokens, "
+              f"train, jitter on, fwd+bwd through the reference's moe_layer_forward + Tensor::backward; "
+              f"median of {args.steps} steps.  The reference computes every capacity row of every expert "
+              f"one expert after another (routing.cpp:397-406), so the 64-expert layer's time is 64x this "
+              f"share plus the O(T d E) gate (<0.2% of its FLOPs); cross-checked against BASELINE.md 3a's "
+              f"affine fit over the full 64-expert layer in profiles/r02_reference_fit.json")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": workload_config(args.gpus),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "host_cores": os.cpu_count(),
+                             "kind": kind, "sample": sample, "extrapolated": True},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-def workload_config(n):
-    return {"workload": WORKLOAD["name"], "experts": WORKLOAD["experts"],
-            "experts_per_gpu": WORKLOAD["experts"] // max(n, 1), "d_model": WORKLOAD["d_model"],
+def workload_config(n, E=None, T=None):
+    E = E or WORKLOAD["experts"]
+    T = T or WORKLOAD["tokens_per_gpu"]
+    name = WORKLOAD["name"] if E == WORKLOAD["experts"] and T == WORKLOAD["tokens_per_gpu"] else \
+        f"c3_variant_E{E}_T{T}"
+    return {"workload": name, "experts": E,
+            "experts_per_gpu": E // max(n, 1), "d_model": WORKLOAD["d_model"],
             "d_ff": WORKLOAD["d_ff"], "top_k": 1, "capacity_factor": 1.0,
             "assignment": "plain", "phase": "train", "jitter_eps": WORKLOAD["jitter_eps"],
-            "balance_coeff": WORKLOAD["balance_coeff"], "tokens_per_gpu": WORKLOAD["tokens_per_gpu"],
-            "global_tokens": WORKLOAD["tokens_per_gpu"] * n, "parallelism": f"ep{n}",
+            "balance_coeff": WORKLOAD["balance_coeff"], "tokens_per_gpu": T,
+            "global_tokens": T * n, "parallelism": f"ep{n}",
             "l2": "inputs larger than L2: expert weights %.2f GB/GPU stream from HBM every step"
-                  % (2 * WORKLOAD["experts"] // max(n, 1) * WORKLOAD["d_model"] * WORKLOAD["d_ff"] * 2 / 1e9)}
+                  % (2 * E // max(n, 1) * WORKLOAD["d_model"] * WORKLOAD["d_ff"] * 2 / 1e9)}
 
 
 # ---------------------------------------------------------------- our kernels
@@ -266,7 +276,7 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if N > 1:
         dist.init_process_group("nccl", device_id=dev)
-    E, d, f = WORKLOAD["experts"], WORKLOAD["d_model"], WORKLOAD["d_ff"]
+    E, d, f = args.experts or WORKLOAD["experts"], WORKLOAD["d_model"], WORKLOAD["d_ff"]
     T = args.tokens_per_gpu
     El = E // N
     cfg = M.RouterConfig(num_experts=E, capacity_factor_train=WORKLOAD["capacity_factor"],
@@ -470,7 +480,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random-init weights of the config-3 architecture, U(-1,1) tokens)",
-            "config": dict(workload_config(N), seeds="per step: derive_seed(derive_seed(42, rank), step)",
+            "config": dict(workload_config(N, E, T), seeds="per step: derive_seed(derive_seed(42, rank), step)",
                            jitter_stream="generated during the previous step's backward (moe_prefetch_jitter)"
                            if args.prefetch else "generated at the head of each forward"),
             "roofline": roof,
@@ -489,9 +499,12 @@ def run_ours(args):
             threads = cpu_threads_for(1.2e9, 16)
             kind, tps, secs = time_reference(threads)
             _, cfg_s, Ts = reference_sample_inputs()
-            line["cpu_baseline"] = {"value": tps, "unit": UNIT, "cores": threads, "kind": kind,
-                                    "sample": f"{threads} concurrent replicas of one config-3 expert "
-                                              f"(d=2048, f=8192, cap=128, {Ts} tokens) fwd+bwd, {secs:.1f} s"}
+            line["cpu_baseline"] = {"value": tps, "unit": UNIT, "cores": threads, "host_cores": os.cpu_count(),
+                                    "kind": kind, "extrapolated": True,
+                                    "sample": f"{threads} concurrent replicas of one expert's share of the "
+                                              f"config-3 layer (E'=1, d=2048, f=8192, cap=128, {Ts} tokens) "
+                                              f"fwd+bwd, {secs:.1f} s; the 64-expert layer is 64 such shares "
+                                              f"run in sequence (routing.cpp:397-406)"}
         except Exception as ex:  # pragma: no cover
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable",
                                     "sample": str(ex)}
@@ -595,6 +608,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tokens-per-gpu", type=int, default=WORKLOAD["tokens_per_gpu"])
+    ap.add_argument("--experts", type=int, default=0,
+                    help="config-3 variant with this many experts in total (EP-overhead baselines: "
+                         "1 GPU with E=64/N experts has the same rows per expert as N GPUs with E=64)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--prefetch", action="store_true",
                     help="generate the next step's jitter stream during this step's backward "

@@ -178,6 +178,35 @@ moe_status moe_adam_update(float* theta, float* m, float* v, const void* grad, i
                            int grad_dtype, void* theta_bf16, const double* scale_dev, double lr,
                            double beta1, double beta2, double eps, int64_t step, void* stream);
 
+/* ---- capacity check: the ZeRO-2 / EP memory planner ---------------------
+ * ParallelPlan / MemoryEstimate / memory_per_gpu / max_model_size
+ * (parallel.hpp:13-74, parallel.cpp:18-115), host arithmetic with the
+ * reference's bytes-per-parameter model (2 param + 2 grad + 12 optimizer),
+ * which is this build's training layout (bf16 params / grads, fp32 master +
+ * Adam moments).  moe_workspace_bytes adds what a handle really allocated
+ * (activations, buffers) so callers can check a plan against HBM. */
+typedef struct {
+    int world_size;      /* N */
+    int expert_parallel; /* ep */
+    int model_parallel;  /* mp; data_parallel = N / mp */
+    int zero_stage;      /* 0 or 2 */
+    int offload;         /* grads + optimizer states in host memory */
+} moe_parallel_plan;
+typedef struct {
+    double nonexpert_params, expert_params, nonexpert_grads, expert_grads, nonexpert_optim,
+        expert_optim;
+    int grad_optim_on_cpu;
+    double gpu_total, cpu_total, optimizer_grad_share;
+} moe_memory_estimate;
+moe_status moe_plan_validate(const moe_parallel_plan* plan);
+const char* moe_plan_last_error(void); /* text of the last plan error (this thread) */
+moe_status moe_memory_per_gpu(const moe_parallel_plan* plan, double nonexpert_params,
+                              double expert_params, moe_memory_estimate* out);
+moe_status moe_max_model_size(const moe_parallel_plan* plan, double gpu_budget_bytes, double base_params,
+                              double params_per_expert, int64_t* max_experts, double* total_params);
+/* Device bytes this handle allocated for its workspace and saved context. */
+moe_status moe_workspace_bytes(const moe_handle* h, size_t* bytes_out);
+
 /* ---- per-stage entry points (routing.hpp:60-118) ----------------------- */
 /* gate_forward (routing.cpp:51-101): probs [T,E] fp32, choice [T*k] int32,
  * gate_prob [T*k] fp32.  x has the handle's dtype. */

@@ -324,4 +324,37 @@ int ref_prune_checkpoint(const char* dir_in, const char* dir_out, int k, int str
     });
 }
 
+// ---- parallel.cpp:18-115: the ZeRO-2 / EP memory planner -----------------
+struct ref_plan {
+    int world_size, expert_parallel, model_parallel, zero_stage, offload;
+};
+int ref_memory_per_gpu(const ref_plan* p, double nonexpert, double expert, double* out7) {
+    return guarded([&] {
+        ParallelPlan plan;
+        plan.world_size = p->world_size;
+        plan.expert_parallel = p->expert_parallel;
+        plan.model_parallel = p->model_parallel;
+        plan.zero_stage = p->zero_stage;
+        plan.offload = p->offload != 0;
+        const MemoryEstimate e = memory_per_gpu(plan, nonexpert, expert);
+        const double v[7] = {e.nonexpert_params, e.expert_params, e.nonexpert_grads, e.expert_grads,
+                             e.nonexpert_optim, e.expert_optim, e.gpu_total()};
+        std::memcpy(out7, v, sizeof(v));
+    });
+}
+int ref_max_model_size(const ref_plan* p, double budget, double base, double per_expert,
+                       int64_t* max_experts, double* total) {
+    return guarded([&] {
+        ParallelPlan plan;
+        plan.world_size = p->world_size;
+        plan.expert_parallel = p->expert_parallel;
+        plan.model_parallel = p->model_parallel;
+        plan.zero_stage = p->zero_stage;
+        plan.offload = p->offload != 0;
+        const MaxModelSize m = max_model_size(plan, budget, base, per_expert);
+        *max_experts = m.max_experts;
+        *total = m.total_params;
+    });
+}
+
 }  // extern "C"

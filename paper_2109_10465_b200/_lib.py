@@ -32,6 +32,18 @@ class moe_router_cfg(C.Structure):
     ]
 
 
+class moe_parallel_plan(C.Structure):
+    _fields_ = [(n, C.c_int) for n in ("world_size", "expert_parallel", "model_parallel",
+                                         "zero_stage", "offload")]
+
+
+class moe_memory_estimate(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("nonexpert_params", "expert_params", "nonexpert_grads",
+                                            "expert_grads", "nonexpert_optim", "expert_optim")] + \
+        [("grad_optim_on_cpu", C.c_int)] + \
+        [(n, C.c_double) for n in ("gpu_total", "cpu_total", "optimizer_grad_share")]
+
+
 class moe_layer_dims(C.Structure):
     _fields_ = [
         ("max_tokens", C.c_int64),
@@ -74,6 +86,13 @@ _SIGS = {
     "moe_ep_traffic": (C.c_int, [H, VP, C.POINTER(C.c_double)]),
     "moe_ep_blob_size": (C.c_size_t, []),
     "moe_gemm_path": (C.c_int, [H, C.POINTER(C.c_int)]),
+    "moe_workspace_bytes": (C.c_int, [H, C.POINTER(C.c_size_t)]),
+    "moe_plan_validate": (C.c_int, [C.POINTER(moe_parallel_plan)]),
+    "moe_plan_last_error": (C.c_char_p, []),
+    "moe_memory_per_gpu": (C.c_int, [C.POINTER(moe_parallel_plan), C.c_double, C.c_double,
+                                     C.POINTER(moe_memory_estimate)]),
+    "moe_max_model_size": (C.c_int, [C.POINTER(moe_parallel_plan), C.c_double, C.c_double, C.c_double,
+                                     C.POINTER(C.c_int64), C.POINTER(C.c_double)]),
     "moe_ep_export": (C.c_int, [H, VP]),
     "moe_ep_import": (C.c_int, [H, VP]),
     "moe_profile_enable": (C.c_int, [H, C.c_int]),

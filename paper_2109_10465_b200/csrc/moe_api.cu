@@ -35,6 +35,9 @@ namespace {
             throw Status(MOE_NCCL, std::string(#expr) + ": " + ncclGetErrorString(_r));    \
     } while (0)
 
+// bytes allocated through DevMem by the handle being created / bound (for
+// moe_workspace_bytes); handles are created one at a time per thread
+thread_local size_t* g_ws_counter = nullptr;
 struct DevMem {
     void* p = nullptr;
     size_t bytes = 0;
@@ -42,6 +45,7 @@ struct DevMem {
         if (b == 0) b = 16;
         MOE_CUDA_CHECK(cudaMalloc(&p, b));
         bytes = b;
+        if (g_ws_counter) *g_ws_counter += b;
     }
     ~DevMem() {
         if (p) cudaFree(p);
@@ -164,7 +168,8 @@ struct moe_handle {
     unsigned long long epoch = 0;
     bool nccl_barrier = false;
     bool defer_balance = false;
-    bool gemm_tc = false;        // bf16 expert GEMMs on tcgen05 (decided at create)  // forward under EP: the balance loss runs next to the dispatch exchange
+    bool gemm_tc = false;        // bf16 expert GEMMs on tcgen05 (decided at create)
+    size_t ws_bytes = 0;         // device bytes allocated by this handle  // forward under EP: the balance loss runs next to the dispatch exchange
     ~moe_handle() {
         for (int b = 0; b < P_NBUF; ++b)
             for (int r = 0; r < 8; ++r)
@@ -998,7 +1003,13 @@ moe_status moe_create(const moe_router_cfg* cfg, const moe_layer_dims* dims, moe
         h->d = dims->d_model;
         h->f = dims->d_ff;
         h->esz = dims->dtype == MOE_BF16 ? 2 : 4;
-        alloc_workspace(h.get());
+        {
+            struct Count {  // RAII: never leave the counter pointing at a failed handle
+                explicit Count(size_t* c) { g_ws_counter = c; }
+                ~Count() { g_ws_counter = nullptr; }
+            } count(&h->ws_bytes);
+            alloc_workspace(h.get());
+        }
         if (h->esz == 2) {
             // The bf16 path's expert GEMMs run on tcgen05 when the shape tiles
             // (d, f multiples of 256); otherwise they run on the fp32-accumulating
@@ -1364,6 +1375,12 @@ moe_status moe_ep_init(moe_handle* h, const void* unique_id) {
         const bool want_ipc = !(tr && std::string(tr) == "nccl");
         if (want_ipc && h->ep <= 8 && (h->El * 4) % 16 == 0) ipc_setup(h);
     });
+}
+
+moe_status moe_workspace_bytes(const moe_handle* h, size_t* bytes_out) {
+    if (!h || !bytes_out) return MOE_SHAPE;
+    *bytes_out = h->ws_bytes;
+    return MOE_OK;
 }
 
 moe_status moe_gemm_path(const moe_handle* h, int* path_out) {
