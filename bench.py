@@ -530,36 +530,54 @@ EXTRA = {
 
 
 def run_extra(args):
-    """Device-timed tokens/s for the other BASELINE configs (rank 0, 1 GPU)."""
+    """Device-timed tokens/s for the other BASELINE configs.  One GPU, or under
+    torchrun N ranks with expert parallelism (E/N experts per rank, every
+    layer's peer map bound with moe_ep_export/import; value = N*T / max-over-
+    ranks step time, weak scaling at T tokens per GPU)."""
     import numpy as np
     import torch
+    import torch.distributed as dist
 
     import paper_2109_10465_b200 as M
     w = EXTRA[args.workload]
-    E, d, f, T, L = w["E"], w["d"], w["f"], args.tokens or w["T"], w["layers"]
+    E, d, f, T, L = args.experts or w["E"], w["d"], w["f"], args.tokens or w["T"], w["layers"]
+    N = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if N > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    El = E // N
     dt = torch.float32 if w["dtype"] == "fp32" else torch.bfloat16
-    dev = torch.device("cuda", 0)
     g = torch.Generator(device=dev).manual_seed(7)
+    gr = torch.Generator(device=dev).manual_seed(70 + rank)
     cfg = M.RouterConfig(num_experts=E, top_k=w["k"], capacity_factor_train=w["C"],
                          capacity_factor_eval=w["C"] if w["phase"] == 1 else 2.0,
                          assignment_mode=M.AssignmentMode(w["mode"]))
     s_w = float(np.sqrt(6.0 / (d + f)))
     layers, params = [], []
     for _ in range(L):
-        layers.append(M.MoeLayer(cfg, T, d, f, dt))
+        layers.append(M.MoeLayer(cfg, T, d, f, dt, ep_size=N, ep_rank=rank))
+        if N > 1:
+            def all_gather(b):
+                out = [None] * N
+                dist.all_gather_object(out, b)
+                return out
+            layers[-1].ep_bootstrap(all_gather, dist.barrier)
         params.append(M.MoeLayerParams(
             (torch.rand(d, E, device=dev, generator=g) * 2 - 1) * float(np.sqrt(6.0 / (d + E))),
-            ((torch.rand(E, d, f, device=dev, generator=g) * 2 - 1) * s_w).to(dt),
-            (torch.rand(E, f, device=dev, generator=g) * 2 - 1) * 0.01,
-            ((torch.rand(E, f, d, device=dev, generator=g) * 2 - 1) * s_w).to(dt),
-            (torch.rand(E, d, device=dev, generator=g) * 2 - 1) * 0.01))
-    x0 = ((torch.rand(T, d, device=dev, generator=g) * 2 - 1)).to(dt)
-    dy0 = ((torch.rand(T, d, device=dev, generator=g) * 2 - 1)).to(dt)
+            ((torch.rand(El, d, f, device=dev, generator=gr) * 2 - 1) * s_w).to(dt),
+            (torch.rand(El, f, device=dev, generator=gr) * 2 - 1) * 0.01,
+            ((torch.rand(El, f, d, device=dev, generator=gr) * 2 - 1) * s_w).to(dt),
+            (torch.rand(El, d, device=dev, generator=gr) * 2 - 1) * 0.01))
+    x0 = ((torch.rand(T, d, device=dev, generator=gr) * 2 - 1)).to(dt)
+    dy0 = ((torch.rand(T, d, device=dev, generator=gr) * 2 - 1)).to(dt)
     ys = [torch.empty_like(x0) for _ in range(L)]
     aux = torch.empty(1, device=dev)
     grads = [dict(dx=torch.empty_like(x0), dgate_w=torch.empty(d, E, device=dev),
-                  dw1=torch.empty(E, d, f, device=dev, dtype=dt), db1=torch.empty(E, f, device=dev),
-                  dw2=torch.empty(E, f, d, device=dev, dtype=dt), db2=torch.empty(E, d, device=dev),
+                  dw1=torch.empty(El, d, f, device=dev, dtype=dt), db1=torch.empty(El, f, device=dev),
+                  dw2=torch.empty(El, f, d, device=dev, dtype=dt), db2=torch.empty(El, d, device=dev),
                   dresidual=torch.empty_like(x0)) for _ in range(L)]
     zero = torch.zeros_like(x0)
     phase = M.Phase(w["phase"])
@@ -567,7 +585,7 @@ def run_extra(args):
     def step(i):
         h = x0
         for l in range(L):  # stack: zero residual inside blocks (model.cpp:340-350)
-            layers[l].forward(h, params[l], phase, M.derive_seed(M.derive_seed(42, i), l),
+            layers[l].forward(h, params[l], phase, M.derive_seed(M.derive_seed(M.derive_seed(42, rank), i), l),
                               residual=zero if L > 1 else None, y=ys[l], aux=aux, decision=False,
                               check=False)
             h = ys[l]
@@ -578,26 +596,59 @@ def run_extra(args):
             layers[l].backward(g_, 1.0, check=False, grads=grads[l])
             g_ = grads[l]["dx"]
 
+    def barrier():
+        torch.cuda.synchronize()
+        if N > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
     for i in range(max(args.warmup, 3)):
         step(i)
     for lay in layers:
         lay.handle.check()
-    torch.cuda.synchronize()
+    barrier()
+    prof = args.workload == "c5" and L == 1
+    if prof:
+        layers[0].handle.profile(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(args.steps):
         step(i)
     e1.record()
-    torch.cuda.synchronize()
+    barrier()
     ms = e0.elapsed_time(e1) / args.steps
+    if N > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
     flops = (4.0 if w["fwd_only"] else 12.0) * T * w["k"] * d * f * L
-    print(json.dumps({"metric": "MoE layer " + ("fwd" if w["fwd_only"] else "fwd+bwd") + " tokens/sec",
-                      "value": T / (ms / 1e3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
-                      "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-                      "dtype": w["dtype"], "data": "synthetic",
-                      "config": {"workload": args.workload, "desc": w["desc"], "tokens": T,
-                                 "layers": L, "experts": E, "d_model": d, "d_ff": f, "top_k": w["k"]},
-                      "expert_tflops_upper_bound": flops / (ms / 1e3) / 1e12}), flush=True)
+    line = {"metric": "MoE layer " + ("fwd" if w["fwd_only"] else "fwd+bwd") + " tokens/sec",
+            "value": N * T / (ms / 1e3), "unit": UNIT, "n_gpus": N, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "dtype": w["dtype"], "data": "synthetic",
+            "config": {"workload": args.workload, "desc": w["desc"], "tokens_per_gpu": T,
+                       "layers": L, "experts": E, "experts_per_gpu": El, "d_model": d, "d_ff": f,
+                       "top_k": w["k"], "parallelism": f"ep{N}"},
+            "expert_tflops_upper_bound_per_gpu": flops / (ms / 1e3) / 1e12}
+    if prof:  # inference regime: gate / dispatch / combine against the HBM roofline
+        hbm = peaks()[0]
+        per = {k: v[0] / max(v[1], 1) for k, v in layers[0].handle.profile_read().items()}
+        layers[0].handle.profile(False)
+        cap, drops, kept = layers[0].handle.stats()
+        n_kept = int(kept.sum().item())
+        roof = {}
+        for name, parts in (("gate", ["gate_logits", "softmax_topk", "balance_loss"]), ("assign", ["assign"]),
+                            ("dispatch", ["dispatch"]), ("combine", ["combine"])):
+            if all(p_ in per for p_ in parts):
+                st_ms = sum(per[p_] for p_ in parts)
+                b = stage_bytes(name, T, d, E, w["k"], n_kept, T - n_kept)
+                roof[name] = {"ms": st_ms, "GB/s": b / (st_ms / 1e3) / 1e9, "frac": b / (st_ms / 1e3) / 1e9 / hbm}
+        line["stages_ms"] = {k: round(v, 4) for k, v in per.items()}
+        line["stage_roofline"] = roof
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if N > 1:
+        dist.destroy_process_group()
     return 0
 
 

@@ -57,7 +57,7 @@ typedef enum {
 
 typedef enum { MOE_TRAIN = 0, MOE_EVAL = 1 } moe_phase;                       /* routing.hpp:13 */
 typedef enum { MOE_PLAIN = 0, MOE_GROUPED = 1, MOE_RTS = 2 } moe_assignment;  /* routing.hpp:15 */
-typedef enum { MOE_F32 = 0, MOE_BF16 = 1 } moe_dtype;
+typedef enum { MOE_F32 = 0, MOE_BF16 = 1, MOE_F64 = 2 } moe_dtype;
 
 #define MOE_KDROPPED (-1) /* routing.hpp:34 kDropped */
 
@@ -134,6 +134,24 @@ moe_status moe_backward(moe_handle* h, const void* dy, float daux, void* dx, flo
  * MOE_UNSUPPORTED instead).  fp32 layers always use SIMT (the parity path). */
 typedef enum { MOE_GEMM_SIMT = 0, MOE_GEMM_TCGEN05 = 1 } moe_gemm_kind;
 moe_status moe_gemm_path(const moe_handle* h, int* path_out);
+
+/* ---- float64 path: the reference's own precision (dtype MOE_F64) --------
+ * Every tensor is float64, including gate_w, biases, aux, gate_prob and all
+ * gradients.  Forward reductions run in the reference's order with separately
+ * rounded products and sums (its x86-64 build has no FMA), so logits, the
+ * expert FFN, y and the decisions match routing.cpp / ops.cpp bit for bit up
+ * to glibc-vs-CUDA exp (<= 1 ulp in the probabilities); the backward follows
+ * the tape's closures to ~1e-15.  For f64 callers (the tape adapter,
+ * gradient checks at h = 1e-5); single rank.  accumulate != 0 adds into the
+ * gradient buffers (the tape's += semantics, tensor.cpp:31-36) instead of
+ * writing them. */
+moe_status moe_forward_f64(moe_handle* h, int64_t T, const double* x, const double* gate_w, const double* w1,
+                           const double* b1, const double* w2, const double* b2, int phase, uint64_t seed,
+                           const double* residual, double* y, double* aux, int32_t* expert_id, int32_t* slot,
+                           double* gate_prob);
+moe_status moe_backward_f64(moe_handle* h, const double* dy, double daux, double* dx, double* dgate_w,
+                            double* dw1, double* db1, double* dw2, double* db2, double* dresidual,
+                            int accumulate);
 
 /* Capacity and kept/dropped statistics of the last forward (host copy;
  * synchronises).  kept_per_expert may be NULL, else [E] int64. */

@@ -15,7 +15,7 @@ LIB_PATH = os.environ.get("MOE_B200_LIB") or os.path.join(HERE, "libmoe_b200.so"
 
 MOE_OK, MOE_SHAPE, MOE_CONFIG, MOE_NONFINITE, MOE_UNIFORM_SHAPE, MOE_INVALID_ARG = range(6)
 MOE_CUDA, MOE_NCCL, MOE_UNSUPPORTED = 6, 7, 8
-MOE_F32, MOE_BF16 = 0, 1
+MOE_F32, MOE_BF16, MOE_F64 = 0, 1, 2
 
 
 class moe_router_cfg(C.Structure):
@@ -86,6 +86,9 @@ _SIGS = {
     "moe_ep_traffic": (C.c_int, [H, VP, C.POINTER(C.c_double)]),
     "moe_ep_blob_size": (C.c_size_t, []),
     "moe_gemm_path": (C.c_int, [H, C.POINTER(C.c_int)]),
+    "moe_forward_f64": (C.c_int, [H, C.c_int64, VP, VP, VP, VP, VP, VP, C.c_int, C.c_uint64, VP, VP, VP,
+                                  VP, VP, VP]),
+    "moe_backward_f64": (C.c_int, [H, VP, C.c_double, VP, VP, VP, VP, VP, VP, VP, C.c_int]),
     "moe_workspace_bytes": (C.c_int, [H, C.POINTER(C.c_size_t)]),
     "moe_plan_validate": (C.c_int, [C.POINTER(moe_parallel_plan)]),
     "moe_plan_last_error": (C.c_char_p, []),

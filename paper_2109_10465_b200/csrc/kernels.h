@@ -254,3 +254,36 @@ namespace moe {
 // permute.cu: f64 checkpoint record -> fp32 / bf16 device tensor
 void launch_convert_f64(const double* src, int64_t n, bool bf16, void* dst, cudaStream_t st);
 }  // namespace moe
+
+namespace moe {
+// f64_layer.cu: the reference-precision (float64) path, see the file header
+void launch_mt64_raw_device(uint64_t seed, int64_t count, uint64_t* out, cudaStream_t st);
+void launch_f64_noise(uint64_t* buf, int64_t n, double lo, double hi, cudaStream_t st);
+void launch_f64_gate(const double* x, const double* noise, const double* gw, double* L, double* P, int64_t T,
+                     int d, int E, int K, int32_t* choice, double* gp, uint32_t* flags, cudaStream_t st);
+void launch_f64_balance(const double* P, const int32_t* choice, int64_t T, int E, int K, double alpha,
+                        double* aux, double* fval, cudaStream_t st);
+void launch_f64_weights(const double* gp, int64_t T, int E, int K, double* w, cudaStream_t st);
+void launch_f64_dispatch(const double* x, int64_t d, int E, int K, int cap_pad, const int32_t* row_src,
+                         const int32_t* kept, double* X, cudaStream_t st);
+void launch_f64_seg_gemm(const double* A, const double* W, double* C, const double* bias, const double* M,
+                         const int32_t* kept, int E, int cap_pad, int64_t K, int64_t N, bool nmajor, int epi,
+                         cudaStream_t st);
+void launch_f64_seg_wgrad(const double* A, const double* B, double* C, const int32_t* kept, int E, int cap_pad,
+                          int64_t M, int64_t N, bool accumulate, cudaStream_t st);
+void launch_f64_combine(const double* O, const double* res, int64_t T, int64_t d, int K, int cap_pad,
+                        const int32_t* choice, const int32_t* pos, const double* w, double* y,
+                        uint32_t* flags, cudaStream_t st);
+void launch_f64_combine_bwd(const double* dy, const double* O, int64_t T, int64_t d, int K, int cap_pad,
+                            const int32_t* choice, const int32_t* pos, const double* w, double* dO, double* dw,
+                            cudaStream_t st);
+void launch_f64_router_bwd(const double* P, const double* gp, const double* dw, const int32_t* choice,
+                           const double* fval, double daux, int64_t T, int E, int K, double* dL,
+                           cudaStream_t st);
+void launch_f64_gate_dw(const double* x, const double* noise, const double* dL, double* dW, int64_t T, int d,
+                        int E, bool accumulate, cudaStream_t st);
+void launch_f64_dx(const double* dL, const double* gw, const double* noise, const double* dX, const double* dy,
+                   int64_t T, int d, int E, int K, int cap_pad, const int32_t* choice, const int32_t* pos,
+                   bool residual_is_x, double* dx, double* dres, bool accumulate, cudaStream_t st);
+void launch_f64_acc_copy(const double* src, double* dst, int64_t n, bool accumulate, cudaStream_t st);
+}  // namespace moe

@@ -195,6 +195,9 @@ struct moe_handle {
     int64_t pf_req_count = 0, pf_count = 0;
     cudaEvent_t ev_pf = nullptr;
     DevMem db1_part;            // [rows/32][f] column sums from the dgrad2 epilogue
+    // float64 path (dtype MOE_F64): logits, probabilities, gate_prob, weights,
+    // noise, dL, dw [T*K], f_e [E]
+    DevMem f_logits, f_probs, f_gp, f_w, f_noise, f_dL, f_dw, f_fval;
     AssignScratch as{};
     std::vector<uint32_t> host_ord;
 
@@ -853,6 +856,96 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
     }
 }
 
+// ---------------------------------------------------------------------------
+// float64 path (f64_layer.cu): moe_layer_forward and its tape backward at the
+// reference's precision, for f64 callers (the tape adapter)
+// ---------------------------------------------------------------------------
+void forward_f64(moe_handle* h, int64_t T, const double* x, const double* gate_w, const double* w1,
+                 const double* b1, const double* w2, const double* b2, int phase, uint64_t seed,
+                 const double* residual, double* y, double* aux, int32_t* expert_id, int32_t* slot,
+                 double* gate_prob) {
+    require(T >= 1 && T <= h->Tmax, MOE_SHAPE, "moe_forward: token count outside [1, max_tokens]");
+    require(x && gate_w && w1 && b1 && w2 && b2 && y && aux, MOE_SHAPE, "moe_forward: null tensor");
+    require(phase == MOE_TRAIN || phase == MOE_EVAL, MOE_CONFIG, "moe_forward: bad phase");
+    cudaStream_t st = h->stream;
+    const int E = h->E, K = h->K;
+    const int d = static_cast<int>(h->d);
+    int mode;
+    set_geometry(h, T, phase, mode);
+    h->fwd_valid = false;
+    const bool jitter = phase == MOE_TRAIN && h->cfg.jitter_eps > 0.0;
+    double* noise = jitter ? h->f_noise.as<double>() : nullptr;
+    if (jitter) {  // routing.cpp:62-70: Rng(derive_seed(seed, "jitter")), row-major
+        launch_mt64_raw_device(derive_seed_tag(seed, "jitter"), T * h->d, h->f_noise.as<uint64_t>(), st);
+        launch_f64_noise(h->f_noise.as<uint64_t>(), T * h->d, 1.0 - h->cfg.jitter_eps, 1.0 + h->cfg.jitter_eps, st);
+    }
+    int32_t* choice = h->choice.as<int32_t>();
+    launch_f64_gate(x, noise, gate_w, h->f_logits.as<double>(), h->f_probs.as<double>(), T, d, E, K, choice,
+                    h->f_gp.as<double>(), h->flags.as<uint32_t>(), st);
+    launch_f64_balance(h->f_probs.as<double>(), choice, T, E, K, h->cfg.balance_coeff, aux,
+                       h->f_fval.as<double>(), st);
+    assign(h, T, choice, h->cap, mode, derive_seed_tag(seed, "assign"), h->slot.as<int32_t>());
+    launch_f64_weights(h->f_gp.as<double>(), T, E, K, h->f_w.as<double>(), st);
+    launch_f64_dispatch(x, h->d, E, K, h->cap_pad, h->row_src.as<int32_t>(), h->kept.as<int32_t>(),
+                        h->Xr.as<double>(), st);
+    const int32_t* kept = h->kept.as<int32_t>();
+    launch_f64_seg_gemm(h->Xr.as<double>(), w1, h->H.as<double>(), b1, nullptr, kept, E, h->cap_pad, h->d, h->f,
+                        true, 2, st);
+    launch_f64_seg_gemm(h->H.as<double>(), w2, h->Or.as<double>(), b2, nullptr, kept, E, h->cap_pad, h->f, h->d,
+                        true, 1, st);
+    launch_f64_combine(h->Or.as<double>(), residual ? residual : x, T, h->d, K, h->cap_pad, choice,
+                       h->pos.as<int32_t>(), h->f_w.as<double>(), y, h->flags.as<uint32_t>(), st);
+    const size_t nk = static_cast<size_t>(T * K);
+    if (expert_id) MOE_CUDA_CHECK(cudaMemcpyAsync(expert_id, choice, 4 * nk, cudaMemcpyDeviceToDevice, st));
+    if (slot) MOE_CUDA_CHECK(cudaMemcpyAsync(slot, h->slot.p, 4 * nk, cudaMemcpyDeviceToDevice, st));
+    if (gate_prob) MOE_CUDA_CHECK(cudaMemcpyAsync(gate_prob, h->f_gp.p, 8 * nk, cudaMemcpyDeviceToDevice, st));
+    h->T = T;
+    h->phase = phase;
+    h->mode = mode;
+    h->has_residual = residual != nullptr;
+    h->jitter_on = jitter;
+    h->x = x;
+    h->gate_w = reinterpret_cast<const float*>(gate_w);
+    h->w1 = w1;
+    h->w2 = w2;
+    h->fwd_valid = true;
+}
+
+void backward_f64(moe_handle* h, const double* dy, double daux, double* dx, double* dgate_w, double* dw1,
+                  double* db1, double* dw2, double* db2, double* dres, bool acc) {
+    require(h->fwd_valid, MOE_SHAPE, "moe_backward: no forward context on this handle");
+    require(dy && dx && dgate_w && dw1 && db1 && dw2 && db2, MOE_SHAPE, "moe_backward: null tensor");
+    require(!h->has_residual || dres, MOE_SHAPE, "moe_backward: dresidual required");
+    cudaStream_t st = h->stream;
+    const int64_t T = h->T;
+    const int E = h->E, K = h->K, d = static_cast<int>(h->d);
+    const int64_t f = h->f;
+    const double* x = static_cast<const double*>(h->x);
+    const double* gw = reinterpret_cast<const double*>(h->gate_w);
+    const double* w1 = static_cast<const double*>(h->w1);
+    const double* w2 = static_cast<const double*>(h->w2);
+    const double* noise = h->jitter_on ? h->f_noise.as<double>() : nullptr;
+    const int32_t* choice = h->choice.as<int32_t>();
+    const int32_t* pos = h->pos.as<int32_t>();
+    const int32_t* kept = h->kept.as<int32_t>();
+    const int cp = h->cap_pad;
+    launch_f64_combine_bwd(dy, h->Or.as<double>(), T, d, K, cp, choice, pos, h->f_w.as<double>(),
+                           h->dOr.as<double>(), h->f_dw.as<double>(), st);
+    launch_f64_router_bwd(h->f_probs.as<double>(), h->f_gp.as<double>(), h->f_dw.as<double>(), choice,
+                          h->f_fval.as<double>(), daux, T, E, K, h->f_dL.as<double>(), st);
+    launch_f64_seg_gemm(h->dOr.as<double>(), w2, h->dH.as<double>(), nullptr, h->H.as<double>(), kept, E, cp, d,
+                        f, false, 3, st);
+    launch_f64_seg_gemm(h->dH.as<double>(), w1, h->dXr.as<double>(), nullptr, nullptr, kept, E, cp, f, d, false,
+                        0, st);
+    launch_f64_seg_wgrad(h->H.as<double>(), h->dOr.as<double>(), dw2, kept, E, cp, f, d, acc, st);
+    launch_f64_seg_wgrad(h->Xr.as<double>(), h->dH.as<double>(), dw1, kept, E, cp, d, f, acc, st);
+    launch_f64_seg_wgrad(nullptr, h->dOr.as<double>(), db2, kept, E, cp, 1, d, acc, st);
+    launch_f64_seg_wgrad(nullptr, h->dH.as<double>(), db1, kept, E, cp, 1, f, acc, st);
+    launch_f64_gate_dw(x, noise, h->f_dL.as<double>(), dgate_w, T, d, E, acc, st);
+    launch_f64_dx(h->f_dL.as<double>(), gw, noise, h->dXr.as<double>(), dy, T, d, E, K, cp, choice, pos,
+                  !h->has_residual, dx, dres, acc, st);
+}
+
 void alloc_workspace(moe_handle* h) {
     const int E = h->E, K = h->K;
     const int64_t T = h->Tmax, d = h->d, f = h->f;
@@ -916,6 +1009,16 @@ void alloc_workspace(moe_handle* h) {
     // buffers start finite (zero) so padded tensor-core tiles never see NaN garbage
     for (DevMem* m : {&h->Xr, &h->H, &h->Or, &h->dOr, &h->dH, &h->dXr})
         MOE_CUDA_CHECK(cudaMemset(m->p, 0, m->bytes));
+    if (es == 8) {
+        h->f_logits.alloc(8 * T * E);
+        h->f_probs.alloc(8 * T * E);
+        h->f_gp.alloc(8 * T * K);
+        h->f_w.alloc(8 * T * K);
+        h->f_noise.alloc(8 * T * d);
+        h->f_dL.alloc(8 * T * E);
+        h->f_dw.alloc(8 * T * K);
+        h->f_fval.alloc(8 * E);
+    }
     h->dL.alloc(4 * T * E);
     h->dxg.alloc(4 * T * d);
     h->dwg_part.alloc(4 * 16 * d * E);
@@ -986,7 +1089,10 @@ moe_status moe_create(const moe_router_cfg* cfg, const moe_layer_dims* dims, moe
         if (st) throw Status(st, why);
         require(dims->max_tokens >= 1 && dims->d_model >= 1 && dims->d_ff >= 1, MOE_SHAPE,
                 "moe_create: dims must be positive");
-        require(dims->dtype == MOE_F32 || dims->dtype == MOE_BF16, MOE_CONFIG, "moe_create: dtype");
+        require(dims->dtype == MOE_F32 || dims->dtype == MOE_BF16 || dims->dtype == MOE_F64, MOE_CONFIG,
+                "moe_create: dtype");
+        require(dims->dtype != MOE_F64 || std::max(1, dims->ep_size) == 1, MOE_UNSUPPORTED,
+                "moe_create: the float64 path is single-rank");
         const int ep = std::max(1, dims->ep_size);
         require(cfg->num_experts % ep == 0, MOE_CONFIG,
                 "simulate: expert_parallel must divide num_experts");
@@ -1002,7 +1108,7 @@ moe_status moe_create(const moe_router_cfg* cfg, const moe_layer_dims* dims, moe
         h->Tmax = dims->max_tokens;
         h->d = dims->d_model;
         h->f = dims->d_ff;
-        h->esz = dims->dtype == MOE_BF16 ? 2 : 4;
+        h->esz = dims->dtype == MOE_BF16 ? 2 : dims->dtype == MOE_F64 ? 8 : 4;
         {
             struct Count {  // RAII: never leave the counter pointing at a failed handle
                 explicit Count(size_t* c) { g_ws_counter = c; }
@@ -1146,6 +1252,7 @@ moe_status moe_forward(moe_handle* h, int64_t T, const void* x, const float* gat
                        int32_t* expert_id, int32_t* slot, float* gate_prob) {
     if (!h) return MOE_SHAPE;
     return guarded(h, [&] {
+        require(h->esz != 8, MOE_CONFIG, "moe_forward: float64 handle, use moe_forward_f64");
         if (h->esz == 2) {
             using B = __nv_bfloat16;
             forward_impl<B>(h, T, static_cast<const B*>(x), gate_w, static_cast<const B*>(w1), b1,
@@ -1165,6 +1272,7 @@ moe_status moe_backward(moe_handle* h, const void* dy, float daux, void* dx, flo
                         void* dw1, float* db1, void* dw2, float* db2, void* dresidual) {
     if (!h) return MOE_SHAPE;
     return guarded(h, [&] {
+        require(h->esz != 8, MOE_CONFIG, "moe_backward: float64 handle, use moe_backward_f64");
         if (h->esz == 2) {
             using B = __nv_bfloat16;
             backward_impl<B>(h, static_cast<const B*>(dy), daux, static_cast<B*>(dx), dgate_w,
@@ -1175,6 +1283,27 @@ moe_status moe_backward(moe_handle* h, const void* dy, float daux, void* dx, flo
                                  dgate_w, static_cast<float*>(dw1), db1, static_cast<float*>(dw2),
                                  db2, static_cast<float*>(dresidual));
         }
+    });
+}
+
+moe_status moe_forward_f64(moe_handle* h, int64_t T, const double* x, const double* gate_w, const double* w1,
+                           const double* b1, const double* w2, const double* b2, int phase, uint64_t seed,
+                           const double* residual, double* y, double* aux, int32_t* expert_id, int32_t* slot,
+                           double* gate_prob) {
+    if (!h) return MOE_SHAPE;
+    return guarded(h, [&] {
+        require(h->esz == 8, MOE_CONFIG, "moe_forward_f64: handle was not created with MOE_F64");
+        forward_f64(h, T, x, gate_w, w1, b1, w2, b2, phase, seed, residual, y, aux, expert_id, slot, gate_prob);
+    });
+}
+
+moe_status moe_backward_f64(moe_handle* h, const double* dy, double daux, double* dx, double* dgate_w,
+                            double* dw1, double* db1, double* dw2, double* db2, double* dresidual,
+                            int accumulate) {
+    if (!h) return MOE_SHAPE;
+    return guarded(h, [&] {
+        require(h->esz == 8, MOE_CONFIG, "moe_backward_f64: handle was not created with MOE_F64");
+        backward_f64(h, dy, daux, dx, dgate_w, dw1, db1, dw2, db2, dresidual, accumulate != 0);
     });
 }
 

@@ -153,6 +153,8 @@ def _dtype_code(t: torch.dtype) -> int:
         return L.MOE_F32
     if t == torch.bfloat16:
         return L.MOE_BF16
+    if t == torch.float64:
+        return L.MOE_F64
     raise ConfigError(f"unsupported activation dtype {t}")
 
 
@@ -507,9 +509,10 @@ class MoeLayer:
             raise ShapeError("moe_layer_forward: expert count does not match config")
         if p.w1.dtype != self.dtype or p.w2.dtype != self.dtype:
             raise ShapeError("moe_layer_forward: expert weight dtype does not match the layer")
+        side = torch.float64 if self.dtype == torch.float64 else torch.float32
         for name in ("gate_w", "b1", "b2"):
-            if getattr(p, name).dtype != torch.float32:
-                raise ShapeError(f"moe_layer_forward: {name} must be float32")
+            if getattr(p, name).dtype != side:
+                raise ShapeError(f"moe_layer_forward: {name} must be {side}")
         for name in ("gate_w", "w1", "b1", "w2", "b2"):
             _dense(getattr(p, name), device, name)
 
@@ -530,16 +533,18 @@ class MoeLayer:
         K = self.cfg.top_k
         dev = x.device
         self.handle.bind_stream()
+        f64 = self.dtype == torch.float64
+        side = torch.float64 if f64 else torch.float32
         y = torch.empty_like(x) if y is None else y
-        aux = torch.empty(1, device=dev, dtype=torch.float32) if aux is None else aux
+        aux = torch.empty(1, device=dev, dtype=side) if aux is None else aux
         eid = slot = gp = None
         if decision:
             eid = torch.empty(T * K, device=dev, dtype=torch.int32)
             slot = torch.empty(T * K, device=dev, dtype=torch.int32)
-            gp = torch.empty(T * K, device=dev, dtype=torch.float32)
-        _check(L.load().moe_forward(self.handle.h, T, _p(x), _p(params.gate_w), _p(params.w1),
-                                    _p(params.b1), _p(params.w2), _p(params.b2), int(phase), seed,
-                                    _p(residual), _p(y), _p(aux), _p(eid), _p(slot), _p(gp)),
+            gp = torch.empty(T * K, device=dev, dtype=side)
+        fwd = L.load().moe_forward_f64 if f64 else L.load().moe_forward
+        _check(fwd(self.handle.h, T, _p(x), _p(params.gate_w), _p(params.w1), _p(params.b1), _p(params.w2),
+                   _p(params.b2), int(phase), seed, _p(residual), _p(y), _p(aux), _p(eid), _p(slot), _p(gp)),
                self.handle.h)
         if check:
             self.handle.check()
@@ -556,25 +561,37 @@ class MoeLayer:
         self._gen += 1
         return y, aux, dec
 
-    def backward(self, dy, daux: float = 1.0, check: bool = True, grads=None):
+    def backward(self, dy, daux: float = 1.0, check: bool = True, grads=None, accumulate: bool = False):
         params, has_res, x = self._saved[:3]
         if tuple(dy.shape) != tuple(x.shape) or dy.dtype != self.dtype:
             raise ShapeError("moe_layer_backward: dy must be [T, d_model] of the layer dtype")
         El, d, f = self.n_local, self.d_model, self.d_ff
         dev = dy.device
+        f64 = self.dtype == torch.float64
+        side = torch.float64 if f64 else torch.float32
         if grads is None:
             grads = dict(dx=torch.empty_like(dy),
                          dgate_w=torch.empty_like(params.gate_w),
                          dw1=torch.empty(El, d, f, device=dev, dtype=self.dtype),
-                         db1=torch.empty(El, f, device=dev, dtype=torch.float32),
+                         db1=torch.empty(El, f, device=dev, dtype=side),
                          dw2=torch.empty(El, f, d, device=dev, dtype=self.dtype),
-                         db2=torch.empty(El, d, device=dev, dtype=torch.float32),
+                         db2=torch.empty(El, d, device=dev, dtype=side),
                          dresidual=torch.empty_like(dy) if has_res else None)
+            accumulate = False
         g = grads
         self.handle.bind_stream()
-        _check(L.load().moe_backward(self.handle.h, _p(dy.contiguous()), float(daux), _p(g["dx"]),
-                                     _p(g["dgate_w"]), _p(g["dw1"]), _p(g["db1"]), _p(g["dw2"]),
-                                     _p(g["db2"]), _p(g.get("dresidual"))), self.handle.h)
+        if f64:
+            _check(L.load().moe_backward_f64(self.handle.h, _p(dy.contiguous()), float(daux), _p(g["dx"]),
+                                             _p(g["dgate_w"]), _p(g["dw1"]), _p(g["db1"]), _p(g["dw2"]),
+                                             _p(g["db2"]), _p(g.get("dresidual")), int(bool(accumulate))),
+                   self.handle.h)
+        else:
+            if accumulate:
+                raise ConfigError("moe_layer_backward: accumulate needs the float64 path or "
+                                  "moe_backward_ex")
+            _check(L.load().moe_backward(self.handle.h, _p(dy.contiguous()), float(daux), _p(g["dx"]),
+                                         _p(g["dgate_w"]), _p(g["dw1"]), _p(g["db1"]), _p(g["dw2"]),
+                                         _p(g["db2"]), _p(g.get("dresidual"))), self.handle.h)
         if check:
             self.handle.check()
         return grads
