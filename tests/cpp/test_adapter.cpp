@@ -170,10 +170,79 @@ static void gpu_cases() {
     }
 }
 
+// The per-stage mirrors of routing.hpp:60-118 on the device, against the
+// reference's known answers (test_routing.cpp, SURVEY §8c KATs).
+static void stage_cases() {
+    {  // test_routing.cpp:53-61: equal logits -> P = [.5, .5], tie to expert 0
+        RouterConfig cfg;
+        cfg.num_experts = 2;
+        const int64_t T = 3, d = 2;
+        std::vector<float> x = {1, 2, -1, 0.5f, 3, -2}, gw = {1, 1, -1, -1};  // columns equal
+        DeviceArray<float> xd(x), gwd(gw);
+        GateResult g = gate_forward(xd.data(), T, d, MOE_F32, gwd.data(), cfg, Phase::kEval, 0);
+        auto P = g.probs.to_host();
+        for (float v : P) CHECK(v == 0.5f);
+        for (int32_t c : g.choice) CHECK(c == 0);
+        CHECK(g.gate_prob.size() == 1 && g.gate_prob[0].to_host()[1] == 0.5f);
+    }
+    {  // test_routing.cpp:118-125: plain, all to expert 0, cap 2 -> [0, 1, D, D]
+        RoutingDecision d = assign_plain({0, 0, 0, 0}, 1, 2);
+        CHECK((d.slot == std::vector<int32_t>{0, 1, kDropped, kDropped}));
+        // k-major top-2: t2's first choice dropped, its second kept
+        RoutingDecision k2 = assign_plain({0, 1, 0, 1, 0, 2}, 3, 2, 2);
+        CHECK((k2.slot == std::vector<int32_t>{0, 0, 1, 1, kDropped, 0}));
+        // grouped: capacity G * ceil(cap / G), per-group bases
+        RoutingDecision g = assign_grouped({0, 0, 0, 0, 0, 0}, 1, 3, 2);
+        CHECK(g.capacity == 4);
+        CHECK((g.slot == std::vector<int32_t>{0, 1, kDropped, 2, 3, kDropped}));
+        CHECK(throws<ConfigError>([] { (void)assign_grouped({0, 0, 0}, 1, 2, 2); }));
+        CHECK(throws<ConfigError>([] { (void)assign_plain({0, 3}, 2, 2); }));
+        // RTS: deterministic, never over capacity, no drops when capacity suffices
+        std::vector<int32_t> ch(32, 0);
+        CHECK(assign_rts(ch, 1, 8, 777).slot == assign_rts(ch, 1, 8, 777).slot);
+        CHECK(assign_rts(ch, 1, 8, 777).drop_count() == 24);
+        CHECK(assign_rts({0, 1, 0, 1, 2, 2}, 3, 2, 5).drop_count() == 0);
+        RouterConfig cfg;
+        cfg.num_experts = 1;
+        cfg.assignment_mode = AssignmentMode::kRts;
+        RoutingDecision ev = make_assignment(ch, 32, cfg, Phase::kEval, 1);  // eval -> plain
+        CHECK(ev.slot == assign_plain(ch, 1, 64).slot);
+    }
+    {  // dispatch / combine round trip (test_routing.cpp:287-314) + exact-zero rows
+        const int64_t T = 6, d = 4;
+        std::vector<float> x(T * d);
+        for (size_t i = 0; i < x.size(); ++i) x[i] = 0.25f * static_cast<float>(i) - 2.f;
+        RoutingDecision dec = assign_plain({0, 1, 0, 1, 0, 2}, 3, 2);
+        DeviceArray<float> xd(x);
+        DispatchBuffer b = dispatch(xd.data(), T, d, MOE_F32, dec);
+        auto occ = b.occupancy.to_host();
+        auto buf = b.data.to_host();
+        const float* bf = reinterpret_cast<const float*>(buf.data());
+        for (int r = 0; r < 6; ++r)
+            if (!occ[r])
+                for (int j = 0; j < d; ++j) CHECK(bf[r * d + j] == 0.f);
+        DeviceArray<float> w(std::vector<float>(T, 1.f));
+        DeviceArray<std::uint8_t> y = combine(b.data.data(), d, MOE_F32, dec, xd.data(), w.data());
+        auto yh = y.to_host();
+        CHECK(std::memcmp(yh.data(), x.data(), sizeof(float) * x.size()) == 0);
+    }
+    {  // balance loss closed form: uniform routing -> alpha (test_routing.cpp:368-381)
+        const int64_t T = 4;
+        RoutingDecision dec = assign_plain({0, 1, 2, 3}, 4, 1);
+        DeviceArray<float> P(std::vector<float>(T * 4, 0.25f));
+        CHECK(std::abs(balance_loss(P.data(), dec, 0.01) - 0.01f) < 1e-7f);
+        DeviceArray<float> bad(std::vector<float>(T * 4, 0.3f));
+        CHECK(throws<std::invalid_argument>([&] { (void)balance_loss(bad.data(), dec, 0.01); }));
+    }
+}
+
 int main(int argc, char** argv) {
     const bool gpu = argc > 1 && std::strcmp(argv[1], "gpu") == 0;
     host_cases();
-    if (gpu) gpu_cases();
+    if (gpu) {
+        gpu_cases();
+        stage_cases();
+    }
     std::printf("%s %s\n", g_fail ? "FAIL" : "OK", gpu ? "host+gpu" : "host");
     return g_fail ? 1 : 0;
 }
