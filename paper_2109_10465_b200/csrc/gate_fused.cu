@@ -1,0 +1,442 @@
+// gate_fused.cu — the fused gate of the bf16 path: logits, softmax, top-1 /
+// top-2, balance-loss partials and the balance-loss finalize in ONE kernel
+// (routing.cpp:51-101 gate_forward + routing.cpp:348-374 balance_loss).
+//
+// A cluster of two CTAs owns 128 tokens; CTA r reduces half of d:
+//
+//   warp 0      TMA producer: raw x (bf16) and jitter (fp32) tiles [128 x 32]
+//               plus the pre-split tf32 hi / lo halves of Wg^T [64 x 32]
+//               (128B-swizzled, read by the MMA in place) into a 3-deep ring
+//   warps 2..5  transform: g = x * noise, 3xTF32 split g = hi + lo, written
+//               into the 128B-swizzled K-major A operand (2-deep ring)
+//   warp 1      MMA: tcgen05.mma kind::tf32, M=128 N=64 K=8, hi*hi + hi*lo +
+//               lo*hi into four TMEM accumulators (one per K=8 sub-step,
+//               summed in fixed order: fp32-FMA accuracy at d = 2048)
+//   epilogue    the two CTAs swap their partial logits for each other's 64
+//               rows through distributed shared memory (st.shared::cluster),
+//               then each thread owns one token row: softmax (ops.cpp:77-90),
+//               top-1 / top-2 with the reference's tie rules (routing.cpp:
+//               77-92), probabilities / choices / gate_prob stores, and the
+//               per-64-row column sums and first-choice counts of the balance
+//               loss; the last CTA to finish reduces them in fixed order
+//               (f64) into aux and the gradient coefficients f_e / T.
+//
+// No logits or split-K partials go to HBM: the kernel reads x (and the
+// jitter) once and writes P, the decision and the small balance partials.
+#include <cuda.h>
+
+#include "common.cuh"
+#include "gemm_tc.h"
+#include "kernels.h"
+#include "tc_ptx.cuh"
+
+namespace moe {
+namespace gf {
+
+using namespace tc;
+
+constexpr int E = 64;              // experts (TMEM columns per accumulator)
+constexpr int BM = 128;            // tokens per cluster
+constexpr int BK = 32;             // fp32 K elements per step (one 128 B swizzle row)
+constexpr int kRaw = 3;            // raw ring depth
+constexpr int kOp = 2;             // A-operand ring depth
+constexpr int kNAcc = 4;           // TMEM accumulators
+constexpr int kThreads = 192;
+constexpr uint32_t kRawX = BM * BK * 2;        //  8 KB bf16 x
+constexpr uint32_t kRawN = BM * BK * 4;        // 16 KB fp32 noise
+constexpr uint32_t kRawB = E * 128;            //  8 KB per hi / lo
+constexpr uint32_t kRawStage = kRawX + kRawN + 2 * kRawB;   // 40 KB
+constexpr uint32_t kOpStage = 2 * BM * 128;                  // 32 KB (A hi, A lo)
+constexpr uint32_t kRecv = 64 * E * 4;                       // 16 KB: peer's partials for my rows
+constexpr uint32_t kSmem = 1024 + kRaw * kRawStage + kOp * kOpStage + kRecv + 512;
+
+struct __align__(64) Params {
+    CUtensorMap tmX, tmN, tmBh, tmBl;
+    float* probs;
+    int32_t* choice;
+    float* gate_prob;
+    float* colsum_part;   // [parts][E], part = 64 tokens
+    int32_t* count_part;  // [parts][E]
+    uint32_t* flags;
+    float* aux;
+    float* fcoef;
+    int32_t* fcount;
+    double* term;         // [E]
+    unsigned* done;
+    double alpha;
+    int64_t T;
+    int d, K, nparts, has_noise;
+};
+
+__device__ __forceinline__ float tf32_rna(float v) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+    return __uint_as_float(r);
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t map_peer(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster_v4(uint32_t addr, float a, float b, float c, float d) {
+    asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c),
+                 "f"(d)
+                 : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t swz(int r, int c) { return r * 128 + ((c ^ (r & 7)) << 4); }
+
+__global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant__ Params p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* raw = sm;
+    uint8_t* op = raw + kRaw * kRawStage;
+    float* recv = reinterpret_cast<float*>(op + kOp * kOpStage);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(recv) + kRecv);
+    uint64_t* raw_full = bars;
+    uint64_t* raw_empty = raw_full + kRaw;
+    uint64_t* op_full = raw_empty + kRaw;
+    uint64_t* op_empty = op_full + kOp;
+    uint64_t* acc_full = op_empty + kOp;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(acc_full + 1);
+    __shared__ int s_last;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const int64_t t0 = static_cast<int64_t>(blockIdx.x >> 1) * BM;
+    const int kspan = p.d / 2;
+    const int kbase = static_cast<int>(rank) * kspan;
+    const int nsteps = kspan / BK;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kRaw; ++i) {
+            mbar_init(&raw_full[i], 1);
+            mbar_init(&raw_empty[i], 4 + 1);  // 4 transform warps + the MMA commit (B read)
+        }
+        for (int i = 0; i < kOp; ++i) {
+            mbar_init(&op_full[i], 4);
+            mbar_init(&op_empty[i], 1);
+        }
+        mbar_init(acc_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        prefetch_tmap(&p.tmX);
+        prefetch_tmap(&p.tmN);
+        prefetch_tmap(&p.tmBh);
+        prefetch_tmap(&p.tmBl);
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                     "r"(kNAcc * E));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    pdl_wait();  // x, the jitter stream and the split gate weights come from predecessors
+    pdl_trigger();
+
+    if (warp == 0) {
+        // ---------------- TMA producer
+        if (lane == 0) {
+            const uint32_t bytes = kRawX + (p.has_noise ? kRawN : 0) + 2 * kRawB;
+            for (int s = 0; s < nsteps; ++s) {
+                const int rs = s % kRaw;
+                if (s >= kRaw) mbar_wait(&raw_empty[rs], ((s / kRaw) - 1) & 1);
+                uint8_t* st = raw + rs * kRawStage;
+                const int k0 = kbase + s * BK;
+                mbar_expect_tx(&raw_full[rs], bytes);
+                tma_load_2d(&p.tmX, &raw_full[rs], st, k0, static_cast<int32_t>(t0));
+                if (p.has_noise) tma_load_2d(&p.tmN, &raw_full[rs], st + kRawX, k0, static_cast<int32_t>(t0));
+                tma_load_2d(&p.tmBh, &raw_full[rs], st + kRawX + kRawN, k0, 0);
+                tma_load_2d(&p.tmBl, &raw_full[rs], st + kRawX + kRawN + kRawB, k0, 0);
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idesc = make_idesc_tf32(BM, E, 0, 0);
+            for (int s = 0; s < nsteps; ++s) {
+                const int rs = s % kRaw, os = s % kOp;
+                mbar_wait(&raw_full[rs], (s / kRaw) & 1);
+                mbar_wait(&op_full[os], (s / kOp) & 1);
+                tc_fence_after();
+                const uint32_t a = smem_u32(op + os * kOpStage);
+                const uint32_t b = smem_u32(raw + rs * kRawStage + kRawX + kRawN);
+#pragma unroll
+                for (int kk = 0; kk < BK / 8; ++kk) {
+                    const uint64_t ah = sdesc(a + kk * 32, 16, 1024);
+                    const uint64_t al = sdesc(a + BM * 128 + kk * 32, 16, 1024);
+                    const uint64_t bh = sdesc(b + kk * 32, 16, 1024);
+                    const uint64_t bl = sdesc(b + kRawB + kk * 32, 16, 1024);
+                    const uint32_t acc = tmem + kk * E;
+                    tc_mma_tf32(acc, ah, bh, idesc, s ? 1u : 0u);
+                    tc_mma_tf32(acc, ah, bl, idesc, 1u);
+                    tc_mma_tf32(acc, al, bh, idesc, 1u);
+                }
+                tc_commit(&op_empty[os]);   // A operand stage free
+                tc_commit(&raw_empty[rs]);  // B halves (in the raw stage) read
+            }
+            tc_commit(acc_full);
+        }
+    } else {
+        // ---------------- transform: g = x * noise -> tf32 hi / lo, swizzled K-major
+        const int tw = warp - 2;
+        const int c = lane & 7;
+        for (int s = 0; s < nsteps; ++s) {
+            const int rs = s % kRaw, os = s % kOp;
+            mbar_wait(&raw_full[rs], (s / kRaw) & 1);
+            if (s >= kOp) mbar_wait(&op_empty[os], ((s / kOp) - 1) & 1);
+            const uint8_t* st = raw + rs * kRawStage;
+            const uint32_t ahi = smem_u32(op + os * kOpStage);
+            const uint32_t alo = ahi + BM * 128;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int r = tw * 32 + (lane >> 3) + 4 * j;
+                const uint2 xv = *reinterpret_cast<const uint2*>(st + r * 64 + c * 8);
+                float g[4] = {__uint_as_float(xv.x << 16), __uint_as_float(xv.x & 0xffff0000u),
+                              __uint_as_float(xv.y << 16), __uint_as_float(xv.y & 0xffff0000u)};
+                if (p.has_noise) {
+                    const float4 nv = *reinterpret_cast<const float4*>(st + kRawX + r * 128 + c * 16);
+                    g[0] *= nv.x; g[1] *= nv.y; g[2] *= nv.z; g[3] *= nv.w;
+                }
+                float h[4], l[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    h[q] = tf32_rna(g[q]);
+                    l[q] = tf32_rna(g[q] - h[q]);
+                }
+                const uint32_t off = swz(r, c);
+                sts128(ahi + off, make_uint4(__float_as_uint(h[0]), __float_as_uint(h[1]), __float_as_uint(h[2]),
+                                             __float_as_uint(h[3])));
+                sts128(alo + off, make_uint4(__float_as_uint(l[0]), __float_as_uint(l[1]), __float_as_uint(l[2]),
+                                             __float_as_uint(l[3])));
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&op_full[os]);
+                mbar_arrive(&raw_empty[rs]);
+            }
+        }
+    }
+
+    // ---------------- epilogue
+    float L[E];
+    const int q = warp & 3;                 // TMEM lane quarter of this warp
+    const int row = q * 32 + lane;          // token row inside the cluster tile
+    const bool mine = (row >> 6) == static_cast<int>(rank);
+    if (warp >= 2) {
+        mbar_wait(acc_full, 0);
+        tc_fence_after();
+#pragma unroll
+        for (int a = 0; a < kNAcc; ++a) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                uint32_t v[32];
+                tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + a * E + h * 32, v);
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    L[h * 32 + j] = a ? L[h * 32 + j] + __uint_as_float(v[j]) : __uint_as_float(v[j]);
+            }
+        }
+        if (!mine) {  // the peer CTA owns this row: ship my half-d partial logits there
+            const uint32_t dst = map_peer(smem_u32(recv + (row & 63) * E), rank ^ 1u);
+#pragma unroll
+            for (int j = 0; j < E; j += 4) st_cluster_v4(dst + 4 * j, L[j], L[j + 1], L[j + 2], L[j + 3]);
+        }
+    }
+    __syncwarp();    // producer / MMA lanes rejoin their warps before the aligned cluster barrier
+    cluster_sync();  // every partial has landed; both CTAs stay resident until here
+    // owner warps: logits = own half + peer half, then the row's routing
+    float* sP = reinterpret_cast<float*>(op);                // [64][E + 1] after the loop
+    int32_t* sC = reinterpret_cast<int32_t*>(sP + 64 * (E + 1));
+    const int64_t t = t0 + row;
+    uint32_t flag = 0;
+    if (warp >= 2 && mine) {
+        const float* pr = recv + (row & 63) * E;
+#pragma unroll
+        for (int j = 0; j < E; ++j) L[j] += pr[j];
+        const int lr = row & 63;
+        if (t < p.T) {
+            float mx = L[0];
+#pragma unroll
+            for (int j = 1; j < E; ++j) mx = fmaxf(mx, L[j]);
+            float s = 0.f;
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                L[j] = expf(L[j] - mx);  // L now holds exp
+                s += L[j];
+            }
+            float psum = 0.f;
+            int c0 = 0;
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                const float pj = L[j] / s;
+                if (!finite_f(pj)) flag |= MOE_FLAG_NONFINITE_DEV;
+                L[j] = pj;
+                psum += pj;
+                if (j && pj > L[c0]) c0 = j;  // strict >, lowest index wins
+            }
+            if (fabsf(psum - 1.0f) > kProbRowTol) flag |= MOE_FLAG_PROB_ROWS_DEV;
+            float4* po = reinterpret_cast<float4*>(p.probs + t * E);
+#pragma unroll
+            for (int j = 0; j < E; j += 4) po[j / 4] = make_float4(L[j], L[j + 1], L[j + 2], L[j + 3]);
+            p.choice[t * p.K] = c0;
+            p.gate_prob[t * p.K] = L[c0];
+            if (p.K == 2) {
+                int c1 = c0 == 0 ? 1 : 0;
+#pragma unroll
+                for (int j = 0; j < E; ++j)
+                    if (j != c0 && L[j] > L[c1]) c1 = j;
+                p.choice[t * p.K + 1] = c1;
+                p.gate_prob[t * p.K + 1] = L[c1];
+            }
+#pragma unroll
+            for (int j = 0; j < E; ++j) sP[lr * (E + 1) + j] = L[j];
+            sC[lr] = c0;
+        } else {
+#pragma unroll
+            for (int j = 0; j < E; ++j) sP[lr * (E + 1) + j] = 0.f;
+            sC[lr] = -1;
+        }
+    }
+    // the two owner warps of this CTA: column sums / first-choice counts of their 64 rows
+    const bool owner_warp = warp >= 2 && ((q >> 1) == static_cast<int>(rank));
+    if (owner_warp) {
+        asm volatile("bar.sync 1, 64;" ::: "memory");
+        const int j = row & 63;  // expert
+        float cs = 0.f;
+        int cnt = 0;
+        for (int r = 0; r < 64; ++r) {
+            cs += sP[r * (E + 1) + j];
+            cnt += sC[r] == j;
+        }
+        const int part = static_cast<int>((t0 >> 6) + rank);
+        if (part < p.nparts) {
+            p.colsum_part[static_cast<int64_t>(part) * E + j] = cs;
+            p.count_part[static_cast<int64_t>(part) * E + j] = cnt;
+        }
+        flag = __reduce_or_sync(0xffffffffu, flag);
+        if (lane == 0 && flag) atomicOr(p.flags, flag);
+        __threadfence();
+        asm volatile("bar.sync 1, 64;" ::: "memory");
+        if (row == static_cast<int>(rank) * 64) s_last = atomicAdd(p.done, 1u) == gridDim.x - 1;
+        asm volatile("bar.sync 1, 64;" ::: "memory");
+        if (s_last) {
+            // balance_loss finalize (routing.cpp:364-373): f_e = alpha E cnt_e / T over
+            // first choices (drops included), aux = sum_e mean_t P[t,e] f_e; fixed order
+            __threadfence();
+            double csum = 0.0;
+            long long ctot = 0;
+            for (int pp = 0; pp < p.nparts; ++pp) {
+                csum += static_cast<double>(reinterpret_cast<volatile float*>(p.colsum_part)[pp * E + j]);
+                ctot += reinterpret_cast<volatile int32_t*>(p.count_part)[pp * E + j];
+            }
+            const double f = p.alpha * static_cast<double>(E) * static_cast<double>(ctot) / static_cast<double>(p.T);
+            p.fcoef[j] = static_cast<float>(f / static_cast<double>(p.T));
+            p.fcount[j] = static_cast<int32_t>(ctot);
+            p.term[j] = csum / static_cast<double>(p.T) * f;
+            asm volatile("bar.sync 1, 64;" ::: "memory");
+            if (j == 0) {
+                double a = 0.0;
+                for (int e = 0; e < E; ++e) a += reinterpret_cast<volatile double*>(p.term)[e];
+                *p.aux = static_cast<float>(a);
+                *p.done = 0u;  // ready for the next call
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kNAcc * E));
+    }
+}
+
+// Wg [d][E] -> Wg^T split into tf32 hi / lo halves [E][d] (the B operand)
+__global__ void split_kernel(const float* __restrict__ wg, float* __restrict__ hi, float* __restrict__ lo, int d) {
+    pdl_wait();
+    pdl_trigger();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= d * E) return;
+    const int j = i / E, e = i % E;
+    const float v = wg[i];
+    const float h = tf32_rna(v);
+    hi[static_cast<int64_t>(e) * d + j] = h;
+    lo[static_cast<int64_t>(e) * d + j] = tf32_rna(v - h);
+}
+
+}  // namespace gf
+
+bool gate_fused_ok(int d, int E) { return E == gf::E && d % (2 * gf::BK) == 0 && d >= 2 * gf::BK; }
+
+void launch_gate_split(const float* wg, float* wsplit, int d, cudaStream_t st) {
+    launch_pdl(gf::split_kernel, dim3(static_cast<unsigned>(ceil_div(static_cast<int64_t>(d) * gf::E, 256))),
+               dim3(256), 0, st, wg, wsplit, wsplit + static_cast<int64_t>(d) * gf::E, d);
+}
+
+int gate_fused_parts(int64_t T) { return static_cast<int>(ceil_div(T, static_cast<int64_t>(64))); }
+
+void launch_gate_fused(const __nv_bfloat16* x, const float* noise, const float* wsplit, int64_t T, int d, int K,
+                       double alpha, float* probs, int32_t* choice, float* gate_prob, float* colsum_part,
+                       int32_t* count_part, uint32_t* flags, float* aux, float* fcoef, int32_t* fcount,
+                       double* term, unsigned* done, cudaStream_t st) {
+    using namespace gf;
+    static bool attr = false;
+    if (!attr) {
+        MOE_CUDA_CHECK(cudaFuncSetAttribute(gate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(kSmem)));
+        attr = true;
+    }
+    Params p{};
+    p.tmX = tc::make_map_2d(x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, T, d, BK, BM, false);
+    p.tmN = tc::make_map_2d(noise ? noise : wsplit, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, noise ? T : E, d, BK,
+                            noise ? BM : E, false);
+    p.tmBh = tc::make_map_2d(wsplit, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, E, d, BK, E, true);
+    p.tmBl = tc::make_map_2d(wsplit + static_cast<int64_t>(d) * E, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, E, d, BK, E,
+                             true);
+    p.probs = probs;
+    p.choice = choice;
+    p.gate_prob = gate_prob;
+    p.colsum_part = colsum_part;
+    p.count_part = count_part;
+    p.flags = flags;
+    p.aux = aux;
+    p.fcoef = fcoef;
+    p.fcount = fcount;
+    p.term = term;
+    p.done = done;
+    p.alpha = alpha;
+    p.T = T;
+    p.d = d;
+    p.K = K;
+    p.nparts = gate_fused_parts(T);
+    p.has_noise = noise != nullptr;
+    const unsigned tiles = static_cast<unsigned>(ceil_div(T, static_cast<int64_t>(BM)));
+    cudaLaunchAttribute attrs[2];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = 2;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[1].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * tiles);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmem;
+    cfg.stream = st;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 2;
+    MOE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gate_kernel, p));
+    count_launch();
+}
+
+}  // namespace moe

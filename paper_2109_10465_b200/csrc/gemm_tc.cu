@@ -859,6 +859,22 @@ CUtensorMap make_map(const void* base, int64_t rows, int64_t cols, int box_cols,
     return m;
 }
 
+// general 2D map: [rows, cols] row-major of `esz`-byte elements, box {box_cols, box_rows}
+CUtensorMap make_map_2d(const void* base, CUtensorMapDataType dt, int esz, int64_t rows, int64_t cols,
+                        int box_cols, int box_rows, bool swizzle128) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols * esz)};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = get_encode()(&m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Status(6, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return m;
+}
+
 int num_sms() {
     static int n = 0;
     if (!n) {

@@ -287,3 +287,16 @@ void launch_f64_dx(const double* dL, const double* gw, const double* noise, cons
                    bool residual_is_x, double* dx, double* dres, bool accumulate, cudaStream_t st);
 void launch_f64_acc_copy(const double* src, double* dst, int64_t n, bool accumulate, cudaStream_t st);
 }  // namespace moe
+
+namespace moe {
+// gate_fused.cu: logits + softmax + top-k + balance partials + balance finalize
+// in one cluster kernel (bf16 path, E == 64)
+bool gate_fused_ok(int d, int E);
+int gate_fused_parts(int64_t T);
+// wsplit [2][E][d]: tf32 hi / lo halves of Wg^T
+void launch_gate_split(const float* wg, float* wsplit, int d, cudaStream_t st);
+void launch_gate_fused(const __nv_bfloat16* x, const float* noise, const float* wsplit, int64_t T, int d, int K,
+                       double alpha, float* probs, int32_t* choice, float* gate_prob, float* colsum_part,
+                       int32_t* count_part, uint32_t* flags, float* aux, float* fcoef, int32_t* fcount,
+                       double* term, unsigned* done, cudaStream_t st);
+}  // namespace moe

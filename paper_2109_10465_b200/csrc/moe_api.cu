@@ -169,6 +169,8 @@ struct moe_handle {
     bool nccl_barrier = false;
     bool defer_balance = false;
     bool gemm_tc = false;        // bf16 expert GEMMs on tcgen05 (decided at create)
+    bool gate_fused = false;     // bf16 gate in one cluster kernel (gate_fused.cu)
+    DevMem wsplit;               // [2][E][d] tf32 hi / lo halves of Wg^T
     size_t ws_bytes = 0;         // device bytes allocated by this handle  // forward under EP: the balance loss runs next to the dispatch exchange
     ~moe_handle() {
         for (int b = 0; b < P_NBUF; ++b)
@@ -488,10 +490,16 @@ void route(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, int phas
     cudaStream_t st = h->stream;
     const bool jitter = phase == MOE_TRAIN && h->cfg.jitter_eps > 0.0;
     const bool gtc = use_gate_tc<TIO>(h);
+    // fused gate (gate_fused.cu): one cluster kernel for logits, softmax,
+    // top-k and the balance loss; MOE_B200_GATE_FUSED=0 keeps the split kernels
+    const bool fused = gtc && h->gate_fused;
     if (gtc) {  // Wg^T for the logits' B operand, on the side stream next to the jitter generator
         MOE_CUDA_CHECK(cudaEventRecord(h->ev_a, st));
         MOE_CUDA_CHECK(cudaStreamWaitEvent(h->side, h->ev_a, 0));
-        launch_gate2_transpose(gate_w, h->wgt.as<float>(), static_cast<int>(h->d), E, h->side);
+        if (fused)
+            launch_gate_split(gate_w, h->wsplit.as<float>(), static_cast<int>(h->d), h->side);
+        else
+            launch_gate2_transpose(gate_w, h->wgt.as<float>(), static_cast<int>(h->d), E, h->side);
         MOE_CUDA_CHECK(cudaEventRecord(h->ev_b, h->side));
     }
     if (jitter) {
@@ -507,6 +515,20 @@ void route(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, int phas
         }
         h->pf_valid = false;
         h->mark("jitter_noise");
+    }
+    if (fused) {
+        if constexpr (std::is_same<TIO, __nv_bfloat16>::value) {
+            MOE_CUDA_CHECK(cudaStreamWaitEvent(st, h->ev_b, 0));
+            launch_gate_fused(x, jitter ? h->noise.as<float>() : nullptr, h->wsplit.as<float>(), T,
+                              static_cast<int>(h->d), K, h->cfg.balance_coeff, h->probs.as<float>(),
+                              h->choice.as<int32_t>(), h->gate_prob.as<float>(), h->colsum_part.as<float>(),
+                              h->count_part.as<int32_t>(), h->flags.as<uint32_t>(),
+                              aux ? aux : h->aux_scratch.as<float>(), h->fcoef.as<float>(),
+                              h->fcount.as<int32_t>(), h->bal_term.as<double>(), h->bal_done.as<unsigned>(), st);
+        }
+        h->mark("gate_fused");
+        h->jitter_on = jitter;
+        return;
     }
     // logits = (x * noise) @ gate_w  (routing.cpp:71)
     int nsplit = 1;
@@ -1023,6 +1045,11 @@ void alloc_workspace(moe_handle* h) {
     h->dxg.alloc(4 * T * d);
     h->dwg_part.alloc(4 * 16 * d * E);
     h->wgt.alloc(4 * d * E);
+    h->wsplit.alloc(8 * d * E);
+    {
+        const char* g = std::getenv("MOE_B200_GATE_FUSED");
+        h->gate_fused = es == 2 && gate_fused_ok(static_cast<int>(d), E) && !(g && g[0] == '0');
+    }
     MOE_CUDA_CHECK(cudaDeviceSynchronize());
 }
 

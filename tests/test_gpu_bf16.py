@@ -211,3 +211,35 @@ def test_bf16_gemm_variants_subprocess(pair):
                         os.path.abspath(__file__)], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("top_k,T", [(1, 8192), (2, 1000), (1, 300)])
+def test_fused_gate_matches_split_kernels(top_k, T):
+    """The fused gate (gate_fused.cu: logits + softmax + top-k + balance loss in
+    one cluster kernel) against the split kernels (MOE_B200_GATE_FUSED=0:
+    split-K logits, softmax_topk, balance_finalize) on the same inputs:
+    identical decisions, probabilities / gate_prob / aux within fp32 rounding,
+    including a ragged last tile (T % 128 != 0)."""
+    import os
+
+    import paper_2109_10465_b200 as M
+    d, f, E, seed = 2048, 256, 64, 5
+    x0, gw, *_ = O.layer_inputs(T, d, 8, E, seed=seed)
+    ocfg = O.make_cfg(num_experts=E, top_k=top_k)
+    x = margin_guard(bf16_round(x0), gw, ocfg, O.TRAIN, seed, round_fn=bf16_round)
+    outs = []
+    for fused in ("1", "0"):
+        os.environ["MOE_B200_GATE_FUSED"] = fused
+        try:
+            layer, p, xd, dy = device_layer(T, d, f, E, seed, x, gw.astype(np.float32).astype(np.float64),
+                                            dict(top_k=top_k))
+        finally:
+            os.environ.pop("MOE_B200_GATE_FUSED", None)
+        y, aux, dec = layer.forward(xd, p, M.Phase.TRAIN, seed)
+        torch.cuda.synchronize()
+        outs.append((dec.expert_id.cpu(), dec.slot.cpu(), dec.gate_prob.cpu(), float(aux[0]), y.float().cpu()))
+    (e1, s1, g1, a1, y1), (e0, s0, g0, a0, y0) = outs
+    assert torch.equal(e1, e0) and torch.equal(s1, s0)
+    assert float((g1 - g0).abs().max()) <= 2e-6
+    assert abs(a1 - a0) <= 1e-6 * max(1.0, abs(a0))
+    assert float((y1 - y0).abs().max()) <= 2e-2 * max(1.0, float(y0.abs().max()))
