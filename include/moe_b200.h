@@ -305,6 +305,9 @@ moe_status moe_debug_mt64_chunk_host(uint64_t seed, int64_t J, int c, int64_t n,
 /* testing: the first `count` raw outputs of Rng(seed) from the device
  * generator into device memory out_dev. */
 moe_status moe_debug_mt64_device(uint64_t seed, int64_t count, uint64_t* out_dev);
+/* testing: Rng(seed).permutation(n) (the RTS order, rng.cpp:94-102) built on
+ * the device (rts.cu) into device memory perm_dev [n] uint32. */
+moe_status moe_debug_rts_order(uint64_t seed, int64_t n, uint32_t* perm_dev);
 /* testing: the first `count` jitter values (float)Rng(seed).uniform(1-eps,
  * 1+eps) (rng.cpp:41-43) from the device generator into device memory. */
 moe_status moe_debug_jitter_device(uint64_t seed, int64_t count, double eps, float* out_dev);

@@ -114,6 +114,7 @@ _SIGS = {
     "moe_adam_update": (C.c_int, [VP, VP, VP, VP, C.c_int64, C.c_int, VP, VP, C.c_double, C.c_double,
                                   C.c_double, C.c_double, C.c_int64, VP]),
     "moe_debug_jitter_device": (C.c_int, [C.c_uint64, C.c_int64, C.c_double, VP]),
+    "moe_debug_rts_order": (C.c_int, [C.c_uint64, C.c_int64, VP]),
     "moe_debug_gate_tc_logits": (C.c_int, [VP, VP, VP, VP, C.c_int64, C.c_int, C.c_int, C.c_int]),
     "moe_debug_gate_tc_dw": (C.c_int, [VP, VP, VP, VP, C.c_int64, C.c_int, C.c_int, C.c_int]),
     "moe_debug_gate_tc_dx": (C.c_int, [C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int, VP, VP, VP, VP,

@@ -12,6 +12,7 @@ constexpr uint32_t MOE_FLAG_NONFINITE_DEV = 0x1u;
 constexpr uint32_t MOE_FLAG_PROB_ROWS_DEV = 0x2u;
 constexpr uint32_t MOE_FLAG_CHOICE_RANGE_DEV = 0x4u;
 constexpr uint32_t MOE_FLAG_UNIFORM_SHAPE_DEV = 0x8u;
+constexpr uint32_t MOE_FLAG_RTS_OVERFLOW_DEV = 0x10u;
 // fp32 probabilities: |sum_e P - 1| bound used in place of the reference's
 // f64 1e-9 (routing.cpp:360-361).
 constexpr float kProbRowTol = 1e-4f;
@@ -299,4 +300,11 @@ void launch_gate_fused(const __nv_bfloat16* x, const float* noise, const float* 
                        double alpha, float* probs, int32_t* choice, float* gate_prob, float* colsum_part,
                        int32_t* count_part, uint32_t* flags, float* aux, float* fcoef, int32_t* fcount,
                        double* term, unsigned* done, cudaStream_t st);
+}  // namespace moe
+
+namespace moe {
+// rts.cu: Rng(seed).permutation(n) on the device (the RTS priority order)
+size_t rts_scratch_bytes(int64_t n);
+void launch_rts_order(uint64_t seed, int64_t n, void* scratch, uint32_t* perm, uint32_t* layer_flags,
+                      cudaStream_t st);
 }  // namespace moe

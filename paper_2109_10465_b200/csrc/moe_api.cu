@@ -176,7 +176,7 @@ struct moe_handle {
         for (int b = 0; b < P_NBUF; ++b)
             for (int r = 0; r < 8; ++r)
                 if (ipc && r != rank && peer[b][r]) cudaIpcCloseMemHandle(peer[b][r]);
-        for (cudaEvent_t e : {ev_a, ev_b, ev_c, ev_side, ev_comm, ev_pf})
+        for (cudaEvent_t e : {ev_a, ev_b, ev_c, ev_side, ev_comm, ev_pf, ev_rts})
             if (e) cudaEventDestroy(e);
         if (side) cudaStreamDestroy(side);
         if (comm_stream) cudaStreamDestroy(comm_stream);
@@ -195,7 +195,9 @@ struct moe_handle {
     bool pf_req = false, pf_valid = false;
     uint64_t pf_req_seed = 0, pf_seed = 0;
     int64_t pf_req_count = 0, pf_count = 0;
-    cudaEvent_t ev_pf = nullptr;
+    cudaEvent_t ev_pf = nullptr, ev_rts = nullptr;
+    DevMem rts_scratch;         // rts.cu working set
+    bool rts_host = false;      // MOE_B200_RTS_HOST=1: RTS order from the host
     DevMem db1_part;            // [rows/32][f] column sums from the dgrad2 epilogue
     // float64 path (dtype MOE_F64): logits, probabilities, gate_prob, weights,
     // noise, dL, dw [T*K], f_e [E]
@@ -571,15 +573,24 @@ void balance_finalize(moe_handle* h, int64_t T, float* aux) {
     h->mark("balance_loss");
 }
 
-void assign(moe_handle* h, int64_t T, const int32_t* choice, int cap, int mode, uint64_t aseed,
-            int32_t* slot_out) {
-    const uint32_t* ord = nullptr;
-    if (mode == MOE_RTS) {
-        // routing.cpp:180-187: priority order = Rng(derive_seed(seed,"assign")).permutation(T)
+// routing.cpp:180-187: the RTS priority order Rng(seed).permutation(T), built on
+// the device (rts.cu) on stream `st`; MOE_B200_RTS_HOST=1 computes it on the host
+void rts_order(moe_handle* h, int64_t T, uint64_t aseed, cudaStream_t st) {
+    if (h->rts_host) {
         h->host_ord.resize(static_cast<size_t>(T));
         permutation(aseed, T, h->host_ord.data());
         MOE_CUDA_CHECK(cudaMemcpyAsync(h->ord.p, h->host_ord.data(), sizeof(uint32_t) * T,
-                                       cudaMemcpyHostToDevice, h->stream));
+                                       cudaMemcpyHostToDevice, st));
+    } else {
+        launch_rts_order(aseed, T, h->rts_scratch.p, h->ord.as<uint32_t>(), h->flags.as<uint32_t>(), st);
+    }
+}
+
+void assign(moe_handle* h, int64_t T, const int32_t* choice, int cap, int mode, uint64_t aseed,
+            int32_t* slot_out, bool ord_ready = false) {
+    const uint32_t* ord = nullptr;
+    if (mode == MOE_RTS) {
+        if (!ord_ready) rts_order(h, T, aseed, h->stream);
         ord = h->ord.as<uint32_t>();
     }
     if (mode == MOE_GROUPED && T % h->cfg.group_count != 0)
@@ -615,8 +626,15 @@ void forward_impl(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, c
     h->defer_balance = ep > 1;
     route<TIO>(h, T, x, gate_w, phase, seed, aux);
     h->defer_balance = false;
+    if (mode == MOE_RTS) {  // the priority order on the side stream, next to the gate kernels
+        MOE_CUDA_CHECK(cudaEventRecord(h->ev_a, st));
+        MOE_CUDA_CHECK(cudaStreamWaitEvent(h->side, h->ev_a, 0));
+        rts_order(h, T, derive_seed_tag(seed, "assign"), h->side);
+        MOE_CUDA_CHECK(cudaEventRecord(h->ev_rts, h->side));
+        MOE_CUDA_CHECK(cudaStreamWaitEvent(st, h->ev_rts, 0));
+    }
     assign(h, T, h->choice.as<int32_t>(), h->cap, mode, derive_seed_tag(seed, "assign"),
-           h->slot.as<int32_t>());
+           h->slot.as<int32_t>(), true);
     h->mark("assign");
     if (ep == 1) launch_combine_weights(T, E, K, h->gate_prob.as<float>(), h->wts.as<float>(), st);
     // dispatch (routing.cpp:396): un-jittered x into [E, cap_pad, d]
@@ -1001,6 +1019,11 @@ void alloc_workspace(moe_handle* h) {
     h->noise.alloc(4 * T * d);
     h->noise_pf.alloc(4 * T * d);
     h->ord.alloc(4 * T);
+    h->rts_scratch.alloc(rts_scratch_bytes(T));
+    {
+        const char* r = std::getenv("MOE_B200_RTS_HOST");
+        h->rts_host = r && r[0] == '1';
+    }
     h->flags.alloc(16);
     MOE_CUDA_CHECK(cudaMemset(h->flags.p, 0, 16));
     const size_t sints = assign_scratch_ints(T, E, K, G);
@@ -1184,7 +1207,7 @@ moe_status moe_create(const moe_router_cfg* cfg, const moe_layer_dims* dims, moe
         }
         MOE_CUDA_CHECK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
         MOE_CUDA_CHECK(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
-        for (cudaEvent_t* e : {&h->ev_a, &h->ev_b, &h->ev_c, &h->ev_side, &h->ev_comm, &h->ev_pf})
+        for (cudaEvent_t* e : {&h->ev_a, &h->ev_b, &h->ev_c, &h->ev_side, &h->ev_comm, &h->ev_pf, &h->ev_rts})
             MOE_CUDA_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     });
     if (s == MOE_OK) *out = h.release();
@@ -1265,6 +1288,10 @@ moe_status moe_check(moe_handle* h, uint32_t* flags_out) {
         h->err = "simulate: per-rank token counts must be identical (All-to-All requires the same "
                  "tensor shape on every rank)";
         return MOE_UNIFORM_SHAPE;
+    }
+    if (fl & MOE_FLAG_RTS_OVERFLOW_DEV) {
+        h->err = "assign_rts: more rejected uniform_int draws than spare generator outputs";
+        return MOE_CUDA;
     }
     if (fl & MOE_FLAG_PROB_ROWS) {
         h->err = "balance_loss: probs rows must sum to 1";
@@ -1634,6 +1661,15 @@ moe_status moe_debug_gate_tc_dx(int64_t T, int d, int E, int K, int cap_pad, con
                                   pos, static_cast<const B*>(dy), residual_is_x != 0, static_cast<B*>(dx),
                                   static_cast<B*>(dres), nullptr);
         MOE_CUDA_CHECK(cudaDeviceSynchronize());
+    });
+}
+moe_status moe_debug_rts_order(uint64_t seed, int64_t n, uint32_t* perm_dev) {
+    return guarded(nullptr, [&] {
+        void* scratch = nullptr;
+        MOE_CUDA_CHECK(cudaMalloc(&scratch, moe::rts_scratch_bytes(n)));
+        moe::launch_rts_order(seed, n, scratch, perm_dev, nullptr, nullptr);
+        MOE_CUDA_CHECK(cudaDeviceSynchronize());
+        MOE_CUDA_CHECK(cudaFree(scratch));
     });
 }
 moe_status moe_debug_jitter_device(uint64_t seed, int64_t count, double eps, float* out_dev) {

@@ -5,6 +5,8 @@ bit-exact.  fp32 path: every output and gradient within
 max|gpu - ref| / max(1, |ref|) <= 1e-5 (the normalisation of the reference's
 gradcheck.hpp:21-24).  bf16 path: see test_gpu_bf16.py.
 """
+import ctypes as C
+
 import numpy as np
 import pytest
 import torch
@@ -331,3 +333,16 @@ def test_drop_position_bias_plain_vs_rts(seed):
     ref = O.restatement().assign(choice.cpu().numpy(), E, cap, 1, O.RTS, 1, seed)
     ref_slot = ref[0] if isinstance(ref, tuple) else ref
     assert np.array_equal(rts.slot.cpu().numpy(), np.asarray(ref_slot)[:T])
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 97, 1000, 8192, 16384, 65537])
+def test_rts_order_device_matches_reference_permutation(n):
+    """rts.cu rebuilds Rng(seed).permutation(n) (rng.cpp:94-102) on the device
+    (mt19937_64 draws + parallel chain reconstruction of the Fisher-Yates
+    swaps): bit-exact against the reference restatement for several seeds."""
+    from paper_2109_10465_b200 import _lib
+    o = O.restatement()
+    for seed in (0, 42, O.restatement().derive_seed(42, "assign"), 2**63 + 5):
+        out = torch.empty(n, dtype=torch.int32, device="cuda")
+        assert _lib.load().moe_debug_rts_order(seed, n, C.c_void_p(out.data_ptr())) == 0
+        assert np.array_equal(out.cpu().numpy().astype(np.uint32), o.permutation(seed, n)), (seed, n)
