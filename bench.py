@@ -307,10 +307,11 @@ def run_ours(args):
                  dresidual=None)
 
     # one layer seed per step, derived like the reference trainer's per-step
-    # seeds (trainer.cpp:146-149).  With --prefetch the next step's jitter
-    # stream is generated during this step's backward (moe_prefetch_jitter);
-    # measured: it hides the 0.2 ms generation but slows the co-running
-    # weight-gradient GEMMs by more (0.27 ms), so the default generates in place
+    # seeds (trainer.cpp:146-149), so the next step's seed is known.  With
+    # prefetch (default; --no-prefetch turns it off) the next step's jitter
+    # stream is generated during this step (moe_prefetch_jitter: MOE_B200_PF_SMS
+    # = 8 CTAs on their own stream next to the forward and dgrad GEMMs, which
+    # leave those SMs free).  Every step still generates exactly one stream.
     step_no = [0]
 
     def seed_of(i):
@@ -318,9 +319,9 @@ def run_ours(args):
 
     def fwd(xx, yy, aa):
         i = step_no[0]
-        layer.forward(xx, params, M.Phase.TRAIN, seed_of(i), y=yy, aux=aa, decision=False, check=False)
         if args.prefetch:
             layer.prefetch_jitter(seed_of(i + 1), T)
+        layer.forward(xx, params, M.Phase.TRAIN, seed_of(i), y=yy, aux=aa, decision=False, check=False)
         step_no[0] += 1
 
     def step():
@@ -435,36 +436,61 @@ def run_ours(args):
     n_rows = int(kept.sum().item()) if N == 1 else None
     if n_rows is None:
         n_rows = T  # EP: every GPU processes ~T kept rows per step (weak scaling)
-    # the dominant kernel family is the expert GEMM (>60% of the step); report
-    # the slowest of its launches
-    modeled = [k for k in per_stage if stage_model(k, T, d, f, El, 1, T)[0] is not None]
-    top = max(modeled or per_stage, key=lambda k: per_stage[k]["ms"])
-    bytes_, flops = stage_model(top, T, d, f, El, n_rows, T)
-    dur = per_stage[top]["ms"] / 1e3
-    roof = None
-    if bytes_ is not None:
-        t_mem = bytes_ / (hbm * 1e9)
-        t_cmp = flops / (tf_sus * 1e12)
-        if t_mem >= t_cmp:
-            ach = bytes_ / dur / 1e9
-            roof = {"kernel": top, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                    "frac": ach / hbm, "peak_source": src, "algorithmic_bytes": bytes_,
-                    "flops": flops, "traffic": None}
+    # The dominant kernel is the row-GEMM family (tc::grouped_gemm_kernel<ROW>:
+    # ffn1_fwd, ffn2_fwd, ffn2_dgrad, ffn1_dgrad — the largest share of the
+    # step); its roofline is the launches' algorithmic bytes (or FLOPs) over
+    # their summed CUDA-event durations.  The weight-gradient family
+    # (tc::grouped_gemm_kernel<WGRAD>) and the slowest single launch are
+    # reported beside it.
+    families = {"tc::grouped_gemm_kernel<ROW> (fwd1, fwd2, dgrad2, dgrad1)":
+                ["ffn1_fwd", "ffn2_fwd", "ffn2_dgrad", "ffn1_dgrad"],
+                "tc::grouped_gemm_kernel<WGRAD> (dW2, dW1)": ["ffn2_wgrad", "ffn1_wgrad"]}
+
+    def family_roof(name, stages_):
+        stages_ = [k for k in stages_ if k in per_stage]
+        if not stages_:
+            return None
+        b_tot = f_tot = ms_tot = 0.0
+        for k in stages_:
+            b_, f_ = stage_model(k, T, d, f, El, n_rows, T)
+            b_tot += b_
+            f_tot += f_
+            ms_tot += per_stage[k]["ms"]
+        dur = ms_tot / 1e3
+        if b_tot / (hbm * 1e9) >= f_tot / (tf_sus * 1e12):
+            ach = b_tot / dur / 1e9
+            r = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                 "peak_source": src}
         else:
-            ach = flops / dur / 1e12
-            roof = {"kernel": top, "bound": "tensor", "achieved": ach, "peak": tf_sus,
-                    "unit": "TFLOP/s", "frac": ach / tf_sus, "peak_source": src + " (sustained)",
-                    "algorithmic_bytes": bytes_, "flops": flops, "traffic": None}
-        roof["launch_ms"] = per_stage[top]["ms"]
-        tr, tsrc = traffic_for(top, f"c3 T={T} N={N}")
-        if tr is not None:
-            roof["traffic"] = tr
-            roof["traffic_source"] = tsrc
+            ach = f_tot / dur / 1e12
+            r = {"kernel": name, "bound": "tensor", "achieved": ach, "peak": tf_sus, "unit": "TFLOP/s",
+                 "frac": ach / tf_sus, "peak_source": src + " (sustained)"}
+        r.update({"launches_per_step": len(stages_), "algorithmic_bytes_per_launch": b_tot / len(stages_),
+                  "flops_per_launch": f_tot / len(stages_), "launch_ms": ms_tot / len(stages_),
+                  "stages": stages_, "traffic": None})
+        tr = [traffic_for(k, f"c3 T={T} N={N}") for k in stages_]
+        if all(t_[0] is not None for t_ in tr):
+            r["traffic"] = sum(t_[0] for t_ in tr) / len(tr)
+            r["traffic_source"] = tr[0][1]
+        return r
+
+    fam = {k: family_roof(k, v) for k, v in families.items()}
+    fam_ms = {k: sum(per_stage[s_]["ms"] for s_ in v if s_ in per_stage) for k, v in families.items()}
+    dom = max(fam_ms, key=fam_ms.get)
+    roof = fam[dom]
+    roof_other = {k: v for k, v in fam.items() if k != dom and v is not None}
+    modeled = [k for k in per_stage if stage_model(k, T, d, f, El, 1, T)[0] is not None]
+    slowest = max(modeled, key=lambda k: per_stage[k]["ms"]) if modeled else None
+    if slowest:
+        b_, f_ = stage_model(slowest, T, d, f, El, n_rows, T)
+        ach = b_ / (per_stage[slowest]["ms"] / 1e3) / 1e9
+        roof_slowest = {"stage": slowest, "achieved": ach, "unit": "GB/s", "frac_of_hbm": ach / hbm,
+                        "launch_ms": per_stage[slowest]["ms"]}
     # HBM-bound stages against the same measured peak
     n_kept = int(kept.sum().item()) if N == 1 else T
     n_drop = T - n_kept
-    groups = {"gate": ["jitter_noise", "gate_logits", "softmax_topk", "balance_loss"],
-              "gate_excl_jitter": ["gate_logits", "softmax_topk", "balance_loss"]}
+    gate_parts = [k for k in ("gate_fused", "gate_logits", "softmax_topk", "balance_loss") if k in per_stage]
+    groups = {"gate": ["jitter_noise"] + gate_parts, "gate_excl_jitter": gate_parts}
     stage_roof = {}
     for name in ["gate", "gate_excl_jitter", "assign", "dispatch", "combine", "combine_bwd", "gate_dx"]:
         parts = groups.get(name, [name])
@@ -481,9 +507,12 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random-init weights of the config-3 architecture, U(-1,1) tokens)",
             "config": dict(workload_config(N, E, T), seeds="per step: derive_seed(derive_seed(42, rank), step)",
-                           jitter_stream="generated during the previous step's backward (moe_prefetch_jitter)"
-                           if args.prefetch else "generated at the head of each forward"),
+                           jitter_stream="each step generates the next step's stream next to its expert GEMMs "
+                                         "(moe_prefetch_jitter, 8 SMs)" if args.prefetch
+                           else "generated at the head of each forward"),
             "roofline": roof,
+            "roofline_other_families": roof_other,
+            "roofline_slowest_launch": roof_slowest if slowest else None,
             "expert_gemms": {"ms_per_step": gemm_ms, "tflops": gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms else None,
                              "frac_of_bf16_sustained": (gemm_flops / (gemm_ms / 1e3) / 1e12) / tf_sus if gemm_ms else None},
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms,
@@ -663,9 +692,10 @@ def main():
                     help="config-3 variant with this many experts in total (EP-overhead baselines: "
                          "1 GPU with E=64/N experts has the same rows per expert as N GPUs with E=64)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--prefetch", action="store_true",
+    ap.add_argument("--no-prefetch", dest="prefetch", action="store_false",
                     help="generate the next step's jitter stream during this step's backward "
-                         "(moe_prefetch_jitter; it co-runs with the weight-gradient GEMMs)")
+                         "(moe_prefetch_jitter, default on: generate the next step's jitter stream next to "
+                         "this step's expert GEMMs; off = generate it at the head of each forward)")
     ap.add_argument("--workload", default="c3", choices=["c3"] + sorted(EXTRA))
     ap.add_argument("--tokens", type=int, default=0, help="override T for --workload c1/c2/c4/c5")
     args = ap.parse_args()

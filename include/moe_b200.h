@@ -159,14 +159,14 @@ moe_status moe_last_decision_stats(moe_handle* h, int* capacity, int64_t* drop_c
                                    int64_t* kept_per_expert);
 
 /* Generate the jitter stream of a FUTURE train-phase moe_forward(seed) with
- * `tokens` rows ahead of use: the work is launched during the next
- * moe_backward on this handle (on its side stream, before the
- * weight-gradient GEMMs) into a second buffer that the matching forward swaps
- * in instead of generating.  The values are identical either way (the stream
- * depends only on the seed); a forward with another seed / token count simply
- * generates as usual.  Measured at config 3 it does not pay (the generator
- * competes with the GEMMs for the SMs), so bench.py only uses it with
- * --prefetch; it is for callers whose backward leaves the GPU idle. */
+ * `tokens` rows ahead of use: the work is launched by the next moe_forward on
+ * this handle (after its gate, on its own stream, as MOE_B200_PF_SMS = 8
+ * CTAs — one chunk of the mt19937_64 stream per SM) and co-runs with that
+ * call's forward and dgrad expert GEMMs, which leave those SMs free; the
+ * matching later forward swaps the buffer in instead of generating on every
+ * SM at its head.  Values are identical either way (the stream depends only on
+ * the seed).  Training-loop pattern (per-step seeds are known ahead,
+ * trainer.cpp:146-149): prefetch(seed_{i+1}); forward(seed_i); backward. */
 moe_status moe_prefetch_jitter(moe_handle* h, uint64_t seed, int64_t tokens);
 
 /* Utilization and drop statistics of the last forward, accumulated on the

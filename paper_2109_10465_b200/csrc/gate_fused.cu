@@ -5,8 +5,9 @@
 // A cluster of two CTAs owns 128 tokens; CTA r reduces half of d:
 //
 //   warp 0      TMA producer: raw x (bf16) and jitter (fp32) tiles [128 x 32]
-//               plus the pre-split tf32 hi / lo halves of Wg^T [64 x 32]
-//               (128B-swizzled, read by the MMA in place) into a 3-deep ring
+//               into a 4-deep ring, and the pre-split tf32 hi / lo halves of
+//               Wg^T [64 x 32] (128B-swizzled, read by the MMA in place) into
+//               a 3-deep ring
 //   warps 2..5  transform: g = x * noise, 3xTF32 split g = hi + lo, written
 //               into the 128B-swizzled K-major A operand (2-deep ring)
 //   warp 1      MMA: tcgen05.mma kind::tf32, M=128 N=64 K=8, hi*hi + hi*lo +
@@ -18,12 +19,14 @@
 //               top-1 / top-2 with the reference's tie rules (routing.cpp:
 //               77-92), probabilities / choices / gate_prob stores, and the
 //               per-64-row column sums and first-choice counts of the balance
-//               loss; the last CTA to finish reduces them in fixed order
-//               (f64) into aux and the gradient coefficients f_e / T.
+//               loss (reduced in fixed order by balance_finalize_kernel on the
+//               side stream, off the routing's critical path).
 //
 // No logits or split-K partials go to HBM: the kernel reads x (and the
 // jitter) once and writes P, the decision and the small balance partials.
 #include <cuda.h>
+
+#include <cstdlib>
 
 #include "common.cuh"
 #include "gemm_tc.h"
@@ -38,17 +41,20 @@ using namespace tc;
 constexpr int E = 64;              // experts (TMEM columns per accumulator)
 constexpr int BM = 128;            // tokens per cluster
 constexpr int BK = 32;             // fp32 K elements per step (one 128 B swizzle row)
-constexpr int kRaw = 3;            // raw ring depth
+constexpr int kRaw = 4;            // raw x / noise ring depth
+constexpr int kB = 3;              // B (Wg^T hi / lo) ring depth
 constexpr int kOp = 2;             // A-operand ring depth
 constexpr int kNAcc = 4;           // TMEM accumulators
-constexpr int kThreads = 192;
+constexpr int kTw = 8;             // transform warps (two per SM sub-partition)
+constexpr int kThreads = 32 * (2 + kTw);
 constexpr uint32_t kRawX = BM * BK * 2;        //  8 KB bf16 x
 constexpr uint32_t kRawN = BM * BK * 4;        // 16 KB fp32 noise
 constexpr uint32_t kRawB = E * 128;            //  8 KB per hi / lo
-constexpr uint32_t kRawStage = kRawX + kRawN + 2 * kRawB;   // 40 KB
+constexpr uint32_t kRawStage = kRawX + kRawN;                // 24 KB
+constexpr uint32_t kBStage = 2 * kRawB;                      // 16 KB
 constexpr uint32_t kOpStage = 2 * BM * 128;                  // 32 KB (A hi, A lo)
 constexpr uint32_t kRecv = 64 * E * 4;                       // 16 KB: peer's partials for my rows
-constexpr uint32_t kSmem = 1024 + kRaw * kRawStage + kOp * kOpStage + kRecv + 512;
+constexpr uint32_t kSmem = 1024 + kRaw * kRawStage + kB * kBStage + kOp * kOpStage + kRecv + 512;
 
 struct __align__(64) Params {
     CUtensorMap tmX, tmN, tmBh, tmBl;
@@ -58,14 +64,9 @@ struct __align__(64) Params {
     float* colsum_part;   // [parts][E], part = 64 tokens
     int32_t* count_part;  // [parts][E]
     uint32_t* flags;
-    float* aux;
-    float* fcoef;
-    int32_t* fcount;
-    double* term;         // [E]
-    unsigned* done;
-    double alpha;
     int64_t T;
     int d, K, nparts, has_noise;
+    int probe;  // timing probes (MOE_B200_GATE_PROBE): 1 no split math, 2 no MMA
 };
 
 __device__ __forceinline__ float tf32_rna(float v) {
@@ -97,16 +98,18 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* raw = sm;
-    uint8_t* op = raw + kRaw * kRawStage;
+    uint8_t* bst = raw + kRaw * kRawStage;
+    uint8_t* op = bst + kB * kBStage;
     float* recv = reinterpret_cast<float*>(op + kOp * kOpStage);
     uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(recv) + kRecv);
     uint64_t* raw_full = bars;
     uint64_t* raw_empty = raw_full + kRaw;
-    uint64_t* op_full = raw_empty + kRaw;
+    uint64_t* b_full = raw_empty + kRaw;
+    uint64_t* b_empty = b_full + kB;
+    uint64_t* op_full = b_empty + kB;
     uint64_t* op_empty = op_full + kOp;
     uint64_t* acc_full = op_empty + kOp;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(acc_full + 1);
-    __shared__ int s_last;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
@@ -114,14 +117,21 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
     const int kspan = p.d / 2;
     const int kbase = static_cast<int>(rank) * kspan;
     const int nsteps = kspan / BK;
+    // every cluster walks its K range from a different starting step, so the
+    // 128 CTAs do not all read the same Wg^T tile from L2 at the same time
+    const int kskew = static_cast<int>((blockIdx.x >> 1) % nsteps);
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < kRaw; ++i) {
             mbar_init(&raw_full[i], 1);
-            mbar_init(&raw_empty[i], 4 + 1);  // 4 transform warps + the MMA commit (B read)
+            mbar_init(&raw_empty[i], kTw);  // the transform warps have read x / noise
+        }
+        for (int i = 0; i < kB; ++i) {
+            mbar_init(&b_full[i], 1);
+            mbar_init(&b_empty[i], 1);    // the MMAs of the step have read B
         }
         for (int i = 0; i < kOp; ++i) {
-            mbar_init(&op_full[i], 4);
+            mbar_init(&op_full[i], kTw);
             mbar_init(&op_empty[i], 1);
         }
         mbar_init(acc_full, 1);
@@ -146,17 +156,20 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
     if (warp == 0) {
         // ---------------- TMA producer
         if (lane == 0) {
-            const uint32_t bytes = kRawX + (p.has_noise ? kRawN : 0) + 2 * kRawB;
+            const uint32_t bytes = kRawX + (p.has_noise ? kRawN : 0);
             for (int s = 0; s < nsteps; ++s) {
-                const int rs = s % kRaw;
+                const int rs = s % kRaw, bs = s % kB;
+                const int k0 = kbase + ((s + kskew) % nsteps) * BK;
                 if (s >= kRaw) mbar_wait(&raw_empty[rs], ((s / kRaw) - 1) & 1);
                 uint8_t* st = raw + rs * kRawStage;
-                const int k0 = kbase + s * BK;
                 mbar_expect_tx(&raw_full[rs], bytes);
                 tma_load_2d(&p.tmX, &raw_full[rs], st, k0, static_cast<int32_t>(t0));
                 if (p.has_noise) tma_load_2d(&p.tmN, &raw_full[rs], st + kRawX, k0, static_cast<int32_t>(t0));
-                tma_load_2d(&p.tmBh, &raw_full[rs], st + kRawX + kRawN, k0, 0);
-                tma_load_2d(&p.tmBl, &raw_full[rs], st + kRawX + kRawN + kRawB, k0, 0);
+                if (s >= kB) mbar_wait(&b_empty[bs], ((s / kB) - 1) & 1);
+                uint8_t* bt = bst + bs * kBStage;
+                mbar_expect_tx(&b_full[bs], kBStage);
+                tma_load_2d(&p.tmBh, &b_full[bs], bt, k0, 0);
+                tma_load_2d(&p.tmBl, &b_full[bs], bt + kRawB, k0, 0);
             }
         }
     } else if (warp == 1) {
@@ -164,14 +177,15 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
         if (lane == 0) {
             constexpr uint32_t idesc = make_idesc_tf32(BM, E, 0, 0);
             for (int s = 0; s < nsteps; ++s) {
-                const int rs = s % kRaw, os = s % kOp;
-                mbar_wait(&raw_full[rs], (s / kRaw) & 1);
+                const int bs = s % kB, os = s % kOp;
+                mbar_wait(&b_full[bs], (s / kB) & 1);
                 mbar_wait(&op_full[os], (s / kOp) & 1);
                 tc_fence_after();
                 const uint32_t a = smem_u32(op + os * kOpStage);
-                const uint32_t b = smem_u32(raw + rs * kRawStage + kRawX + kRawN);
+                const uint32_t b = smem_u32(bst + bs * kBStage);
 #pragma unroll
                 for (int kk = 0; kk < BK / 8; ++kk) {
+                    if (p.probe & 2) break;
                     const uint64_t ah = sdesc(a + kk * 32, 16, 1024);
                     const uint64_t al = sdesc(a + BM * 128 + kk * 32, 16, 1024);
                     const uint64_t bh = sdesc(b + kk * 32, 16, 1024);
@@ -181,14 +195,14 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
                     tc_mma_tf32(acc, ah, bl, idesc, 1u);
                     tc_mma_tf32(acc, al, bh, idesc, 1u);
                 }
-                tc_commit(&op_empty[os]);   // A operand stage free
-                tc_commit(&raw_empty[rs]);  // B halves (in the raw stage) read
+                tc_commit(&op_empty[os]);  // A operand stage free
+                tc_commit(&b_empty[bs]);   // B stage free
             }
             tc_commit(acc_full);
         }
     } else {
         // ---------------- transform: g = x * noise -> tf32 hi / lo, swizzled K-major
-        const int tw = warp - 2;
+        const int tw = warp - 2;  // rows [16 tw, 16 tw + 16)
         const int c = lane & 7;
         for (int s = 0; s < nsteps; ++s) {
             const int rs = s % kRaw, os = s % kOp;
@@ -198,8 +212,8 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
             const uint32_t ahi = smem_u32(op + os * kOpStage);
             const uint32_t alo = ahi + BM * 128;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int r = tw * 32 + (lane >> 3) + 4 * j;
+            for (int j = 0; j < 4; ++j) {
+                const int r = tw * 16 + (lane >> 3) + 4 * j;
                 const uint2 xv = *reinterpret_cast<const uint2*>(st + r * 64 + c * 8);
                 float g[4] = {__uint_as_float(xv.x << 16), __uint_as_float(xv.x & 0xffff0000u),
                               __uint_as_float(xv.y << 16), __uint_as_float(xv.y & 0xffff0000u)};
@@ -208,10 +222,15 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
                     g[0] *= nv.x; g[1] *= nv.y; g[2] *= nv.z; g[3] *= nv.w;
                 }
                 float h[4], l[4];
+                if (p.probe & 1) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    h[q] = tf32_rna(g[q]);
-                    l[q] = tf32_rna(g[q] - h[q]);
+                    for (int q = 0; q < 4; ++q) h[q] = l[q] = g[q];
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        h[q] = tf32_rna(g[q]);
+                        l[q] = tf32_rna(g[q] - h[q]);
+                    }
                 }
                 const uint32_t off = swz(r, c);
                 sts128(ahi + off, make_uint4(__float_as_uint(h[0]), __float_as_uint(h[1]), __float_as_uint(h[2]),
@@ -230,10 +249,11 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
 
     // ---------------- epilogue
     float L[E];
+    const bool epi = warp >= 2 && warp < 6;  // one epilogue warp per TMEM lane quarter
     const int q = warp & 3;                 // TMEM lane quarter of this warp
     const int row = q * 32 + lane;          // token row inside the cluster tile
     const bool mine = (row >> 6) == static_cast<int>(rank);
-    if (warp >= 2) {
+    if (epi) {
         mbar_wait(acc_full, 0);
         tc_fence_after();
 #pragma unroll
@@ -260,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
     int32_t* sC = reinterpret_cast<int32_t*>(sP + 64 * (E + 1));
     const int64_t t = t0 + row;
     uint32_t flag = 0;
-    if (warp >= 2 && mine) {
+    if (epi && mine) {
         const float* pr = recv + (row & 63) * E;
 #pragma unroll
         for (int j = 0; j < E; ++j) L[j] += pr[j];
@@ -309,7 +329,7 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
         }
     }
     // the two owner warps of this CTA: column sums / first-choice counts of their 64 rows
-    const bool owner_warp = warp >= 2 && ((q >> 1) == static_cast<int>(rank));
+    const bool owner_warp = epi && ((q >> 1) == static_cast<int>(rank));
     if (owner_warp) {
         asm volatile("bar.sync 1, 64;" ::: "memory");
         const int j = row & 63;  // expert
@@ -326,32 +346,6 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
         }
         flag = __reduce_or_sync(0xffffffffu, flag);
         if (lane == 0 && flag) atomicOr(p.flags, flag);
-        __threadfence();
-        asm volatile("bar.sync 1, 64;" ::: "memory");
-        if (row == static_cast<int>(rank) * 64) s_last = atomicAdd(p.done, 1u) == gridDim.x - 1;
-        asm volatile("bar.sync 1, 64;" ::: "memory");
-        if (s_last) {
-            // balance_loss finalize (routing.cpp:364-373): f_e = alpha E cnt_e / T over
-            // first choices (drops included), aux = sum_e mean_t P[t,e] f_e; fixed order
-            __threadfence();
-            double csum = 0.0;
-            long long ctot = 0;
-            for (int pp = 0; pp < p.nparts; ++pp) {
-                csum += static_cast<double>(reinterpret_cast<volatile float*>(p.colsum_part)[pp * E + j]);
-                ctot += reinterpret_cast<volatile int32_t*>(p.count_part)[pp * E + j];
-            }
-            const double f = p.alpha * static_cast<double>(E) * static_cast<double>(ctot) / static_cast<double>(p.T);
-            p.fcoef[j] = static_cast<float>(f / static_cast<double>(p.T));
-            p.fcount[j] = static_cast<int32_t>(ctot);
-            p.term[j] = csum / static_cast<double>(p.T) * f;
-            asm volatile("bar.sync 1, 64;" ::: "memory");
-            if (j == 0) {
-                double a = 0.0;
-                for (int e = 0; e < E; ++e) a += reinterpret_cast<volatile double*>(p.term)[e];
-                *p.aux = static_cast<float>(a);
-                *p.done = 0u;  // ready for the next call
-            }
-        }
     }
     tc_fence_before();
     __syncthreads();
@@ -386,9 +380,8 @@ void launch_gate_split(const float* wg, float* wsplit, int d, cudaStream_t st) {
 int gate_fused_parts(int64_t T) { return static_cast<int>(ceil_div(T, static_cast<int64_t>(64))); }
 
 void launch_gate_fused(const __nv_bfloat16* x, const float* noise, const float* wsplit, int64_t T, int d, int K,
-                       double alpha, float* probs, int32_t* choice, float* gate_prob, float* colsum_part,
-                       int32_t* count_part, uint32_t* flags, float* aux, float* fcoef, int32_t* fcount,
-                       double* term, unsigned* done, cudaStream_t st) {
+                       float* probs, int32_t* choice, float* gate_prob, float* colsum_part, int32_t* count_part,
+                       uint32_t* flags, cudaStream_t st) {
     using namespace gf;
     static bool attr = false;
     if (!attr) {
@@ -409,17 +402,16 @@ void launch_gate_fused(const __nv_bfloat16* x, const float* noise, const float* 
     p.colsum_part = colsum_part;
     p.count_part = count_part;
     p.flags = flags;
-    p.aux = aux;
-    p.fcoef = fcoef;
-    p.fcount = fcount;
-    p.term = term;
-    p.done = done;
-    p.alpha = alpha;
     p.T = T;
     p.d = d;
     p.K = K;
     p.nparts = gate_fused_parts(T);
     p.has_noise = noise != nullptr;
+    static const int probe = [] {
+        const char* e = std::getenv("MOE_B200_GATE_PROBE");
+        return e ? std::atoi(e) : 0;
+    }();
+    p.probe = probe;
     const unsigned tiles = static_cast<unsigned>(ceil_div(T, static_cast<int64_t>(BM)));
     cudaLaunchAttribute attrs[2];
     attrs[0].id = cudaLaunchAttributeClusterDimension;

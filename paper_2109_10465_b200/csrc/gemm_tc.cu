@@ -885,9 +885,11 @@ int num_sms() {
     }
     return n;
 }
+// SMs for a persistent grid that leaves `reserve` SMs to a co-running kernel
+int grid_sms(int reserve) { return std::max(2, num_sms() - std::max(0, reserve)); }
 
 template <int KIND>
-void launch(const Params& p, int64_t max_tiles, cudaStream_t st) {
+void launch(const Params& p, int64_t max_tiles, cudaStream_t st, int reserve) {
     static bool attr = false;
     if (!attr) {
         MOE_CUDA_CHECK(cudaFuncSetAttribute(grouped_gemm_kernel<KIND>,
@@ -895,13 +897,13 @@ void launch(const Params& p, int64_t max_tiles, cudaStream_t st) {
                                             static_cast<int>(KCfg<KIND>::smem)));
         attr = true;
     }
-    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms(), max_tiles)));
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(grid_sms(reserve), max_tiles)));
     launch_pdl(grouped_gemm_kernel<KIND>, dim3(grid), dim3(kThreads), KCfg<KIND>::smem, st, p);
 }
 
 
 template <int KIND>
-void launch_pair(const Params& p, int64_t max_pair_tiles, cudaStream_t st) {
+void launch_pair(const Params& p, int64_t max_pair_tiles, cudaStream_t st, int reserve) {
     static bool attr = false;
     if (!attr) {
         MOE_CUDA_CHECK(cudaFuncSetAttribute(pair::gemm2_kernel<KIND>,
@@ -909,7 +911,7 @@ void launch_pair(const Params& p, int64_t max_pair_tiles, cudaStream_t st) {
                                             static_cast<int>(pair::kSmem)));
         attr = true;
     }
-    const int npairs = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(num_sms() / 2, max_pair_tiles)));
+    const int npairs = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(grid_sms(reserve) / 2, max_pair_tiles)));
     launch_pdl(pair::gemm2_kernel<KIND>, dim3(2 * npairs), dim3(kThreads), pair::kSmem, st, p);
 }
 
@@ -974,9 +976,9 @@ void launch_row_gemm_tc(const RowGemmArgs& a, cudaStream_t st) {
     if (use_pair) {
         if (!a.w_nmajor)  // each CTA stages 128 of the 256 weight rows
             p.tmB = tc::make_map(a.W, static_cast<int64_t>(a.El) * a.N, a.K, tc::BK, 128);
-        tc::launch_pair<tc::ROW>(p, (max_tiles + 1) / 2, st);
+        tc::launch_pair<tc::ROW>(p, (max_tiles + 1) / 2, st, a.sm_reserve);
     } else {
-        tc::launch<tc::ROW>(p, max_tiles, st);
+        tc::launch<tc::ROW>(p, max_tiles, st, a.sm_reserve);
     }
 }
 
@@ -1001,9 +1003,9 @@ void launch_wgrad_gemm_tc(const WgradGemmArgs& a, cudaStream_t st) {
     const bool use_pair = (a.M / tc::BM) % 2 == 0 &&
                           (ov >= 0 ? ov == 1 : static_cast<int64_t>(a.ep) * a.cap_pad >= 4 * tc::BK);
     if (use_pair)
-        tc::launch_pair<tc::WGRAD>(p, max_tiles / 2, st);
+        tc::launch_pair<tc::WGRAD>(p, max_tiles / 2, st, a.sm_reserve);
     else
-        tc::launch<tc::WGRAD>(p, max_tiles, st);
+        tc::launch<tc::WGRAD>(p, max_tiles, st, a.sm_reserve);
 }
 
 }  // namespace moe

@@ -14,6 +14,7 @@ void launch_wgrad_gemm_tc(const WgradGemmArgs& a, cudaStream_t st);
 // Force the SIMT path for bf16 as well (testing / A-B comparisons).
 void tc_set_enabled(bool on);
 bool tc_enabled();
+
 namespace tc {
 // 2D TMA tensor map over [rows, cols] row-major elements of `esz` bytes
 CUtensorMap make_map_2d(const void* base, CUtensorMapDataType dt, int esz, int64_t rows, int64_t cols,

@@ -140,6 +140,9 @@ struct RowGemmArgs {
     // rank, [El * cap_pad][N], NVLink-mapped), row (seg % El) * cap_pad + m,
     // instead of C — the combine exchange's copy folded into the epilogue
     void* const* c_peer = nullptr;
+    // SMs left free for a co-running kernel (the jitter prefetch); the
+    // persistent grid uses the rest
+    int sm_reserve = 0;
 };
 template <class T>
 void launch_row_gemm_simt(const RowGemmArgs& a, cudaStream_t st);
@@ -152,6 +155,7 @@ struct WgradGemmArgs {
     const int32_t* counts;
     int64_t M, N;
     int ep, El, cap_pad;
+    int sm_reserve = 0;  // as RowGemmArgs::sm_reserve
 };
 template <class T>
 void launch_wgrad_gemm_simt(const WgradGemmArgs& a, cudaStream_t st);
@@ -161,8 +165,10 @@ void launch_wgrad_gemm_simt(const WgradGemmArgs& a, cudaStream_t st);
 namespace moe {
 // rng.cu: device mt19937_64 jitter stream; returns false if the device
 // generator cannot serve this request (caller then uploads the host stream).
+// max_ctas: the stream is cut into at most that many chunks, one CTA (one SM)
+// each (a generator that co-runs with kernels owning the other SMs)
 bool launch_jitter_noise_device(uint64_t seed, int64_t count, double eps, float* noise,
-                                cudaStream_t st);
+                                cudaStream_t st, int max_ctas = 148);
 // router.cu: balance_loss from explicit probabilities (per-stage API)
 void launch_balance_from_probs(const float* probs, int64_t T, int E, int K,
                                const int32_t* expert_id, double alpha, float* loss,
@@ -296,10 +302,11 @@ bool gate_fused_ok(int d, int E);
 int gate_fused_parts(int64_t T);
 // wsplit [2][E][d]: tf32 hi / lo halves of Wg^T
 void launch_gate_split(const float* wg, float* wsplit, int d, cudaStream_t st);
+// writes P, the decision and per-64-token balance partials [gate_fused_parts][E]
+// (finalize with launch_balance_finalize)
 void launch_gate_fused(const __nv_bfloat16* x, const float* noise, const float* wsplit, int64_t T, int d, int K,
-                       double alpha, float* probs, int32_t* choice, float* gate_prob, float* colsum_part,
-                       int32_t* count_part, uint32_t* flags, float* aux, float* fcoef, int32_t* fcount,
-                       double* term, unsigned* done, cudaStream_t st);
+                       float* probs, int32_t* choice, float* gate_prob, float* colsum_part, int32_t* count_part,
+                       uint32_t* flags, cudaStream_t st);
 }  // namespace moe
 
 namespace moe {

@@ -176,10 +176,11 @@ struct moe_handle {
         for (int b = 0; b < P_NBUF; ++b)
             for (int r = 0; r < 8; ++r)
                 if (ipc && r != rank && peer[b][r]) cudaIpcCloseMemHandle(peer[b][r]);
-        for (cudaEvent_t e : {ev_a, ev_b, ev_c, ev_side, ev_comm, ev_pf, ev_rts})
+        for (cudaEvent_t e : {ev_a, ev_b, ev_c, ev_side, ev_comm, ev_pf, ev_rts, ev_bal})
             if (e) cudaEventDestroy(e);
         if (side) cudaStreamDestroy(side);
         if (comm_stream) cudaStreamDestroy(comm_stream);
+        if (pf_stream) cudaStreamDestroy(pf_stream);
     }
 
     // workspace
@@ -195,7 +196,11 @@ struct moe_handle {
     bool pf_req = false, pf_valid = false;
     uint64_t pf_req_seed = 0, pf_seed = 0;
     int64_t pf_req_count = 0, pf_count = 0;
-    cudaEvent_t ev_pf = nullptr, ev_rts = nullptr;
+    cudaEvent_t ev_pf = nullptr, ev_rts = nullptr, ev_bal = nullptr;
+    bool bal_pending = false;  // balance finalize on the side stream not yet joined
+    cudaStream_t pf_stream = nullptr;  // the next forward's jitter generator (prefetch)
+    int pf_sms = 8;                    // SMs it runs on (MOE_B200_PF_SMS)
+    int pf_reserve = 0;                // SMs the expert GEMMs leave to it right now
     DevMem rts_scratch;         // rts.cu working set
     bool rts_host = false;      // MOE_B200_RTS_HOST=1: RTS order from the host
     DevMem db1_part;            // [rows/32][f] column sums from the dgrad2 epilogue
@@ -440,6 +445,7 @@ bool row_gemm(moe_handle* h, const TIO* A, const TIO* W, TIO* C, const float* bi
     a.w_nmajor = w_nmajor;
     a.epi = epi;
     a.colsum = colsum;
+    a.sm_reserve = h->pf_reserve;
     if constexpr (std::is_same<TIO, __nv_bfloat16>::value) {
         if (tc_row_gemm_supported(a)) {
             a.c_peer = c_peer;
@@ -465,6 +471,7 @@ void wgrad_gemm(moe_handle* h, const TIO* A, const TIO* B, TIO* C, int64_t M, in
     a.ep = nseg_ep;
     a.El = h->El;
     a.cap_pad = h->cap_pad;
+    a.sm_reserve = h->pf_reserve;
     if constexpr (std::is_same<TIO, __nv_bfloat16>::value) {
         if (tc_wgrad_gemm_supported(a)) {
             launch_wgrad_gemm_tc(a, h->stream);
@@ -522,13 +529,21 @@ void route(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, int phas
         if constexpr (std::is_same<TIO, __nv_bfloat16>::value) {
             MOE_CUDA_CHECK(cudaStreamWaitEvent(st, h->ev_b, 0));
             launch_gate_fused(x, jitter ? h->noise.as<float>() : nullptr, h->wsplit.as<float>(), T,
-                              static_cast<int>(h->d), K, h->cfg.balance_coeff, h->probs.as<float>(),
-                              h->choice.as<int32_t>(), h->gate_prob.as<float>(), h->colsum_part.as<float>(),
-                              h->count_part.as<int32_t>(), h->flags.as<uint32_t>(),
-                              aux ? aux : h->aux_scratch.as<float>(), h->fcoef.as<float>(),
-                              h->fcount.as<int32_t>(), h->bal_term.as<double>(), h->bal_done.as<unsigned>(), st);
+                              static_cast<int>(h->d), K, h->probs.as<float>(), h->choice.as<int32_t>(),
+                              h->gate_prob.as<float>(), h->colsum_part.as<float>(), h->count_part.as<int32_t>(),
+                              h->flags.as<uint32_t>(), st);
         }
         h->mark("gate_fused");
+        // aux and f_e / T from the per-64-token partials, on the side stream (the
+        // assignment and the expert GEMMs do not need them); forward_impl joins it
+        MOE_CUDA_CHECK(cudaEventRecord(h->ev_a, st));
+        MOE_CUDA_CHECK(cudaStreamWaitEvent(h->side, h->ev_a, 0));
+        launch_balance_finalize(h->colsum_part.as<float>(), h->count_part.as<int32_t>(), gate_fused_parts(T), T, E,
+                                h->cfg.balance_coeff, aux ? aux : h->aux_scratch.as<float>(), h->fcoef.as<float>(),
+                                h->fcount.as<int32_t>(), h->bal_term.as<double>(), h->bal_done.as<unsigned>(),
+                                h->side);
+        MOE_CUDA_CHECK(cudaEventRecord(h->ev_bal, h->side));
+        h->bal_pending = true;
         h->jitter_on = jitter;
         return;
     }
@@ -635,6 +650,24 @@ void forward_impl(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, c
     }
     assign(h, T, h->choice.as<int32_t>(), h->cap, mode, derive_seed_tag(seed, "assign"),
            h->slot.as<int32_t>(), true);
+    // Jitter stream of the NEXT forward (moe_prefetch_jitter): generated on its
+    // own stream by pf_sms CTAs (one chunk of the stream per SM) while this
+    // call's expert GEMMs (forward and dgrad) run on the other SMs, instead of
+    // heading the next forward on all of them.  This forward's gate has
+    // already consumed its own stream.
+    h->pf_reserve = 0;
+    if (h->pf_req) {
+        MOE_CUDA_CHECK(cudaEventRecord(h->ev_a, st));
+        MOE_CUDA_CHECK(cudaStreamWaitEvent(h->pf_stream, h->ev_a, 0));
+        launch_jitter_noise_device(h->pf_req_seed, h->pf_req_count, h->cfg.jitter_eps, h->noise_pf.as<float>(),
+                                   h->pf_stream, h->pf_sms);
+        MOE_CUDA_CHECK(cudaEventRecord(h->ev_pf, h->pf_stream));
+        h->pf_valid = true;
+        h->pf_seed = h->pf_req_seed;
+        h->pf_count = h->pf_req_count;
+        h->pf_req = false;
+        h->pf_reserve = h->pf_sms;
+    }
     h->mark("assign");
     if (ep == 1) launch_combine_weights(T, E, K, h->gate_prob.as<float>(), h->wts.as<float>(), st);
     // dispatch (routing.cpp:396): un-jittered x into [E, cap_pad, d]
@@ -658,7 +691,7 @@ void forward_impl(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, c
                       nccl_type(h->esz), h->esz}}, false, &sc);
         h->stream = saved;
         MOE_CUDA_CHECK(cudaEventRecord(h->ev_comm, h->comm_stream));
-        balance_finalize(h, T, aux);
+        if (!h->bal_pending) balance_finalize(h, T, aux);  // (the fused gate's runs on the side stream)
         launch_combine_weights(T, E, K, h->gate_prob.as<float>(), h->wts.as<float>(), st);
         MOE_CUDA_CHECK(cudaStreamWaitEvent(st, h->ev_comm, 0));
         counts = h->counts_r.as<int32_t>();
@@ -699,6 +732,10 @@ void forward_impl(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, c
                         h->pos.as<int32_t>(), h->wts.as<float>(), residual ? residual : x, y,
                         h->flags.as<uint32_t>(), st);
     h->mark("combine");
+    if (h->bal_pending) {  // the balance loss (side stream) is part of this call's outputs
+        MOE_CUDA_CHECK(cudaStreamWaitEvent(st, h->ev_bal, 0));
+        h->bal_pending = false;
+    }
     const size_t nk = static_cast<size_t>(T * K);
     if (expert_id)
         MOE_CUDA_CHECK(cudaMemcpyAsync(expert_id, h->choice.p, 4 * nk, cudaMemcpyDeviceToDevice, st));
@@ -823,17 +860,8 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
     }
     launch_colsum_groups<TIO>(h->dOr.as<TIO>(), d, ep, El, h->cap_pad, counts, db2, side);
     if (!db1_fused) launch_colsum_groups<TIO>(h->dH.as<TIO>(), f, ep, El, h->cap_pad, counts, db1, side);
-    if (h->pf_req) {  // jitter stream of the next forward (moe_prefetch_jitter), ~40 KB smem per CTA:
-        // it co-runs with the weight-gradient GEMMs below instead of heading the next forward
-        launch_jitter_noise_device(h->pf_req_seed, h->pf_req_count, h->cfg.jitter_eps,
-                                   h->noise_pf.as<float>(), side);
-        MOE_CUDA_CHECK(cudaEventRecord(h->ev_pf, side));
-        h->pf_valid = true;
-        h->pf_seed = h->pf_req_seed;
-        h->pf_count = h->pf_req_count;
-        h->pf_req = false;
-    }
     MOE_CUDA_CHECK(cudaEventRecord(h->ev_side, side));
+    h->pf_reserve = 0;  // the prefetched jitter stream is done by now: the weight gradients take every SM
     wgrad_gemm<TIO>(h, h->H.as<TIO>(), h->dOr.as<TIO>(), dw2, f, d, counts, ep);
     h->mark("ffn2_wgrad");
     wgrad_gemm<TIO>(h, h->Xr.as<TIO>(), h->dH.as<TIO>(), dw1, d, f, counts, ep);
@@ -1207,7 +1235,10 @@ moe_status moe_create(const moe_router_cfg* cfg, const moe_layer_dims* dims, moe
         }
         MOE_CUDA_CHECK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
         MOE_CUDA_CHECK(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
-        for (cudaEvent_t* e : {&h->ev_a, &h->ev_b, &h->ev_c, &h->ev_side, &h->ev_comm, &h->ev_pf, &h->ev_rts})
+        MOE_CUDA_CHECK(cudaStreamCreateWithFlags(&h->pf_stream, cudaStreamNonBlocking));
+        if (const char* v = std::getenv("MOE_B200_PF_SMS")) h->pf_sms = std::max(1, std::min(64, std::atoi(v)));
+        for (cudaEvent_t* e : {&h->ev_a, &h->ev_b, &h->ev_c, &h->ev_side, &h->ev_comm, &h->ev_pf, &h->ev_rts,
+                                &h->ev_bal})
             MOE_CUDA_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     });
     if (s == MOE_OK) *out = h.release();

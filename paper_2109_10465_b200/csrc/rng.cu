@@ -535,9 +535,9 @@ static const Table& table_for(int64_t J, int P) {
 }
 
 void generate(uint64_t seed, int64_t count, double lo, double hi, float* noise, uint64_t* raw,
-              cudaStream_t st) {
+              cudaStream_t st, int max_ctas = kNumSMs) {
     if (count <= 0) return;
-    const int P = static_cast<int>(std::min<int64_t>(kNumSMs, ceil_div(count, 4096)));
+    const int P = static_cast<int>(std::min<int64_t>(std::max(1, max_ctas), ceil_div(count, 4096)));
     const int64_t J = ceil_div(count, P);
     const Table& tab = table_for(J, P);
     const size_t smem = sizeof(uint64_t) * (kBaseAlloc + N + 16 + kBaseBlocks + 1 + kRing + 2) +
@@ -582,8 +582,8 @@ void generate(uint64_t seed, int64_t count, double lo, double hi, float* noise, 
 
 
 bool launch_jitter_noise_device(uint64_t seed, int64_t count, double eps, float* noise,
-                                cudaStream_t st) {
-    mt::generate(seed, count, 1.0 - eps, 1.0 + eps, noise, nullptr, st);
+                                cudaStream_t st, int max_ctas) {
+    mt::generate(seed, count, 1.0 - eps, 1.0 + eps, noise, nullptr, st, max_ctas);
     return true;
 }
 

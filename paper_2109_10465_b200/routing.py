@@ -606,8 +606,10 @@ class MoeLayer:
         self.handle.ep_bootstrap(all_gather, barrier)
 
     def prefetch_jitter(self, seed: int, tokens: int):
-        """moe_prefetch_jitter: generate the jitter stream of the forward with
-        this seed during the next backward (values unchanged)."""
+        """moe_prefetch_jitter: generate the jitter stream of a later forward
+        with this seed during the next forward/backward call, next to its
+        expert GEMMs (values unchanged).  Call before forward(seed_i) with
+        seed_{i+1}."""
         _check(L.load().moe_prefetch_jitter(self.handle.h, seed, tokens), self.handle.h)
 
 

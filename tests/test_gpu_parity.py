@@ -281,7 +281,8 @@ def test_autograd_adapter_matches_explicit_backward():
 @pytest.mark.gpu
 def test_prefetched_jitter_stream_is_identical():
     """moe_prefetch_jitter: a forward that swaps in the stream generated during
-    the previous backward gives bit-identical outputs and gradients."""
+    the previous call (next to its GEMMs, on MOE_B200_PF_SMS SMs) gives
+    bit-identical outputs and gradients."""
     import torch
     import paper_2109_10465_b200 as M
     T, d, f, E = 512, 256, 512, 16
@@ -296,9 +297,9 @@ def test_prefetched_jitter_stream_is_identical():
     outs = []
     for prefetch in (False, True):
         layer = M.MoeLayer(M.RouterConfig(num_experts=E), T, d, f, torch.bfloat16)
-        layer.forward(x, p, M.Phase.TRAIN, 100)
         if prefetch:
             layer.prefetch_jitter(101, T)
+        layer.forward(x, p, M.Phase.TRAIN, 100)
         layer.backward(dy, 1.0)
         y, aux, dec = layer.forward(x, p, M.Phase.TRAIN, 101)
         gr = layer.backward(dy, 1.0)
