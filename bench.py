@@ -310,7 +310,7 @@ def run_ours(args):
     # seeds (trainer.cpp:146-149), so the next step's seed is known.  With
     # prefetch (default; --no-prefetch turns it off) the next step's jitter
     # stream is generated during this step (moe_prefetch_jitter: MOE_B200_PF_SMS
-    # = 8 CTAs on their own stream next to the forward and dgrad GEMMs, which
+    # = 10 CTAs on their own stream next to the forward and dgrad GEMMs, which
     # leave those SMs free).  Every step still generates exactly one stream.
     step_no = [0]
 
@@ -508,7 +508,7 @@ def run_ours(args):
             "data": "synthetic (random-init weights of the config-3 architecture, U(-1,1) tokens)",
             "config": dict(workload_config(N, E, T), seeds="per step: derive_seed(derive_seed(42, rank), step)",
                            jitter_stream="each step generates the next step's stream next to its expert GEMMs "
-                                         "(moe_prefetch_jitter, 8 SMs)" if args.prefetch
+                                         "(moe_prefetch_jitter, 10 SMs)" if args.prefetch
                            else "generated at the head of each forward"),
             "roofline": roof,
             "roofline_other_families": roof_other,

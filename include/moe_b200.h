@@ -160,7 +160,7 @@ moe_status moe_last_decision_stats(moe_handle* h, int* capacity, int64_t* drop_c
 
 /* Generate the jitter stream of a FUTURE train-phase moe_forward(seed) with
  * `tokens` rows ahead of use: the work is launched by the next moe_forward on
- * this handle (after its gate, on its own stream, as MOE_B200_PF_SMS = 8
+ * this handle (after its gate, on its own stream, as MOE_B200_PF_SMS = 10
  * CTAs — one chunk of the mt19937_64 stream per SM) and co-runs with that
  * call's forward and dgrad expert GEMMs, which leave those SMs free; the
  * matching later forward swaps the buffer in instead of generating on every

@@ -4,8 +4,9 @@
 //
 // A cluster of two CTAs owns 128 tokens; CTA r reduces half of d:
 //
-//   warp 0      TMA producer: raw x (bf16) and jitter (fp32) tiles [128 x 32]
-//               into a 4-deep ring, and the pre-split tf32 hi / lo halves of
+//   warp 0      TMA producer: raw x (bf16) and jitter (fp32) tiles [128 x 64]
+//               (128 B row segments, 128B-swizzled) into a 2-deep ring, and
+//               the pre-split tf32 hi / lo halves of
 //               Wg^T [64 x 32] (128B-swizzled, read by the MMA in place) into
 //               a 3-deep ring
 //   warps 2..5  transform: g = x * noise, 3xTF32 split g = hi + lo, written
@@ -40,17 +41,18 @@ using namespace tc;
 
 constexpr int E = 64;              // experts (TMEM columns per accumulator)
 constexpr int BM = 128;            // tokens per cluster
-constexpr int BK = 32;             // fp32 K elements per step (one 128 B swizzle row)
-constexpr int kRaw = 4;            // raw x / noise ring depth
+constexpr int BK = 32;             // fp32 K elements per MMA step (one 128 B swizzle row)
+constexpr int BKR = 64;            // K elements per raw stage (x rows of 128 B: full DRAM bursts)
+constexpr int kRaw = 2;            // raw x / noise ring depth
 constexpr int kB = 3;              // B (Wg^T hi / lo) ring depth
 constexpr int kOp = 2;             // A-operand ring depth
 constexpr int kNAcc = 4;           // TMEM accumulators
 constexpr int kTw = 8;             // transform warps (two per SM sub-partition)
 constexpr int kThreads = 32 * (2 + kTw);
-constexpr uint32_t kRawX = BM * BK * 2;        //  8 KB bf16 x
-constexpr uint32_t kRawN = BM * BK * 4;        // 16 KB fp32 noise
+constexpr uint32_t kRawX = BM * BKR * 2;       // 16 KB bf16 x   [128 rows x 128 B], 128B swizzle
+constexpr uint32_t kRawN = BM * BKR * 4;       // 32 KB fp32 noise: two [128 x 128 B] halves, swizzled
 constexpr uint32_t kRawB = E * 128;            //  8 KB per hi / lo
-constexpr uint32_t kRawStage = kRawX + kRawN;                // 24 KB
+constexpr uint32_t kRawStage = kRawX + kRawN;                // 48 KB
 constexpr uint32_t kBStage = 2 * kRawB;                      // 16 KB
 constexpr uint32_t kOpStage = 2 * BM * 128;                  // 32 KB (A hi, A lo)
 constexpr uint32_t kRecv = 64 * E * 4;                       // 16 KB: peer's partials for my rows
@@ -116,10 +118,11 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
     const int64_t t0 = static_cast<int64_t>(blockIdx.x >> 1) * BM;
     const int kspan = p.d / 2;
     const int kbase = static_cast<int>(rank) * kspan;
-    const int nsteps = kspan / BK;
-    // every cluster walks its K range from a different starting step, so the
+    const int nsteps = kspan / BK;   // MMA steps
+    const int nraw = kspan / BKR;    // raw stages (two MMA steps each)
+    // every cluster walks its K range from a different starting stage, so the
     // 128 CTAs do not all read the same Wg^T tile from L2 at the same time
-    const int kskew = static_cast<int>((blockIdx.x >> 1) % nsteps);
+    const int kskew = static_cast<int>((blockIdx.x >> 1) % nraw);
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < kRaw; ++i) {
@@ -157,19 +160,25 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
         // ---------------- TMA producer
         if (lane == 0) {
             const uint32_t bytes = kRawX + (p.has_noise ? kRawN : 0);
-            for (int s = 0; s < nsteps; ++s) {
-                const int rs = s % kRaw, bs = s % kB;
-                const int k0 = kbase + ((s + kskew) % nsteps) * BK;
-                if (s >= kRaw) mbar_wait(&raw_empty[rs], ((s / kRaw) - 1) & 1);
+            for (int r = 0; r < nraw; ++r) {
+                const int rs = r % kRaw;
+                const int k0 = kbase + ((r + kskew) % nraw) * BKR;
+                if (r >= kRaw) mbar_wait(&raw_empty[rs], ((r / kRaw) - 1) & 1);
                 uint8_t* st = raw + rs * kRawStage;
                 mbar_expect_tx(&raw_full[rs], bytes);
                 tma_load_2d(&p.tmX, &raw_full[rs], st, k0, static_cast<int32_t>(t0));
-                if (p.has_noise) tma_load_2d(&p.tmN, &raw_full[rs], st + kRawX, k0, static_cast<int32_t>(t0));
-                if (s >= kB) mbar_wait(&b_empty[bs], ((s / kB) - 1) & 1);
-                uint8_t* bt = bst + bs * kBStage;
-                mbar_expect_tx(&b_full[bs], kBStage);
-                tma_load_2d(&p.tmBh, &b_full[bs], bt, k0, 0);
-                tma_load_2d(&p.tmBl, &b_full[bs], bt + kRawB, k0, 0);
+                if (p.has_noise) {
+                    tma_load_2d(&p.tmN, &raw_full[rs], st + kRawX, k0, static_cast<int32_t>(t0));
+                    tma_load_2d(&p.tmN, &raw_full[rs], st + kRawX + kRawN / 2, k0 + BK, static_cast<int32_t>(t0));
+                }
+                for (int h = 0; h < 2; ++h) {
+                    const int s = 2 * r + h, bs = s % kB;
+                    if (s >= kB) mbar_wait(&b_empty[bs], ((s / kB) - 1) & 1);
+                    uint8_t* bt = bst + bs * kBStage;
+                    mbar_expect_tx(&b_full[bs], kBStage);
+                    tma_load_2d(&p.tmBh, &b_full[bs], bt, k0 + h * BK, 0);
+                    tma_load_2d(&p.tmBl, &b_full[bs], bt + kRawB, k0 + h * BK, 0);
+                }
             }
         }
     } else if (warp == 1) {
@@ -203,47 +212,50 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
     } else {
         // ---------------- transform: g = x * noise -> tf32 hi / lo, swizzled K-major
         const int tw = warp - 2;  // rows [16 tw, 16 tw + 16)
-        const int c = lane & 7;
-        for (int s = 0; s < nsteps; ++s) {
-            const int rs = s % kRaw, os = s % kOp;
-            mbar_wait(&raw_full[rs], (s / kRaw) & 1);
-            if (s >= kOp) mbar_wait(&op_empty[os], ((s / kOp) - 1) & 1);
+        const int c = lane & 7;   // 4-element K chunk of the 32-element MMA step
+        for (int r = 0; r < nraw; ++r) {
+            const int rs = r % kRaw;
+            mbar_wait(&raw_full[rs], (r / kRaw) & 1);
             const uint8_t* st = raw + rs * kRawStage;
-            const uint32_t ahi = smem_u32(op + os * kOpStage);
-            const uint32_t alo = ahi + BM * 128;
+            for (int h = 0; h < 2; ++h) {
+                const int s = 2 * r + h, os = s % kOp;
+                if (s >= kOp) mbar_wait(&op_empty[os], ((s / kOp) - 1) & 1);
+                const uint32_t ahi = smem_u32(op + os * kOpStage);
+                const uint32_t alo = ahi + BM * 128;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int r = tw * 16 + (lane >> 3) + 4 * j;
-                const uint2 xv = *reinterpret_cast<const uint2*>(st + r * 64 + c * 8);
-                float g[4] = {__uint_as_float(xv.x << 16), __uint_as_float(xv.x & 0xffff0000u),
-                              __uint_as_float(xv.y << 16), __uint_as_float(xv.y & 0xffff0000u)};
-                if (p.has_noise) {
-                    const float4 nv = *reinterpret_cast<const float4*>(st + kRawX + r * 128 + c * 16);
-                    g[0] *= nv.x; g[1] *= nv.y; g[2] *= nv.z; g[3] *= nv.w;
-                }
-                float h[4], l[4];
-                if (p.probe & 1) {
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) h[q] = l[q] = g[q];
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        h[q] = tf32_rna(g[q]);
-                        l[q] = tf32_rna(g[q] - h[q]);
+                for (int j = 0; j < 4; ++j) {
+                    const int row = tw * 16 + (lane >> 3) + 4 * j;
+                    // x: 128 B rows, 16 B chunk (4h + c/2) swizzled with row % 8
+                    const uint2 xv = *reinterpret_cast<const uint2*>(
+                        st + row * 128 + ((((h << 2) + (c >> 1)) ^ (row & 7)) << 4) + ((c & 1) << 3));
+                    float g[4] = {__uint_as_float(xv.x << 16), __uint_as_float(xv.x & 0xffff0000u),
+                                  __uint_as_float(xv.y << 16), __uint_as_float(xv.y & 0xffff0000u)};
+                    if (p.has_noise) {
+                        const float4 nv = *reinterpret_cast<const float4*>(st + kRawX + h * (kRawN / 2) + swz(row, c));
+                        g[0] *= nv.x; g[1] *= nv.y; g[2] *= nv.z; g[3] *= nv.w;
                     }
+                    float hi[4], lo[4];
+                    if (p.probe & 1) {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) hi[q] = lo[q] = g[q];
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            hi[q] = tf32_rna(g[q]);
+                            lo[q] = tf32_rna(g[q] - hi[q]);
+                        }
+                    }
+                    const uint32_t off = swz(row, c);
+                    sts128(ahi + off, make_uint4(__float_as_uint(hi[0]), __float_as_uint(hi[1]),
+                                                 __float_as_uint(hi[2]), __float_as_uint(hi[3])));
+                    sts128(alo + off, make_uint4(__float_as_uint(lo[0]), __float_as_uint(lo[1]),
+                                                 __float_as_uint(lo[2]), __float_as_uint(lo[3])));
                 }
-                const uint32_t off = swz(r, c);
-                sts128(ahi + off, make_uint4(__float_as_uint(h[0]), __float_as_uint(h[1]), __float_as_uint(h[2]),
-                                             __float_as_uint(h[3])));
-                sts128(alo + off, make_uint4(__float_as_uint(l[0]), __float_as_uint(l[1]), __float_as_uint(l[2]),
-                                             __float_as_uint(l[3])));
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&op_full[os]);
             }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&op_full[os]);
-                mbar_arrive(&raw_empty[rs]);
-            }
+            if (lane == 0) mbar_arrive(&raw_empty[rs]);
         }
     }
 
@@ -370,7 +382,7 @@ __global__ void split_kernel(const float* __restrict__ wg, float* __restrict__ h
 
 }  // namespace gf
 
-bool gate_fused_ok(int d, int E) { return E == gf::E && d % (2 * gf::BK) == 0 && d >= 2 * gf::BK; }
+bool gate_fused_ok(int d, int E) { return E == gf::E && d % (2 * gf::BKR) == 0 && d >= 2 * gf::BKR; }
 
 void launch_gate_split(const float* wg, float* wsplit, int d, cudaStream_t st) {
     launch_pdl(gf::split_kernel, dim3(static_cast<unsigned>(ceil_div(static_cast<int64_t>(d) * gf::E, 256))),
@@ -390,9 +402,9 @@ void launch_gate_fused(const __nv_bfloat16* x, const float* noise, const float* 
         attr = true;
     }
     Params p{};
-    p.tmX = tc::make_map_2d(x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, T, d, BK, BM, false);
+    p.tmX = tc::make_map_2d(x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, T, d, BKR, BM, true);
     p.tmN = tc::make_map_2d(noise ? noise : wsplit, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, noise ? T : E, d, BK,
-                            noise ? BM : E, false);
+                            noise ? BM : E, true);
     p.tmBh = tc::make_map_2d(wsplit, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, E, d, BK, E, true);
     p.tmBl = tc::make_map_2d(wsplit + static_cast<int64_t>(d) * E, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, E, d, BK, E,
                              true);

@@ -199,7 +199,8 @@ struct moe_handle {
     cudaEvent_t ev_pf = nullptr, ev_rts = nullptr, ev_bal = nullptr;
     bool bal_pending = false;  // balance finalize on the side stream not yet joined
     cudaStream_t pf_stream = nullptr;  // the next forward's jitter generator (prefetch)
-    int pf_sms = 8;                    // SMs it runs on (MOE_B200_PF_SMS)
+    int pf_sms = 10;                   // SMs it runs on (MOE_B200_PF_SMS)
+    bool pf_hold = false;              // keep them reserved through the dW2 GEMM
     int pf_reserve = 0;                // SMs the expert GEMMs leave to it right now
     DevMem rts_scratch;         // rts.cu working set
     bool rts_host = false;      // MOE_B200_RTS_HOST=1: RTS order from the host
@@ -861,9 +862,12 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
     launch_colsum_groups<TIO>(h->dOr.as<TIO>(), d, ep, El, h->cap_pad, counts, db2, side);
     if (!db1_fused) launch_colsum_groups<TIO>(h->dH.as<TIO>(), f, ep, El, h->cap_pad, counts, db1, side);
     MOE_CUDA_CHECK(cudaEventRecord(h->ev_side, side));
-    h->pf_reserve = 0;  // the prefetched jitter stream is done by now: the weight gradients take every SM
+    // the prefetched jitter stream is done by now (measured), so the weight
+    // gradients take every SM (MOE_B200_PF_HOLD=1 keeps the reserve for dW2 too)
+    if (!h->pf_hold) h->pf_reserve = 0;
     wgrad_gemm<TIO>(h, h->H.as<TIO>(), h->dOr.as<TIO>(), dw2, f, d, counts, ep);
     h->mark("ffn2_wgrad");
+    h->pf_reserve = 0;
     wgrad_gemm<TIO>(h, h->Xr.as<TIO>(), h->dH.as<TIO>(), dw1, d, f, counts, ep);
     h->mark("ffn1_wgrad");
     // one CTA per SM: (d/128 column tiles) x splits <= 148
@@ -1237,6 +1241,7 @@ moe_status moe_create(const moe_router_cfg* cfg, const moe_layer_dims* dims, moe
         MOE_CUDA_CHECK(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
         MOE_CUDA_CHECK(cudaStreamCreateWithFlags(&h->pf_stream, cudaStreamNonBlocking));
         if (const char* v = std::getenv("MOE_B200_PF_SMS")) h->pf_sms = std::max(1, std::min(64, std::atoi(v)));
+        if (const char* v = std::getenv("MOE_B200_PF_HOLD")) h->pf_hold = v[0] == '1';
         for (cudaEvent_t* e : {&h->ev_a, &h->ev_b, &h->ev_c, &h->ev_side, &h->ev_comm, &h->ev_pf, &h->ev_rts,
                                 &h->ev_bal})
             MOE_CUDA_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
