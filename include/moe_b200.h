@@ -305,6 +305,10 @@ moe_status moe_debug_mt64_chunk_host(uint64_t seed, int64_t J, int c, int64_t n,
 /* testing: the first `count` raw outputs of Rng(seed) from the device
  * generator into device memory out_dev. */
 moe_status moe_debug_mt64_device(uint64_t seed, int64_t count, uint64_t* out_dev);
+/* debugging: %globaltimer phase stamps [ncta][8] of the last fused-gate launch
+ * when MOE_B200_GATE_PROBE has bit 8 (start, after pdl_wait, accumulator
+ * ready, epilogue before / after the cluster barrier, routing done). */
+moe_status moe_debug_gate_stamps(uint64_t* host, int ncta, int* n_out);
 /* testing: Rng(seed).permutation(n) (the RTS order, rng.cpp:94-102) built on
  * the device (rts.cu) into device memory perm_dev [n] uint32. */
 moe_status moe_debug_rts_order(uint64_t seed, int64_t n, uint32_t* perm_dev);

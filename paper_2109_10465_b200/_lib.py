@@ -115,6 +115,7 @@ _SIGS = {
                                   C.c_double, C.c_double, C.c_int64, VP]),
     "moe_debug_jitter_device": (C.c_int, [C.c_uint64, C.c_int64, C.c_double, VP]),
     "moe_debug_rts_order": (C.c_int, [C.c_uint64, C.c_int64, VP]),
+    "moe_debug_gate_stamps": (C.c_int, [VP, C.c_int, C.POINTER(C.c_int)]),
     "moe_debug_gate_tc_logits": (C.c_int, [VP, VP, VP, VP, C.c_int64, C.c_int, C.c_int, C.c_int]),
     "moe_debug_gate_tc_dw": (C.c_int, [VP, VP, VP, VP, C.c_int64, C.c_int, C.c_int, C.c_int]),
     "moe_debug_gate_tc_dx": (C.c_int, [C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int, VP, VP, VP, VP,

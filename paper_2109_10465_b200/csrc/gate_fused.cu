@@ -35,6 +35,7 @@
 #include "tc_ptx.cuh"
 
 namespace moe {
+unsigned long long* g_gate_stamps = nullptr;  // probe 8 (debug)
 namespace gf {
 
 using namespace tc;
@@ -68,7 +69,8 @@ struct __align__(64) Params {
     uint32_t* flags;
     int64_t T;
     int d, K, nparts, has_noise;
-    int probe;  // timing probes (MOE_B200_GATE_PROBE): 1 no split math, 2 no MMA
+    int probe;  // timing probes (MOE_B200_GATE_PROBE): 1 no split math, 2 no MMA, 8 phase timestamps
+    unsigned long long* stamps;  // probe 8: [CTA][8] %globaltimer at phase boundaries
 };
 
 __device__ __forceinline__ float tf32_rna(float v) {
@@ -95,6 +97,12 @@ __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ uint32_t swz(int r, int c) { return r * 128 + ((c ^ (r & 7)) << 4); }
+__device__ __forceinline__ void stamp(const Params& p, int i) {
+    if (!(p.probe & 8)) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.stamps[blockIdx.x * 8 + i] = t;
+}
 
 __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant__ Params p) {
     extern __shared__ uint8_t smem_raw[];
@@ -124,6 +132,7 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
     // 128 CTAs do not all read the same Wg^T tile from L2 at the same time
     const int kskew = static_cast<int>((blockIdx.x >> 1) % nraw);
 
+    if (threadIdx.x == 0) stamp(p, 0);
     if (threadIdx.x == 0) {
         for (int i = 0; i < kRaw; ++i) {
             mbar_init(&raw_full[i], 1);
@@ -155,6 +164,7 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
     const uint32_t tmem = *tslot;
     pdl_wait();  // x, the jitter stream and the split gate weights come from predecessors
     pdl_trigger();
+    if (threadIdx.x == 0) stamp(p, 1);
 
     if (warp == 0) {
         // ---------------- TMA producer
@@ -268,6 +278,7 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
     if (epi) {
         mbar_wait(acc_full, 0);
         tc_fence_after();
+        if (warp == 2 && lane == 0) stamp(p, 2);
 #pragma unroll
         for (int a = 0; a < kNAcc; ++a) {
 #pragma unroll
@@ -286,7 +297,9 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
         }
     }
     __syncwarp();    // producer / MMA lanes rejoin their warps before the aligned cluster barrier
+    if (warp == 2 && lane == 0) stamp(p, 3);
     cluster_sync();  // every partial has landed; both CTAs stay resident until here
+    if (warp == 2 && lane == 0) stamp(p, 4);
     // owner warps: logits = own half + peer half, then the row's routing
     float* sP = reinterpret_cast<float*>(op);                // [64][E + 1] after the loop
     int32_t* sC = reinterpret_cast<int32_t*>(sP + 64 * (E + 1));
@@ -304,32 +317,41 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
             float s = 0.f;
 #pragma unroll
             for (int j = 0; j < E; ++j) {
-                L[j] = expf(L[j] - mx);  // L now holds exp
+                L[j] = __expf(L[j] - mx);  // L now holds exp (ex2.approx: ~2 ulp)
                 s += L[j];
             }
+            const float sinv = 1.0f / s;
             float psum = 0.f;
             int c0 = 0;
+            float b0 = 0.f;  // running best, in registers (no dynamic indexing of L)
 #pragma unroll
             for (int j = 0; j < E; ++j) {
-                const float pj = L[j] / s;
+                const float pj = L[j] * sinv;
                 if (!finite_f(pj)) flag |= MOE_FLAG_NONFINITE_DEV;
                 L[j] = pj;
                 psum += pj;
-                if (j && pj > L[c0]) c0 = j;  // strict >, lowest index wins
+                if (j == 0 || pj > b0) {  // strict >, lowest index wins
+                    b0 = pj;
+                    c0 = j;
+                }
             }
             if (fabsf(psum - 1.0f) > kProbRowTol) flag |= MOE_FLAG_PROB_ROWS_DEV;
             float4* po = reinterpret_cast<float4*>(p.probs + t * E);
 #pragma unroll
             for (int j = 0; j < E; j += 4) po[j / 4] = make_float4(L[j], L[j + 1], L[j + 2], L[j + 3]);
             p.choice[t * p.K] = c0;
-            p.gate_prob[t * p.K] = L[c0];
-            if (p.K == 2) {
+            p.gate_prob[t * p.K] = b0;
+            if (p.K == 2) {  // second choice: initial candidate c0 == 0 ? 1 : 0 (routing.cpp:84-91)
                 int c1 = c0 == 0 ? 1 : 0;
+                float b1 = c0 == 0 ? L[1] : L[0];
 #pragma unroll
                 for (int j = 0; j < E; ++j)
-                    if (j != c0 && L[j] > L[c1]) c1 = j;
+                    if (j != c0 && L[j] > b1) {
+                        b1 = L[j];
+                        c1 = j;
+                    }
                 p.choice[t * p.K + 1] = c1;
-                p.gate_prob[t * p.K + 1] = L[c1];
+                p.gate_prob[t * p.K + 1] = b1;
             }
 #pragma unroll
             for (int j = 0; j < E; ++j) sP[lr * (E + 1) + j] = L[j];
@@ -345,12 +367,14 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
     if (owner_warp) {
         asm volatile("bar.sync 1, 64;" ::: "memory");
         const int j = row & 63;  // expert
-        float cs = 0.f;
+        float cs4[4] = {0.f, 0.f, 0.f, 0.f};  // four interleaved partial sums, fixed order
         int cnt = 0;
+#pragma unroll 4
         for (int r = 0; r < 64; ++r) {
-            cs += sP[r * (E + 1) + j];
+            cs4[r & 3] += sP[r * (E + 1) + j];
             cnt += sC[r] == j;
         }
+        const float cs = (cs4[0] + cs4[1]) + (cs4[2] + cs4[3]);
         const int part = static_cast<int>((t0 >> 6) + rank);
         if (part < p.nparts) {
             p.colsum_part[static_cast<int64_t>(part) * E + j] = cs;
@@ -358,6 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
         }
         flag = __reduce_or_sync(0xffffffffu, flag);
         if (lane == 0 && flag) atomicOr(p.flags, flag);
+        if (lane == 0) stamp(p, 5);
     }
     tc_fence_before();
     __syncthreads();
@@ -424,6 +449,10 @@ void launch_gate_fused(const __nv_bfloat16* x, const float* noise, const float* 
         return e ? std::atoi(e) : 0;
     }();
     p.probe = probe;
+    static unsigned long long* stamps = nullptr;
+    if ((probe & 8) && !stamps) MOE_CUDA_CHECK(cudaMalloc(&stamps, 8 * 8 * 4096));
+    p.stamps = stamps;
+    if (probe & 8) g_gate_stamps = stamps;
     const unsigned tiles = static_cast<unsigned>(ceil_div(T, static_cast<int64_t>(BM)));
     cudaLaunchAttribute attrs[2];
     attrs[0].id = cudaLaunchAttributeClusterDimension;
@@ -441,6 +470,14 @@ void launch_gate_fused(const __nv_bfloat16* x, const float* noise, const float* 
     cfg.numAttrs = 2;
     MOE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gate_kernel, p));
     count_launch();
+}
+
+// debug: copy the probe-8 phase timestamps of the last launch (ncta x 8 u64)
+int gate_fused_stamps(unsigned long long* host, int ncta) {
+    if (!g_gate_stamps) return 0;
+    cudaDeviceSynchronize();
+    cudaMemcpy(host, g_gate_stamps, sizeof(unsigned long long) * 8 * ncta, cudaMemcpyDeviceToHost);
+    return ncta;
 }
 
 }  // namespace moe

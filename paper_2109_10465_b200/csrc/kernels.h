@@ -302,6 +302,7 @@ bool gate_fused_ok(int d, int E);
 int gate_fused_parts(int64_t T);
 // wsplit [2][E][d]: tf32 hi / lo halves of Wg^T
 void launch_gate_split(const float* wg, float* wsplit, int d, cudaStream_t st);
+int gate_fused_stamps(unsigned long long* host, int ncta);  // debug (MOE_B200_GATE_PROBE=8)
 // writes P, the decision and per-64-token balance partials [gate_fused_parts][E]
 // (finalize with launch_balance_finalize)
 void launch_gate_fused(const __nv_bfloat16* x, const float* noise, const float* wsplit, int64_t T, int d, int K,

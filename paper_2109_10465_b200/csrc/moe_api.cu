@@ -1699,6 +1699,10 @@ moe_status moe_debug_gate_tc_dx(int64_t T, int d, int E, int K, int cap_pad, con
         MOE_CUDA_CHECK(cudaDeviceSynchronize());
     });
 }
+moe_status moe_debug_gate_stamps(uint64_t* host, int ncta, int* n_out) {
+    *n_out = moe::gate_fused_stamps(reinterpret_cast<unsigned long long*>(host), ncta);
+    return MOE_OK;
+}
 moe_status moe_debug_rts_order(uint64_t seed, int64_t n, uint32_t* perm_dev) {
     return guarded(nullptr, [&] {
         void* scratch = nullptr;
