@@ -153,6 +153,22 @@ moe_status moe_backward_f64(moe_handle* h, const double* dy, double daux, double
                             double* dw1, double* db1, double* dw2, double* db2, double* dresidual,
                             int accumulate);
 
+/* moe_backward with output options (flags, OR-ed):
+ *   MOE_GRAD_ACCUMULATE   every gradient is ADDED into its buffer (the
+ *                         reference tape's +=, tensor.cpp:31-36 — gradient
+ *                         accumulation over micro-batches); dW1 / dW2 are
+ *                         read-modify-written by the weight-gradient GEMM
+ *                         epilogue itself, the others land in handle
+ *                         scratch and are added after
+ *   MOE_GRAD_WEIGHTS_F32  (bf16 layers) dw1 / dw2 are FLOAT32 buffers,
+ *                         written straight from the fp32 TMEM accumulators
+ *                         (mixed-precision callers with fp32 masters)
+ * flags = 0 is moe_backward. */
+#define MOE_GRAD_ACCUMULATE 0x1u
+#define MOE_GRAD_WEIGHTS_F32 0x2u
+moe_status moe_backward_ex(moe_handle* h, const void* dy, float daux, void* dx, float* dgate_w, void* dw1,
+                           float* db1, void* dw2, float* db2, void* dresidual, unsigned flags);
+
 /* Capacity and kept/dropped statistics of the last forward (host copy;
  * synchronises).  kept_per_expert may be NULL, else [E] int64. */
 moe_status moe_last_decision_stats(moe_handle* h, int* capacity, int64_t* drop_count,

@@ -72,6 +72,7 @@ _SIGS = {
     "moe_forward": (C.c_int, [H, C.c_int64, VP, VP, VP, VP, VP, VP, C.c_int, C.c_uint64, VP, VP, VP,
                               VP, VP, VP]),
     "moe_backward": (C.c_int, [H, VP, C.c_float, VP, VP, VP, VP, VP, VP, VP]),
+    "moe_backward_ex": (C.c_int, [H, VP, C.c_float, VP, VP, VP, VP, VP, VP, VP, C.c_uint]),
     "moe_last_decision_stats": (C.c_int, [H, C.POINTER(C.c_int), C.POINTER(C.c_int64), VP]),
     "moe_gate": (C.c_int, [H, C.c_int64, VP, VP, C.c_int, C.c_uint64, VP, VP, VP]),
     "moe_assign": (C.c_int, [H, C.c_int64, VP, C.c_int, C.c_uint64, VP, C.POINTER(C.c_int)]),

@@ -242,13 +242,21 @@ wgrad_gemm_simt_kernel(WgradGemmArgs a) {
             __syncthreads();
         }
     }
-    T* C = static_cast<T*>(a.C) + (int64_t)g * M * N;
+    const bool add = a.c_mode & 1;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int64_t gm = m0 + tm + i, gn = n0 + tn + j;
-            if (gm < M && gn < N) C[gm * N + gn] = from_f<T>(acc.v[i][j]);
+            if (gm >= M || gn >= N) continue;
+            const int64_t o = (int64_t)g * M * N + gm * N + gn;
+            if (a.c_mode & 2) {  // fp32 output
+                float* C = static_cast<float*>(a.C);
+                C[o] = add ? C[o] + acc.v[i][j] : acc.v[i][j];
+            } else {
+                T* C = static_cast<T*>(a.C);
+                C[o] = from_f<T>(add ? to_f(C[o]) + acc.v[i][j] : acc.v[i][j]);
+            }
         }
 }
 

@@ -83,6 +83,7 @@ struct __align__(64) Params {
     int b_mn;        // ROW: 1 if W is N-major
     float* colsum;   // ROW: optional per-32-row-block column sums of C
     int c_peer;      // ROW: store origin rank r's rows through tmC_peer[r]
+    int c_mode;      // WGRAD: bit 0 accumulate into C, bit 1 C is fp32 (direct stores, no TMA)
     CUtensorMap tmC_peer[8];  // [El*cap_pad, N] slices in the origin ranks' buffers
 };
 
@@ -390,6 +391,38 @@ __global__ void __launch_bounds__(kThreads, 1) grouped_gemm_kernel(const __grid_
                 }
                 if (KIND == ROW && p.colsum)
                     epi_colsum64(f, lane, p.colsum + static_cast<int64_t>(box_row / 32) * p.N + ncol0 + c);
+                if (KIND == WGRAD && p.c_mode) {
+                    // fp32 and / or accumulating dW: this thread's row of 64
+                    // columns straight to global (read-modify-write when accumulating)
+                    const int64_t o = crow * p.N + ncol0 + c;
+                    if (p.c_mode & 2) {
+                        float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.C) + o);
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) {
+                            float4 v = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+                            if (p.c_mode & 1) {
+                                const float4 old = dst[q];
+                                v.x += old.x; v.y += old.y; v.z += old.z; v.w += old.w;
+                            }
+                            dst[q] = v;
+                        }
+                    } else {
+                        uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.C) + o);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const uint4 old = dst[q];
+                            const __nv_bfloat162* ob = reinterpret_cast<const __nv_bfloat162*>(&old);
+                            uint4 u;
+                            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+                            for (int j = 0; j < 4; ++j)
+                                h2[j] = __floats2bfloat162_rn(f[q * 8 + 2 * j] + __low2float(ob[j]),
+                                                              f[q * 8 + 2 * j + 1] + __high2float(ob[j]));
+                            dst[q] = u;
+                        }
+                    }
+                    continue;
+                }
                 // stage the warp's 32 x 64 bf16 block (128B-swizzled rows) and
                 // hand it to the TMA engine; two buffers alternate per warp
                 uint8_t* sbuf = cstage + ((quarter * kEpiBufs + (cbuf % kEpiBufs)) * kStageCBytes);
@@ -998,9 +1031,10 @@ void launch_wgrad_gemm_tc(const WgradGemmArgs& a, cudaStream_t st) {
     p.cap_pad = a.cap_pad;
     p.epi = EPI_NONE;
     p.b_mn = 1;
+    p.c_mode = a.c_mode;
     const int64_t max_tiles = static_cast<int64_t>(a.El) * (a.M / tc::BM) * (a.N / tc::BN);
     const int ov = tc::pair_override();
-    const bool use_pair = (a.M / tc::BM) % 2 == 0 &&
+    const bool use_pair = a.c_mode == 0 && (a.M / tc::BM) % 2 == 0 &&
                           (ov >= 0 ? ov == 1 : static_cast<int64_t>(a.ep) * a.cap_pad >= 4 * tc::BK);
     if (use_pair)
         tc::launch_pair<tc::WGRAD>(p, max_tiles / 2, st, a.sm_reserve);

@@ -156,6 +156,9 @@ struct WgradGemmArgs {
     int64_t M, N;
     int ep, El, cap_pad;
     int sm_reserve = 0;  // as RowGemmArgs::sm_reserve
+    // output mode: bit 0 = accumulate into C (the tape's +=, tensor.cpp:31-36),
+    // bit 1 = C is fp32 (fp32 weight gradients of a bf16 layer)
+    int c_mode = 0;
 };
 template <class T>
 void launch_wgrad_gemm_simt(const WgradGemmArgs& a, cudaStream_t st);
@@ -315,4 +318,9 @@ namespace moe {
 size_t rts_scratch_bytes(int64_t n);
 void launch_rts_order(uint64_t seed, int64_t n, void* scratch, uint32_t* perm, uint32_t* layer_flags,
                       cudaStream_t st);
+}  // namespace moe
+
+namespace moe {
+// dst[i] += src[i] (fp32 math; dst and src both bf16 or both fp32)
+void launch_add_into(void* dst, const void* src, int64_t n, bool bf16, cudaStream_t st);
 }  // namespace moe

@@ -202,6 +202,9 @@ struct moe_handle {
     int pf_sms = 10;                   // SMs it runs on (MOE_B200_PF_SMS)
     bool pf_hold = false;              // keep them reserved through the dW2 GEMM
     int pf_reserve = 0;                // SMs the expert GEMMs leave to it right now
+    int wmode = 0;                     // weight-gradient output mode of this backward (WgradGemmArgs::c_mode)
+    // moe_backward_ex(MOE_GRAD_ACCUMULATE): the non-weight grads land here first
+    DevMem acc_dx, acc_dres, acc_dgw, acc_db1, acc_db2;
     DevMem rts_scratch;         // rts.cu working set
     bool rts_host = false;      // MOE_B200_RTS_HOST=1: RTS order from the host
     DevMem db1_part;            // [rows/32][f] column sums from the dgrad2 epilogue
@@ -460,7 +463,7 @@ bool row_gemm(moe_handle* h, const TIO* A, const TIO* W, TIO* C, const float* bi
 }
 
 template <class TIO>
-void wgrad_gemm(moe_handle* h, const TIO* A, const TIO* B, TIO* C, int64_t M, int64_t N,
+void wgrad_gemm(moe_handle* h, const TIO* A, const TIO* B, void* C, int64_t M, int64_t N,
                 const int32_t* counts, int nseg_ep) {
     WgradGemmArgs a;
     a.A = A;
@@ -473,6 +476,7 @@ void wgrad_gemm(moe_handle* h, const TIO* A, const TIO* B, TIO* C, int64_t M, in
     a.El = h->El;
     a.cap_pad = h->cap_pad;
     a.sm_reserve = h->pf_reserve;
+    a.c_mode = h->wmode;
     if constexpr (std::is_same<TIO, __nv_bfloat16>::value) {
         if (tc_wgrad_gemm_supported(a)) {
             launch_wgrad_gemm_tc(a, h->stream);
@@ -755,8 +759,8 @@ void forward_impl(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, c
 }
 
 template <class TIO>
-void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dgate_w, TIO* dw1,
-                   float* db1, TIO* dw2, float* db2, TIO* dres) {
+void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dgate_w, void* dw1,
+                   float* db1, void* dw2, float* db2, TIO* dres) {
     require(h->fwd_valid, MOE_SHAPE, "moe_backward: no forward context on this handle");
     require(dy && dx && dgate_w && dw1 && db1 && dw2 && db2, MOE_SHAPE, "moe_backward: null tensor");
     require(!h->has_residual || dres, MOE_SHAPE, "moe_backward: dresidual required");
@@ -1360,18 +1364,65 @@ moe_status moe_forward(moe_handle* h, int64_t T, const void* x, const float* gat
 
 moe_status moe_backward(moe_handle* h, const void* dy, float daux, void* dx, float* dgate_w,
                         void* dw1, float* db1, void* dw2, float* db2, void* dresidual) {
+    return moe_backward_ex(h, dy, daux, dx, dgate_w, dw1, db1, dw2, db2, dresidual, 0u);
+}
+
+moe_status moe_backward_ex(moe_handle* h, const void* dy, float daux, void* dx, float* dgate_w, void* dw1,
+                           float* db1, void* dw2, float* db2, void* dresidual, unsigned flags) {
     if (!h) return MOE_SHAPE;
     return guarded(h, [&] {
         require(h->esz != 8, MOE_CONFIG, "moe_backward: float64 handle, use moe_backward_f64");
+        require((flags & ~(MOE_GRAD_ACCUMULATE | MOE_GRAD_WEIGHTS_F32)) == 0u, MOE_CONFIG,
+                "moe_backward_ex: unknown flag");
+        const bool acc = flags & MOE_GRAD_ACCUMULATE;
+        // dW1 / dW2: written or accumulated by the weight-gradient GEMM epilogue itself,
+        // in the activation dtype or (MOE_GRAD_WEIGHTS_F32) in fp32
+        h->wmode = (acc ? 1 : 0) | ((flags & MOE_GRAD_WEIGHTS_F32) && h->esz == 2 ? 2 : 0);
+        struct Reset {
+            moe_handle* h;
+            ~Reset() { h->wmode = 0; }
+        } reset{h};
+        void* udx = dx;
+        void* ures = dresidual;
+        float *udgw = dgate_w, *udb1 = db1, *udb2 = db2;
+        const int64_t T = h->T, d = h->d, f = h->f, E = h->E, El = h->El;
+        if (acc) {  // the other grads go to scratch, then dst += scratch (tensor.cpp:31-36 semantics)
+            require(h->fwd_valid && dx && dgate_w && db1 && db2, MOE_SHAPE, "moe_backward: null tensor");
+            auto need = [](DevMem& m, size_t b) {
+                if (m.bytes < b) {
+                    if (m.p) MOE_CUDA_CHECK(cudaFree(m.p));
+                    m.p = nullptr;
+                    m.alloc(b);
+                }
+            };
+            need(h->acc_dx, h->esz * h->Tmax * d);
+            need(h->acc_dgw, 4 * d * E);
+            need(h->acc_db1, 4 * El * f);
+            need(h->acc_db2, 4 * El * d);
+            dx = h->acc_dx.p;
+            dgate_w = h->acc_dgw.as<float>();
+            db1 = h->acc_db1.as<float>();
+            db2 = h->acc_db2.as<float>();
+            if (dresidual) {
+                need(h->acc_dres, h->esz * h->Tmax * d);
+                dresidual = h->acc_dres.p;
+            }
+        }
         if (h->esz == 2) {
             using B = __nv_bfloat16;
-            backward_impl<B>(h, static_cast<const B*>(dy), daux, static_cast<B*>(dx), dgate_w,
-                             static_cast<B*>(dw1), db1, static_cast<B*>(dw2), db2,
+            backward_impl<B>(h, static_cast<const B*>(dy), daux, static_cast<B*>(dx), dgate_w, dw1, db1, dw2, db2,
                              static_cast<B*>(dresidual));
         } else {
-            backward_impl<float>(h, static_cast<const float*>(dy), daux, static_cast<float*>(dx),
-                                 dgate_w, static_cast<float*>(dw1), db1, static_cast<float*>(dw2),
-                                 db2, static_cast<float*>(dresidual));
+            backward_impl<float>(h, static_cast<const float*>(dy), daux, static_cast<float*>(dx), dgate_w, dw1,
+                                 db1, dw2, db2, static_cast<float*>(dresidual));
+        }
+        if (acc) {
+            const bool bf = h->esz == 2;
+            launch_add_into(udx, dx, T * d, bf, h->stream);
+            if (ures) launch_add_into(ures, dresidual, T * d, bf, h->stream);
+            launch_add_into(udgw, dgate_w, d * E, false, h->stream);
+            launch_add_into(udb1, db1, El * f, false, h->stream);
+            launch_add_into(udb2, db2, El * d, false, h->stream);
         }
     });
 }

@@ -680,4 +680,24 @@ void launch_ep_shape_check(const long long* all_t, int ep, const ShapeCheck& sc,
     launch_pdl(ep_shape_check_kernel, dim3(1), dim3(32), 0, st, all_t, ep, sc);
 }
 
+// dst += src (the accumulate mode of moe_backward_ex for the non-weight grads)
+template <class T>
+__global__ void add_into_kernel(T* __restrict__ dst, const T* __restrict__ src, int64_t n) {
+    pdl_wait();
+    pdl_trigger();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = from_f<T>(to_f(dst[i]) + to_f(src[i]));
+}
+
+void launch_add_into(void* dst, const void* src, int64_t n, bool bf16, cudaStream_t st) {
+    if (n <= 0) return;
+    const unsigned g = (unsigned)std::min<int64_t>(4 * kNumSMs, ceil_div(n, (int64_t)256));
+    if (bf16)
+        launch_pdl(add_into_kernel<__nv_bfloat16>, dim3(g), dim3(256), 0, st, static_cast<__nv_bfloat16*>(dst),
+                   static_cast<const __nv_bfloat16*>(src), n);
+    else
+        launch_pdl(add_into_kernel<float>, dim3(g), dim3(256), 0, st, static_cast<float*>(dst),
+                   static_cast<const float*>(src), n);
+}
+
 }  // namespace moe

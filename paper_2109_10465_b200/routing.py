@@ -561,7 +561,12 @@ class MoeLayer:
         self._gen += 1
         return y, aux, dec
 
-    def backward(self, dy, daux: float = 1.0, check: bool = True, grads=None, accumulate: bool = False):
+    def backward(self, dy, daux: float = 1.0, check: bool = True, grads=None, accumulate: bool = False,
+                 weights_f32: bool = False):
+        """Backward of <dy, y> + daux * aux for the last forward (moe_backward_ex).
+        ``accumulate``: add into ``grads`` instead of writing them (the tape's
+        +=); ``weights_f32``: dw1 / dw2 of a bf16 layer in float32 (fp32
+        masters).  ``grads`` is allocated when None."""
         params, has_res, x = self._saved[:3]
         if tuple(dy.shape) != tuple(x.shape) or dy.dtype != self.dtype:
             raise ShapeError("moe_layer_backward: dy must be [T, d_model] of the layer dtype")
@@ -569,12 +574,13 @@ class MoeLayer:
         dev = dy.device
         f64 = self.dtype == torch.float64
         side = torch.float64 if f64 else torch.float32
+        wdt = torch.float32 if (weights_f32 and self.dtype == torch.bfloat16) else self.dtype
         if grads is None:
             grads = dict(dx=torch.empty_like(dy),
                          dgate_w=torch.empty_like(params.gate_w),
-                         dw1=torch.empty(El, d, f, device=dev, dtype=self.dtype),
+                         dw1=torch.empty(El, d, f, device=dev, dtype=wdt),
                          db1=torch.empty(El, f, device=dev, dtype=side),
-                         dw2=torch.empty(El, f, d, device=dev, dtype=self.dtype),
+                         dw2=torch.empty(El, f, d, device=dev, dtype=wdt),
                          db2=torch.empty(El, d, device=dev, dtype=side),
                          dresidual=torch.empty_like(dy) if has_res else None)
             accumulate = False
@@ -586,12 +592,10 @@ class MoeLayer:
                                              _p(g["db2"]), _p(g.get("dresidual")), int(bool(accumulate))),
                    self.handle.h)
         else:
-            if accumulate:
-                raise ConfigError("moe_layer_backward: accumulate needs the float64 path or "
-                                  "moe_backward_ex")
-            _check(L.load().moe_backward(self.handle.h, _p(dy.contiguous()), float(daux), _p(g["dx"]),
-                                         _p(g["dgate_w"]), _p(g["dw1"]), _p(g["db1"]), _p(g["dw2"]),
-                                         _p(g["db2"]), _p(g.get("dresidual"))), self.handle.h)
+            flags = (1 if accumulate else 0) | (2 if weights_f32 else 0)
+            _check(L.load().moe_backward_ex(self.handle.h, _p(dy.contiguous()), float(daux), _p(g["dx"]),
+                                            _p(g["dgate_w"]), _p(g["dw1"]), _p(g["db1"]), _p(g["dw2"]),
+                                            _p(g["db2"]), _p(g.get("dresidual")), flags), self.handle.h)
         if check:
             self.handle.check()
         return grads

@@ -243,3 +243,42 @@ def test_fused_gate_matches_split_kernels(top_k, T):
     assert float((g1 - g0).abs().max()) <= 2e-6
     assert abs(a1 - a0) <= 1e-6 * max(1.0, abs(a0))
     assert float((y1 - y0).abs().max()) <= 2e-2 * max(1.0, float(y0.abs().max()))
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_backward_accumulate_and_fp32_weight_grads(dtype):
+    """moe_backward_ex: MOE_GRAD_WEIGHTS_F32 writes the very fp32 accumulators
+    the bf16 output rounds (bf16(dW_f32) == dW_bf16 bit for bit), and
+    MOE_GRAD_ACCUMULATE adds every gradient into its buffer (the tape's +=,
+    tensor.cpp:31-36): a second accumulating pass doubles it (exactly where
+    the sum is exact, within one bf16 rounding for bf16 dW)."""
+    import paper_2109_10465_b200 as M
+    T, d, f, E, seed = 1024, 256, 512, 8, 3
+    dt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    r = lambda *s: torch.rand(*s, device="cuda", generator=g) * 2 - 1  # noqa: E731
+    p = M.MoeLayerParams(r(d, E) * 0.1, (r(E, d, f) * 0.05).to(dt), r(E, f) * 0.01, (r(E, f, d) * 0.05).to(dt),
+                         r(E, d) * 0.01)
+    x, dy = r(T, d).to(dt), r(T, d).to(dt)
+    layer = M.MoeLayer(M.RouterConfig(num_experts=E), T, d, f, dt)
+    layer.forward(x, p, M.Phase.TRAIN, seed)
+    g1 = {k: (v.clone() if v is not None else None) for k, v in layer.backward(dy, 1.0).items()}
+    if dtype == "bf16":
+        gf = layer.backward(dy, 1.0, weights_f32=True)
+        assert gf["dw1"].dtype == torch.float32
+        assert torch.equal(gf["dw1"].to(torch.bfloat16), g1["dw1"])
+        assert torch.equal(gf["dw2"].to(torch.bfloat16), g1["dw2"])
+        acc32 = {k: (v.clone() if v is not None else None) for k, v in gf.items()}
+        layer.backward(dy, 1.0, grads=acc32, accumulate=True, weights_f32=True)
+        assert torch.equal(acc32["dw1"], 2 * gf["dw1"]) and torch.equal(acc32["dw2"], 2 * gf["dw2"])
+    acc = {k: (v.clone() if v is not None else None) for k, v in g1.items()}
+    layer.backward(dy, 1.0, grads=acc, accumulate=True)
+    torch.cuda.synchronize()
+    for k in ("dx", "dgate_w", "db1", "db2"):
+        assert torch.equal(acc[k], 2 * g1[k]), k
+    for k in ("dw1", "dw2"):
+        if dtype == "fp32":
+            assert torch.equal(acc[k], 2 * g1[k]), k
+        else:  # bf16(f + bf16(f)): within one bf16 rounding of 2 bf16(f)
+            err = (acc[k].float() - 2 * g1[k].float()).abs()
+            assert bool((err <= 2.0 ** -7 * acc[k].float().abs() + 1e-30).all()), k
