@@ -507,13 +507,15 @@ void route(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, int phas
     // fused gate (gate_fused.cu): one cluster kernel for logits, softmax,
     // top-k and the balance loss; MOE_B200_GATE_FUSED=0 keeps the split kernels
     const bool fused = gtc && h->gate_fused;
-    if (gtc) {  // Wg^T for the logits' B operand, on the side stream next to the jitter generator
+    if (fused) {
+        // tf32 hi / lo halves of Wg^T for the fused gate's B operand: a 4 us kernel
+        // on the main stream (PDL hands over to the gate; a side-stream launch
+        // cost more in cross-stream wait than it overlapped)
+        launch_gate_split(gate_w, h->wsplit.as<float>(), static_cast<int>(h->d), st);
+    } else if (gtc) {  // Wg^T for the logits' B operand, on the side stream next to the jitter generator
         MOE_CUDA_CHECK(cudaEventRecord(h->ev_a, st));
         MOE_CUDA_CHECK(cudaStreamWaitEvent(h->side, h->ev_a, 0));
-        if (fused)
-            launch_gate_split(gate_w, h->wsplit.as<float>(), static_cast<int>(h->d), h->side);
-        else
-            launch_gate2_transpose(gate_w, h->wgt.as<float>(), static_cast<int>(h->d), E, h->side);
+        launch_gate2_transpose(gate_w, h->wgt.as<float>(), static_cast<int>(h->d), E, h->side);
         MOE_CUDA_CHECK(cudaEventRecord(h->ev_b, h->side));
     }
     if (jitter) {
@@ -532,7 +534,6 @@ void route(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, int phas
     }
     if (fused) {
         if constexpr (std::is_same<TIO, __nv_bfloat16>::value) {
-            MOE_CUDA_CHECK(cudaStreamWaitEvent(st, h->ev_b, 0));
             launch_gate_fused(x, jitter ? h->noise.as<float>() : nullptr, h->wsplit.as<float>(), T,
                               static_cast<int>(h->d), K, h->probs.as<float>(), h->choice.as<int32_t>(),
                               h->gate_prob.as<float>(), h->colsum_part.as<float>(), h->count_part.as<int32_t>(),
