@@ -312,6 +312,11 @@ def run_ours(args):
     # stream is generated during this step (moe_prefetch_jitter: MOE_B200_PF_SMS
     # = 10 CTAs on their own stream next to the forward and dgrad GEMMs, which
     # leave those SMs free).  Every step still generates exactly one stream.
+    # Only on one GPU: there the expert GEMMs stream weights from HBM and lose
+    # little with 10 SMs fewer; under expert parallelism they are tensor-bound
+    # and the prefetch costs more than it hides (measured at N=2: 7.59M with,
+    # 8.36M tokens/s without).
+    args.prefetch = args.prefetch and N == 1
     step_no = [0]
 
     def seed_of(i):
