@@ -237,6 +237,8 @@ def stage_bytes(stage, T, d, E, K, n_kept, n_drop):
         return n_kept * d * s + T * d * s + n_drop * d * s
     if stage == "combine_bwd":   # dy read (kept tokens) + dO rows write
         return 2 * n_kept * d * s
+    if stage == "combine_router_bwd":  # dy read once + O rows read (the <dy, O> dots) + dO rows write
+        return 3 * n_kept * d * s
     if stage == "gate_dx":       # dX rows gathered + dx write (+ dy of dropped tokens)
         return n_kept * d * s + T * d * s + n_drop * d * s
     return None
@@ -497,7 +499,7 @@ def run_ours(args):
     gate_parts = [k for k in ("gate_fused", "gate_logits", "softmax_topk", "balance_loss") if k in per_stage]
     groups = {"gate": ["jitter_noise"] + gate_parts, "gate_excl_jitter": gate_parts}
     stage_roof = {}
-    for name in ["gate", "gate_excl_jitter", "assign", "dispatch", "combine", "combine_bwd", "gate_dx"]:
+    for name in ["gate", "gate_excl_jitter", "assign", "dispatch", "combine", "combine_bwd", "combine_router_bwd", "gate_dx"]:
         parts = groups.get(name, [name])
         if not all(p in per_stage for p in parts):
             continue

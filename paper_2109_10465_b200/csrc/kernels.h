@@ -48,6 +48,14 @@ void launch_router_bwd(int64_t T, int d, int E, int K, const TIO* dy, const TIO*
                        const float* probs, const float* fcoef, float daux, float* dL,
                        cudaStream_t st);
 
+// router_bwd with the combine backward (dO rows = w dy[t], expert tails
+// zeroed) folded in: one pass over dy for single-rank layers.
+template <class TIO>
+void launch_router_combine_bwd(int64_t T, int d, int E, int K, const TIO* dy, const TIO* O, int cap_pad,
+                               const int32_t* choice, const int32_t* pos, const float* gate_prob,
+                               const float* probs, const float* fcoef, float daux, const float* w,
+                               const int32_t* kept, TIO* dO, float* dL, cudaStream_t st);
+
 // ---- rng.cu ---------------------------------------------------------------
 // Jitter noise n[i] = lo + (hi-lo) * ((mt() >> 11) * 2^-53) for i in [0, count)
 // of the mt19937_64 stream seeded with `seed` (routing.cpp:62-70), generated

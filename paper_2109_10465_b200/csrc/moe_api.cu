@@ -170,6 +170,7 @@ struct moe_handle {
     bool defer_balance = false;
     bool gemm_tc = false;        // bf16 expert GEMMs on tcgen05 (decided at create)
     bool gate_fused = false;     // bf16 gate in one cluster kernel (gate_fused.cu)
+    bool rcb_fused = true;       // single rank: combine backward folded into router_bwd
     DevMem wsplit;               // [2][E][d] tf32 hi / lo halves of Wg^T
     size_t ws_bytes = 0;         // device bytes allocated by this handle  // forward under EP: the balance loss runs next to the dispatch exchange
     ~moe_handle() {
@@ -775,9 +776,19 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
     h->mark("begin");
     // combine backward: dO rows = w * dy[t]
     TIO* dOloc = static_cast<TIO*>(h->loc(h->dOr, h->dOloc));
-    launch_combine_bwd_gather<TIO>(dy, d, E, K, h->cap_pad, h->row_src.as<int32_t>(),
-                                   h->kept.as<int32_t>(), h->wts.as<float>(), dOloc, st);
-    h->mark("combine_bwd");
+    const bool rcb = ep == 1 && h->rcb_fused && E <= 64;
+    if (rcb) {  // one pass over dy: dO rows and the routing / softmax backward -> dL
+        launch_router_combine_bwd<TIO>(T, static_cast<int>(d), E, K, dy, Oloc, h->cap_pad,
+                                       h->choice.as<int32_t>(), h->pos.as<int32_t>(),
+                                       h->gate_prob.as<float>(), h->probs.as<float>(),
+                                       h->fcoef.as<float>(), daux, h->wts.as<float>(),
+                                       h->kept.as<int32_t>(), dOloc, h->dL.as<float>(), st);
+        h->mark("combine_router_bwd");
+    } else {
+        launch_combine_bwd_gather<TIO>(dy, d, E, K, h->cap_pad, h->row_src.as<int32_t>(),
+                                       h->kept.as<int32_t>(), h->wts.as<float>(), dOloc, st);
+        h->mark("combine_bwd");
+    }
     const int32_t* counts = h->kept.as<int32_t>();
     if (ep > 1) {  // dO to the expert owners on the comm stream, next to the router backward
         MOE_CUDA_CHECK(cudaEventRecord(h->ev_c, st));
@@ -791,11 +802,13 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
         counts = h->counts_r.as<int32_t>();
     }
     // routing weights / balance loss / softmax backward -> dL
-    launch_router_bwd<TIO>(T, static_cast<int>(d), E, K, dy, Oloc, h->cap_pad,
-                           h->choice.as<int32_t>(), h->pos.as<int32_t>(),
-                           h->gate_prob.as<float>(), h->probs.as<float>(), h->fcoef.as<float>(),
-                           daux, h->dL.as<float>(), st);
-    h->mark("router_bwd");
+    if (!rcb) {
+        launch_router_bwd<TIO>(T, static_cast<int>(d), E, K, dy, Oloc, h->cap_pad,
+                               h->choice.as<int32_t>(), h->pos.as<int32_t>(),
+                               h->gate_prob.as<float>(), h->probs.as<float>(), h->fcoef.as<float>(),
+                               daux, h->dL.as<float>(), st);
+        h->mark("router_bwd");
+    }
     if (ep > 1) {
         MOE_CUDA_CHECK(cudaStreamWaitEvent(st, h->ev_comm, 0));
         h->mark("a2a_dO");
@@ -1109,6 +1122,8 @@ void alloc_workspace(moe_handle* h) {
     {
         const char* g = std::getenv("MOE_B200_GATE_FUSED");
         h->gate_fused = es == 2 && gate_fused_ok(static_cast<int>(d), E) && !(g && g[0] == '0');
+        const char* r = std::getenv("MOE_B200_RCB_FUSED");
+        h->rcb_fused = !(r && r[0] == '0');
     }
     MOE_CUDA_CHECK(cudaDeviceSynchronize());
 }

@@ -484,6 +484,164 @@ router_bwd_kernel(int64_t T, int d, int E, int K, const TIO* __restrict__ dy,
     }
 }
 
+// The same with the combine backward folded in (single-rank layers): the warp
+// that reads dy[t] for <dy, O[row_k]> also writes dO[row_k] = w_k dy[t]
+// (permute.cu combine_bwd_gather_kernel), so dy is read once and the two
+// passes become one.  Blocks past the token range zero the expert tails
+// [kept[e], roundup(kept[e], 128)) that the tensor-core tiles read.  The dot
+// products accumulate in the same order as router_bwd_kernel.
+template <class TIO, int V>
+__global__ void __launch_bounds__(256, 4)
+router_combine_bwd_kernel(int64_t T, int d, int E, int K, const TIO* __restrict__ dy,
+                          const TIO* __restrict__ O, int cap_pad, const int32_t* __restrict__ choice,
+                          const int32_t* __restrict__ pos, const float* __restrict__ gate_prob,
+                          const float* __restrict__ probs, const float* __restrict__ fcoef, float daux,
+                          const float* __restrict__ w, const int32_t* __restrict__ kept,
+                          TIO* __restrict__ dO, float* __restrict__ dL) {
+    pdl_wait();
+    pdl_trigger();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t tok_blocks = (T + 7) / 8;
+    if ((int64_t)blockIdx.x >= tok_blocks) {  // expert tails
+        const int64_t q = ((int64_t)blockIdx.x - tok_blocks) * 8 + warp;
+        const int e = (int)(q / kRowAlign);
+        if (e >= E) return;
+        const int n = kept[e];
+        const int64_t p = n + q % kRowAlign;
+        if (p >= round_up_dev(n, kRowAlign)) return;
+        TIO* dst = dO + ((int64_t)e * cap_pad + p) * d;
+        for (int64_t j = (int64_t)lane * V; j < d; j += 32 * V) zero_vec<TIO, V>(dst + j);
+        return;
+    }
+    const int64_t t = (int64_t)blockIdx.x * 8 + warp;
+    if (t >= T) return;
+    int64_t row[2] = {-1, -1};
+    float wk[2] = {0.f, 0.f};
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {  // K <= 2
+        if (k >= K) break;
+        const int32_t p = pos[t * K + k];
+        if (p < 0) continue;
+        row[k] = (int64_t)choice[t * K + k] * cap_pad + p;
+        wk[k] = w[t * K + k];
+    }
+    // the softmax-backward operands, loaded ahead of the row traffic (E <= 64)
+    float pe[2], fe[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const int e = lane + 32 * i;
+        pe[i] = e < E ? __ldg(probs + t * E + e) : 0.f;
+        fe[i] = e < E ? __ldg(fcoef + e) : 0.f;
+    }
+    float acc[2] = {0.f, 0.f};
+    const TIO* dyt = dy + t * d;
+    if constexpr (V * sizeof(TIO) == 16) {
+        // raw 16-byte vectors in registers (kU per operand in flight per lane)
+        constexpr int kU = 4;
+        for (int j0 = lane * V; j0 < d; j0 += 32 * V * kU) {
+            Vec16<TIO> a[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u)
+                if (j0 + u * 32 * V < d) a[u].u = __ldg(reinterpret_cast<const uint4*>(dyt + j0 + u * 32 * V));
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                if (row[k] < 0) continue;
+                const TIO* Ok = O + row[k] * d;
+                TIO* dOk = dO + row[k] * d;
+                Vec16<TIO> b[kU];
+#pragma unroll
+                for (int u = 0; u < kU; ++u)
+                    if (j0 + u * 32 * V < d) b[u].u = __ldg(reinterpret_cast<const uint4*>(Ok + j0 + u * 32 * V));
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    if (j0 + u * 32 * V >= d) continue;
+                    Vec16<TIO> o;
+#pragma unroll
+                    for (int q = 0; q < V; ++q) {
+                        const float av = to_f(a[u].e[q]);
+                        acc[k] = fmaf(av, to_f(b[u].e[q]), acc[k]);
+                        o.e[q] = from_f<TIO>(av * wk[k]);
+                    }
+                    *reinterpret_cast<uint4*>(dOk + j0 + u * 32 * V) = o.u;
+                }
+            }
+        }
+    } else {
+        for (int j = lane * V; j < d; j += 32 * V) {
+            float a[V];
+            load_f<TIO, V>(dyt + j, a);
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                if (row[k] < 0) continue;
+                float b[V], v[V];
+                load_f<TIO, V>(O + row[k] * d + j, b);
+#pragma unroll
+                for (int q = 0; q < V; ++q) {
+                    acc[k] = fmaf(a[q], b[q], acc[k]);
+                    v[q] = a[q] * wk[k];
+                }
+                store_f<TIO, V>(dO + row[k] * d + j, v);
+            }
+        }
+    }
+    float dw[2];
+    dw[0] = row[0] >= 0 ? warp_sum(acc[0]) : 0.f;
+    dw[1] = row[1] >= 0 ? warp_sum(acc[1]) : 0.f;
+    float dp[2];
+    if (K == 1) {
+        dp[0] = (float)E * dw[0];
+        dp[1] = 0.f;
+    } else {
+        const float p0 = gate_prob[t * 2], p1 = gate_prob[t * 2 + 1];
+        const float S = p0 + p1;
+        const float ds = -(dw[0] * p0 + dw[1] * p1) / (S * S);
+        dp[0] = dw[0] / S + ds;
+        dp[1] = dw[1] / S + ds;
+    }
+    const int c0 = choice[t * K];
+    const int c1 = K == 2 ? choice[t * K + 1] : -1;
+    float g[2];
+    float dot = 0.f;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const int e = lane + 32 * i;
+        g[i] = daux * fe[i];
+        if (e == c0) g[i] += dp[0];
+        if (e == c1) g[i] += dp[1];
+        if (e < E) dot = fmaf(g[i], pe[i], dot);
+    }
+    dot = warp_sum(dot);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const int e = lane + 32 * i;
+        if (e < E) dL[t * E + e] = pe[i] * (g[i] - dot);
+    }
+}
+
+template <class TIO>
+void launch_router_combine_bwd(int64_t T, int d, int E, int K, const TIO* dy, const TIO* O, int cap_pad,
+                               const int32_t* choice, const int32_t* pos, const float* gate_prob,
+                               const float* probs, const float* fcoef, float daux, const float* w,
+                               const int32_t* kept, TIO* dO, float* dL, cudaStream_t st) {
+    if (E > 64) throw Status(6, "router_combine_bwd: E <= 64");
+    const unsigned grid = (unsigned)(ceil_div(T, (int64_t)8) + ceil_div((int64_t)E * kRowAlign, (int64_t)8));
+    if (vec_width<TIO>(d) > 1)
+        launch_pdl(router_combine_bwd_kernel<TIO, 16 / sizeof(TIO)>, dim3(grid), dim3(256), 0, st, T, d, E, K,
+                   dy, O, cap_pad, choice, pos, gate_prob, probs, fcoef, daux, w, kept, dO, dL);
+    else
+        launch_pdl(router_combine_bwd_kernel<TIO, 1>, dim3(grid), dim3(256), 0, st, T, d, E, K, dy, O, cap_pad,
+                   choice, pos, gate_prob, probs, fcoef, daux, w, kept, dO, dL);
+}
+template void launch_router_combine_bwd<float>(int64_t, int, int, int, const float*, const float*, int,
+                                               const int32_t*, const int32_t*, const float*, const float*,
+                                               const float*, float, const float*, const int32_t*, float*,
+                                               float*, cudaStream_t);
+template void launch_router_combine_bwd<__nv_bfloat16>(int64_t, int, int, int, const __nv_bfloat16*,
+                                                       const __nv_bfloat16*, int, const int32_t*,
+                                                       const int32_t*, const float*, const float*,
+                                                       const float*, float, const float*, const int32_t*,
+                                                       __nv_bfloat16*, float*, cudaStream_t);
+
 template <class TIO>
 void launch_router_bwd(int64_t T, int d, int E, int K, const TIO* dy, const TIO* O, int cap_pad,
                        const int32_t* choice, const int32_t* pos, const float* gate_prob,
