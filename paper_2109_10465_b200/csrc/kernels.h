@@ -322,6 +322,14 @@ void launch_gate_fused(const __nv_bfloat16* x, const float* noise, const float* 
 }  // namespace moe
 
 namespace moe {
+// gate_bwd.cu: dWg partials [splits][d][E] = (x*noise)^T dL on the tensor
+// cores, TMA-fed with MN-major operands (bf16 path, E == 64, d % 128 == 0)
+bool gate_dw_tma_ok(int d, int E);
+void launch_gate_dw_tma(const __nv_bfloat16* x, const float* noise, const float* dL, float* part, int64_t T, int d,
+                        int splits, cudaStream_t st);
+}  // namespace moe
+
+namespace moe {
 // rts.cu: Rng(seed).permutation(n) on the device (the RTS priority order)
 size_t rts_scratch_bytes(int64_t n);
 void launch_rts_order(uint64_t seed, int64_t n, void* scratch, uint32_t* perm, uint32_t* layer_flags,

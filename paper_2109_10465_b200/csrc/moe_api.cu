@@ -171,6 +171,7 @@ struct moe_handle {
     bool gemm_tc = false;        // bf16 expert GEMMs on tcgen05 (decided at create)
     bool gate_fused = false;     // bf16 gate in one cluster kernel (gate_fused.cu)
     bool rcb_fused = true;       // single rank: combine backward folded into router_bwd
+    bool gate_dw_tma = false;    // dWg by the TMA-fed MN-major kernel (gate_bwd.cu)
     DevMem wsplit;               // [2][E][d] tf32 hi / lo halves of Wg^T
     size_t ws_bytes = 0;         // device bytes allocated by this handle  // forward under EP: the balance loss runs next to the dispatch exchange
     ~moe_handle() {
@@ -892,9 +893,14 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
     const int tc_dw_splits = static_cast<int>(std::max<int64_t>(
         1, std::min<int64_t>({16, kNumSMs / std::max<int64_t>(1, d / 128), (T + 31) / 32})));
     if (gtc) {  // dWg = (x*noise)^T dL on the tensor cores, split-K + fixed-order reduce
-        if constexpr (std::is_same<TIO, __nv_bfloat16>::value)
-            launch_gate_tc_dw<TIO>(x, noise, h->dL.as<float>(), h->dwg_part.as<float>(), T,
-                                   static_cast<int>(d), E, tc_dw_splits, st);
+        if constexpr (std::is_same<TIO, __nv_bfloat16>::value) {
+            if (h->gate_dw_tma)
+                launch_gate_dw_tma(x, noise, h->dL.as<float>(), h->dwg_part.as<float>(), T, static_cast<int>(d),
+                                   tc_dw_splits, st);
+            else
+                launch_gate_tc_dw<TIO>(x, noise, h->dL.as<float>(), h->dwg_part.as<float>(), T,
+                                       static_cast<int>(d), E, tc_dw_splits, st);
+        }
         launch_splitk_reduce(h->dwg_part.as<float>(), tc_dw_splits, d * E, dgate_w, st);
         h->mark("gate_dw");
     }
@@ -1124,6 +1130,8 @@ void alloc_workspace(moe_handle* h) {
         h->gate_fused = es == 2 && gate_fused_ok(static_cast<int>(d), E) && !(g && g[0] == '0');
         const char* r = std::getenv("MOE_B200_RCB_FUSED");
         h->rcb_fused = !(r && r[0] == '0');
+        const char* gd = std::getenv("MOE_B200_GATE_DW_TMA");
+        h->gate_dw_tma = gate_dw_tma_ok(static_cast<int>(d), E) && !(gd && gd[0] == '0');
     }
     MOE_CUDA_CHECK(cudaDeviceSynchronize());
 }
