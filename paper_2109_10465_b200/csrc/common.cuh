@@ -150,4 +150,11 @@ __device__ __forceinline__ float warp_sum(float v) {
 
 __device__ __forceinline__ bool finite_f(float v) { return isfinite(v); }
 
+// round-to-nearest (ties away) to tf32, as the tensor-core gate kernels read fp32 operands
+__device__ __forceinline__ float tf32_rna_dev(float v) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+    return __uint_as_float(r);
+}
+
 }  // namespace moe

@@ -19,6 +19,8 @@ namespace tc {
 // 2D TMA tensor map over [rows, cols] row-major elements of `esz` bytes
 CUtensorMap make_map_2d(const void* base, CUtensorMapDataType dt, int esz, int64_t rows, int64_t cols,
                         int box_cols, int box_rows, bool swizzle128);
+CUtensorMap make_map_2d_swz(const void* base, CUtensorMapDataType dt, int esz, int64_t rows, int64_t cols,
+                            int box_cols, int box_rows, int swizzle_bytes);
 }  // namespace tc
 
 }  // namespace moe

@@ -46,7 +46,7 @@ template <class TIO>
 void launch_router_bwd(int64_t T, int d, int E, int K, const TIO* dy, const TIO* O, int cap_pad,
                        const int32_t* choice, const int32_t* pos, const float* gate_prob,
                        const float* probs, const float* fcoef, float daux, float* dL,
-                       cudaStream_t st);
+                       cudaStream_t st, float* dLr = nullptr);
 
 // router_bwd with the combine backward (dO rows = w dy[t], expert tails
 // zeroed) folded in: one pass over dy for single-rank layers.
@@ -54,7 +54,8 @@ template <class TIO>
 void launch_router_combine_bwd(int64_t T, int d, int E, int K, const TIO* dy, const TIO* O, int cap_pad,
                                const int32_t* choice, const int32_t* pos, const float* gate_prob,
                                const float* probs, const float* fcoef, float daux, const float* w,
-                               const int32_t* kept, TIO* dO, float* dL, cudaStream_t st);
+                               const int32_t* kept, TIO* dO, float* dL, cudaStream_t st,
+                               float* dLr = nullptr);
 
 // ---- rng.cu ---------------------------------------------------------------
 // Jitter noise n[i] = lo + (hi-lo) * ((mt() >> 11) * 2^-53) for i in [0, count)
@@ -327,6 +328,13 @@ namespace moe {
 bool gate_dw_tma_ok(int d, int E);
 void launch_gate_dw_tma(const __nv_bfloat16* x, const float* noise, const float* dL, float* part, int64_t T, int d,
                         int splits, cudaStream_t st);
+// dx = (dLr WgR^T) * noise + dispatch-backward rows (+ dy / dres), persistent
+// TMA-fed tcgen05 kernel; dLr / WgR are the tf32-rounded dL / Wg
+bool gate_dx_tma_ok(int d, int E, int K);
+void launch_gate_round_wg(const float* wg, float* wgr, int d, int E, cudaStream_t st);
+void launch_gate_dx_tma(int64_t T, int d, int K, int cap_pad, const float* dLr, const float* wgr, const float* noise,
+                        const __nv_bfloat16* dX, const int32_t* choice, const int32_t* pos, const __nv_bfloat16* dy,
+                        bool residual_is_x, __nv_bfloat16* dx, __nv_bfloat16* dres, cudaStream_t st);
 }  // namespace moe
 
 namespace moe {

@@ -172,6 +172,7 @@ struct moe_handle {
     bool gate_fused = false;     // bf16 gate in one cluster kernel (gate_fused.cu)
     bool rcb_fused = true;       // single rank: combine backward folded into router_bwd
     bool gate_dw_tma = false;    // dWg by the TMA-fed MN-major kernel (gate_bwd.cu)
+    bool gate_dx_tma = false;    // dx by the persistent TMA-fed kernel (gate_bwd.cu)
     DevMem wsplit;               // [2][E][d] tf32 hi / lo halves of Wg^T
     size_t ws_bytes = 0;         // device bytes allocated by this handle  // forward under EP: the balance loss runs next to the dispatch exchange
     ~moe_handle() {
@@ -190,7 +191,7 @@ struct moe_handle {
     DevMem colsum_part, count_part, fcoef, fcount, aux_scratch, noise, ord, flags;
     DevMem hist, base, gkept;
     DevMem Xloc, Xr, H, Or, Oloc, dOloc, dOr, dH, dXr, dXloc;
-    DevMem dL, dxg, dwg_part, wgt;
+    DevMem dL, dLr, dxg, dwg_part, wgt;
     DevMem bal_term, bal_done;  // balance_finalize per-expert terms + CTA counter
     // jitter stream double buffer: `noise` is the current forward's stream;
     // `noise_pf` receives a stream generated ahead of use (moe_prefetch_jitter)
@@ -778,12 +779,15 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
     // combine backward: dO rows = w * dy[t]
     TIO* dOloc = static_cast<TIO*>(h->loc(h->dOr, h->dOloc));
     const bool rcb = ep == 1 && h->rcb_fused && E <= 64;
+    // the persistent dx kernel reads tf32-rounded dL (written next to dL by the router backward)
+    const bool dx_tma = std::is_same<TIO, __nv_bfloat16>::value && use_gate_tc<TIO>(h) && h->gate_dx_tma;
+    float* dLr = dx_tma ? h->dLr.as<float>() : nullptr;
     if (rcb) {  // one pass over dy: dO rows and the routing / softmax backward -> dL
         launch_router_combine_bwd<TIO>(T, static_cast<int>(d), E, K, dy, Oloc, h->cap_pad,
                                        h->choice.as<int32_t>(), h->pos.as<int32_t>(),
                                        h->gate_prob.as<float>(), h->probs.as<float>(),
                                        h->fcoef.as<float>(), daux, h->wts.as<float>(),
-                                       h->kept.as<int32_t>(), dOloc, h->dL.as<float>(), st);
+                                       h->kept.as<int32_t>(), dOloc, h->dL.as<float>(), st, dLr);
         h->mark("combine_router_bwd");
     } else {
         launch_combine_bwd_gather<TIO>(dy, d, E, K, h->cap_pad, h->row_src.as<int32_t>(),
@@ -807,7 +811,7 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
         launch_router_bwd<TIO>(T, static_cast<int>(d), E, K, dy, Oloc, h->cap_pad,
                                h->choice.as<int32_t>(), h->pos.as<int32_t>(),
                                h->gate_prob.as<float>(), h->probs.as<float>(), h->fcoef.as<float>(),
-                               daux, h->dL.as<float>(), st);
+                               daux, h->dL.as<float>(), st, dLr);
         h->mark("router_bwd");
     }
     if (ep > 1) {
@@ -878,6 +882,7 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
                              h->dxg.as<float>(), side);
         }
     }
+    if (dx_tma) launch_gate_round_wg(h->gate_w, h->wgt.as<float>(), static_cast<int>(d), E, side);
     launch_colsum_groups<TIO>(h->dOr.as<TIO>(), d, ep, El, h->cap_pad, counts, db2, side);
     if (!db1_fused) launch_colsum_groups<TIO>(h->dH.as<TIO>(), f, ep, El, h->cap_pad, counts, db1, side);
     MOE_CUDA_CHECK(cudaEventRecord(h->ev_side, side));
@@ -926,10 +931,15 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
         MOE_CUDA_CHECK(cudaEventRecord(h->ev_comm, h->comm_stream));
     }
     if (gtc) {  // dx = (dL Wg^T) * noise + dispatch bwd + residual, one tensor-core kernel
-        if constexpr (std::is_same<TIO, __nv_bfloat16>::value)
-            launch_gate_tc_dx<TIO>(T, static_cast<int>(d), E, K, h->cap_pad, h->dL.as<float>(),
-                                   h->gate_w, noise, dXloc, h->choice.as<int32_t>(),
-                                   h->pos.as<int32_t>(), dy, !h->has_residual, dx, dres, st);
+        if constexpr (std::is_same<TIO, __nv_bfloat16>::value) {
+            if (dx_tma)
+                launch_gate_dx_tma(T, static_cast<int>(d), K, h->cap_pad, dLr, h->wgt.as<float>(), noise, dXloc,
+                                   h->choice.as<int32_t>(), h->pos.as<int32_t>(), dy, !h->has_residual, dx, dres, st);
+            else
+                launch_gate_tc_dx<TIO>(T, static_cast<int>(d), E, K, h->cap_pad, h->dL.as<float>(),
+                                       h->gate_w, noise, dXloc, h->choice.as<int32_t>(),
+                                       h->pos.as<int32_t>(), dy, !h->has_residual, dx, dres, st);
+        }
     } else if (g2) {  // dx = dxg (side stream, noise applied) + dispatch bwd + residual
         launch_dx_assemble<TIO>(T, d, E, K, h->cap_pad, h->dxg.as<float>(), nullptr, dXloc,
                                 h->choice.as<int32_t>(), h->pos.as<int32_t>(), dy,
@@ -1121,6 +1131,7 @@ void alloc_workspace(moe_handle* h) {
         h->f_fval.alloc(8 * E);
     }
     h->dL.alloc(4 * T * E);
+    h->dLr.alloc(4 * T * E);
     h->dxg.alloc(4 * T * d);
     h->dwg_part.alloc(4 * 16 * d * E);
     h->wgt.alloc(4 * d * E);
@@ -1132,6 +1143,8 @@ void alloc_workspace(moe_handle* h) {
         h->rcb_fused = !(r && r[0] == '0');
         const char* gd = std::getenv("MOE_B200_GATE_DW_TMA");
         h->gate_dw_tma = gate_dw_tma_ok(static_cast<int>(d), E) && !(gd && gd[0] == '0');
+        const char* gx = std::getenv("MOE_B200_GATE_DX_TMA");
+        h->gate_dx_tma = gate_dx_tma_ok(static_cast<int>(d), E, K) && !(gx && gx[0] == '0');
     }
     MOE_CUDA_CHECK(cudaDeviceSynchronize());
 }

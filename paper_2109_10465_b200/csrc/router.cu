@@ -431,7 +431,7 @@ router_bwd_kernel(int64_t T, int d, int E, int K, const TIO* __restrict__ dy,
                   const TIO* __restrict__ O, int cap_pad, const int32_t* __restrict__ choice,
                   const int32_t* __restrict__ pos, const float* __restrict__ gate_prob,
                   const float* __restrict__ probs, const float* __restrict__ fcoef, float daux,
-                  float* __restrict__ dL) {
+                  float* __restrict__ dL, float* __restrict__ dLr) {
     pdl_wait();
     pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -480,7 +480,9 @@ router_bwd_kernel(int64_t T, int d, int E, int K, const TIO* __restrict__ dy,
         float g = daux * fcoef[e];
         if (e == c0) g += dp[0];
         if (e == c1) g += dp[1];
-        dL[t * E + e] = probs[t * E + e] * (g - dot);
+        const float v = probs[t * E + e] * (g - dot);
+        dL[t * E + e] = v;
+        if (dLr) dLr[t * E + e] = tf32_rna_dev(v);
     }
 }
 
@@ -497,7 +499,7 @@ router_combine_bwd_kernel(int64_t T, int d, int E, int K, const TIO* __restrict_
                           const int32_t* __restrict__ pos, const float* __restrict__ gate_prob,
                           const float* __restrict__ probs, const float* __restrict__ fcoef, float daux,
                           const float* __restrict__ w, const int32_t* __restrict__ kept,
-                          TIO* __restrict__ dO, float* __restrict__ dL) {
+                          TIO* __restrict__ dO, float* __restrict__ dL, float* __restrict__ dLr) {
     pdl_wait();
     pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -614,7 +616,11 @@ router_combine_bwd_kernel(int64_t T, int d, int E, int K, const TIO* __restrict_
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
         const int e = lane + 32 * i;
-        if (e < E) dL[t * E + e] = pe[i] * (g[i] - dot);
+        if (e < E) {
+            const float v = pe[i] * (g[i] - dot);
+            dL[t * E + e] = v;
+            if (dLr) dLr[t * E + e] = tf32_rna_dev(v);
+        }
     }
 }
 
@@ -622,46 +628,46 @@ template <class TIO>
 void launch_router_combine_bwd(int64_t T, int d, int E, int K, const TIO* dy, const TIO* O, int cap_pad,
                                const int32_t* choice, const int32_t* pos, const float* gate_prob,
                                const float* probs, const float* fcoef, float daux, const float* w,
-                               const int32_t* kept, TIO* dO, float* dL, cudaStream_t st) {
+                               const int32_t* kept, TIO* dO, float* dL, cudaStream_t st, float* dLr) {
     if (E > 64) throw Status(6, "router_combine_bwd: E <= 64");
     const unsigned grid = (unsigned)(ceil_div(T, (int64_t)8) + ceil_div((int64_t)E * kRowAlign, (int64_t)8));
     if (vec_width<TIO>(d) > 1)
         launch_pdl(router_combine_bwd_kernel<TIO, 16 / sizeof(TIO)>, dim3(grid), dim3(256), 0, st, T, d, E, K,
-                   dy, O, cap_pad, choice, pos, gate_prob, probs, fcoef, daux, w, kept, dO, dL);
+                   dy, O, cap_pad, choice, pos, gate_prob, probs, fcoef, daux, w, kept, dO, dL, dLr);
     else
         launch_pdl(router_combine_bwd_kernel<TIO, 1>, dim3(grid), dim3(256), 0, st, T, d, E, K, dy, O, cap_pad,
-                   choice, pos, gate_prob, probs, fcoef, daux, w, kept, dO, dL);
+                   choice, pos, gate_prob, probs, fcoef, daux, w, kept, dO, dL, dLr);
 }
 template void launch_router_combine_bwd<float>(int64_t, int, int, int, const float*, const float*, int,
                                                const int32_t*, const int32_t*, const float*, const float*,
                                                const float*, float, const float*, const int32_t*, float*,
-                                               float*, cudaStream_t);
+                                               float*, cudaStream_t, float*);
 template void launch_router_combine_bwd<__nv_bfloat16>(int64_t, int, int, int, const __nv_bfloat16*,
                                                        const __nv_bfloat16*, int, const int32_t*,
                                                        const int32_t*, const float*, const float*,
                                                        const float*, float, const float*, const int32_t*,
-                                                       __nv_bfloat16*, float*, cudaStream_t);
+                                                       __nv_bfloat16*, float*, cudaStream_t, float*);
 
 template <class TIO>
 void launch_router_bwd(int64_t T, int d, int E, int K, const TIO* dy, const TIO* O, int cap_pad,
                        const int32_t* choice, const int32_t* pos, const float* gate_prob,
                        const float* probs, const float* fcoef, float daux, float* dL,
-                       cudaStream_t st) {
+                       cudaStream_t st, float* dLr) {
     if (vec_width<TIO>(d) > 1)
         launch_pdl(router_bwd_kernel<TIO, 16 / sizeof(TIO)>, dim3((int)ceil_div(T, 8)), dim3(256), 0, st, 
-            T, d, E, K, dy, O, cap_pad, choice, pos, gate_prob, probs, fcoef, daux, dL);
+            T, d, E, K, dy, O, cap_pad, choice, pos, gate_prob, probs, fcoef, daux, dL, dLr);
     else
         launch_pdl(router_bwd_kernel<TIO, 1>, dim3((int)ceil_div(T, 8)), dim3(256), 0, st, 
-            T, d, E, K, dy, O, cap_pad, choice, pos, gate_prob, probs, fcoef, daux, dL);
+            T, d, E, K, dy, O, cap_pad, choice, pos, gate_prob, probs, fcoef, daux, dL, dLr);
 }
 
 template void launch_router_bwd<float>(int64_t, int, int, int, const float*, const float*, int,
                                        const int32_t*, const int32_t*, const float*, const float*,
-                                       const float*, float, float*, cudaStream_t);
+                                       const float*, float, float*, cudaStream_t, float*);
 template void launch_router_bwd<__nv_bfloat16>(int64_t, int, int, int, const __nv_bfloat16*,
                                                const __nv_bfloat16*, int, const int32_t*,
                                                const int32_t*, const float*, const float*,
-                                               const float*, float, float*, cudaStream_t);
+                                               const float*, float, float*, cudaStream_t, float*);
 
 }  // namespace moe
 
