@@ -48,6 +48,7 @@ constexpr int kMaxGroups = 256;
 
 enum Kind { ROW = 0, WGRAD = 1 };
 
+
 // Pipeline shape per kind.  ROW (fwd/dgrad, K = d or f) is MMA/HBM-streaming:
 // 4 x 48 KB stages keep ~3 stages in flight, enough to cover TMA latency at
 // the MMA's ~94 B/clk consumption (3 stages starved the MMA).  WGRAD (K = the
@@ -84,6 +85,7 @@ struct __align__(64) Params {
     float* colsum;   // ROW: optional per-32-row-block column sums of C
     int c_peer;      // ROW: store origin rank r's rows through tmC_peer[r]
     int c_mode;      // WGRAD: bit 0 accumulate into C, bit 1 C is fp32 (direct stores, no TMA)
+    int tmem_x64;    // epilogue TMEM loads: 1 = one x64 load per chunk, 0 = two x32 loads
     CUtensorMap tmC_peer[8];  // [El*cap_pad, N] slices in the origin ranks' buffers
 };
 
@@ -349,7 +351,12 @@ __global__ void __launch_bounds__(kThreads, 1) grouped_gemm_kernel(const __grid_
 #pragma unroll 1
             for (int c = 0; c < BN; c += 64) {
                 float f[64];
-                {
+                if (p.tmem_x64) {  // one 32x32b.x64 TMEM load (one wait) per 64-column chunk
+                    uint32_t v[64];
+                    tmem_ld64(tbase + c, v);
+#pragma unroll
+                    for (int j = 0; j < 64; ++j) f[j] = __uint_as_float(v[j]);
+                } else {
                     uint32_t v[32];
                     tmem_ld32(tbase + c, v);
 #pragma unroll
@@ -778,7 +785,12 @@ gemm2_kernel(const __grid_constant__ Params p) {
 #pragma unroll 1
             for (int c = 0; c < BN; c += 64) {
                 float f[64];
-                {
+                if (p.tmem_x64) {  // one 32x32b.x64 TMEM load (one wait) per 64-column chunk
+                    uint32_t v[64];
+                    tmem_ld64(tbase + c, v);
+#pragma unroll
+                    for (int j = 0; j < 64; ++j) f[j] = __uint_as_float(v[j]);
+                } else {
                     uint32_t v[32];
                     tmem_ld32(tbase + c, v);
 #pragma unroll
@@ -969,10 +981,24 @@ void launch_pair(const Params& p, int64_t max_pair_tiles, cudaStream_t st, int r
 
 // 2-CTA pairs pay off when the MMA is the bottleneck: every expert has >= 2
 // row tiles (ROW) / K spans >= 256 rows (WGRAD).  MOE_B200_PAIR=0/1 forces.
+static int tmem_x64() {  // MOE_B200_TMEM_X64=0: two x32 TMEM loads per epilogue chunk
+    static int v = [] {
+        const char* e = std::getenv("MOE_B200_TMEM_X64");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
 static int pair_override() {
     static int v = [] {
         const char* e = std::getenv("MOE_B200_PAIR");
         return e ? std::atoi(e) : -1;
+    }();
+    return v;
+}
+static int wg_pair_override() {  // MOE_B200_WG_PAIR=0/1: weight-gradient GEMMs only
+    static int v = [] {
+        const char* e = std::getenv("MOE_B200_WG_PAIR");
+        return e ? std::atoi(e) : pair_override();
     }();
     return v;
 }
@@ -1022,6 +1048,7 @@ void launch_row_gemm_tc(const RowGemmArgs& a, cudaStream_t st) {
             p.tmC_peer[r] = tc::make_map(a.c_peer[r], static_cast<int64_t>(a.El) * a.cap_pad, a.N, 64, 32);
         p.c_peer = 1;
     }
+    p.tmem_x64 = tc::tmem_x64();
     const int64_t max_tiles = rows / tc::BM * (a.N / tc::BN);
     const int ov = tc::pair_override();
     const bool use_pair = ov >= 0 ? ov == 1 : static_cast<int64_t>(a.ep) * a.cap_pad >= 2 * tc::BM;
@@ -1051,8 +1078,9 @@ void launch_wgrad_gemm_tc(const WgradGemmArgs& a, cudaStream_t st) {
     p.epi = EPI_NONE;
     p.b_mn = 1;
     p.c_mode = a.c_mode;
+    p.tmem_x64 = tc::tmem_x64();
     const int64_t max_tiles = static_cast<int64_t>(a.El) * (a.M / tc::BM) * (a.N / tc::BN);
-    const int ov = tc::pair_override();
+    const int ov = tc::wg_pair_override();
     const bool use_pair = a.c_mode == 0 && (a.M / tc::BM) % 2 == 0 &&
                           (ov >= 0 ? ov == 1 : static_cast<int64_t>(a.ep) * a.cap_pad >= 4 * tc::BK);
     if (use_pair)

@@ -45,16 +45,17 @@ int main() {
                                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) { printf("encode failed %d\n", (int)r); return 1; }
         const int MT = rows / 128, NT = cols / 256;
-        for (int bufs : {2, 4}) {
+        for (int grid : {148, 140, 136, 132, 128, 120, 112, 96, 64})
+        for (int bufs : {2}) {
             cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
             cudaFuncSetAttribute(store_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
-            store_tiles<<<148, 128, 65536>>>(tm, MT, NT, bufs);
+            store_tiles<<<grid, 128, 65536>>>(tm, MT, NT, bufs);
             cudaEventRecord(a);
-            for (int k = 0; k < 5; ++k) store_tiles<<<148, 128, 65536>>>(tm, MT, NT, bufs);
+            for (int k = 0; k < 5; ++k) store_tiles<<<grid, 128, 65536>>>(tm, MT, NT, bufs);
             cudaEventRecord(b); cudaEventSynchronize(b);
             float ms; cudaEventElapsedTime(&ms, a, b);
-            printf("%s bufs %d: %.3f ms per pass, %.0f GB/s (%s)\n", shape == 0 ? "dW2 [524288 x 2048]" : "dW1 [131072 x 8192]",
-                   bufs, ms / 5, 5.0 * rows * cols * 2 / (ms / 1e3) / 1e9, cudaGetErrorString(cudaGetLastError()));
+            printf("%s grid %d bufs %d: %.3f ms per pass, %.0f GB/s (%s)\n", shape == 0 ? "dW2 [524288 x 2048]" : "dW1 [131072 x 8192]",
+                   grid, bufs, ms / 5, 5.0 * rows * cols * 2 / (ms / 1e3) / 1e9, cudaGetErrorString(cudaGetLastError()));
         }
         cudaFree(p);
     }
