@@ -10,9 +10,10 @@ import sys
 ORDER = [("gate_kernel", ["gate_fused"]), ("logits_kernel", ["gate_logits"]),
          ("dispatch_gather_kernel", ["dispatch"]),
          ("grouped_gemm_kernel<0>", ["ffn1_fwd", "ffn2_fwd", "ffn2_dgrad", "ffn1_dgrad"]),
+         ("router_combine_bwd_kernel", ["combine_router_bwd"]),
          ("combine_kernel", ["combine"]), ("combine_bwd_gather_kernel", ["combine_bwd"]),
-         ("grouped_gemm_kernel<1>", ["ffn2_wgrad", "ffn1_wgrad"]), ("gtc::dw_kernel", ["gate_dw"]),
-         ("gtc::dx_kernel", ["gate_dx"])]
+         ("grouped_gemm_kernel<1>", ["ffn2_wgrad", "ffn1_wgrad"]), ("dw_kernel", ["gate_dw"]),
+         ("dx_kernel", ["gate_dx"])]
 
 src = sys.argv[1]
 rows = list(csv.reader(open(src)))
