@@ -171,6 +171,8 @@ struct moe_handle {
     bool gemm_tc = false;        // bf16 expert GEMMs on tcgen05 (decided at create)
     bool gate_fused = false;     // bf16 gate in one cluster kernel (gate_fused.cu)
     bool rcb_fused = true;       // single rank: combine backward folded into router_bwd
+    bool rcb_ep = true;          // ... also under EP (MOE_B200_RCB_EP=0: two kernels, dO exchange next to router_bwd)
+    bool dw_early = true;        // EP: gate dW + its all-reduce before the expert backward (MOE_B200_DW_EARLY=0: after)
     bool gate_dw_tma = false;    // dWg by the TMA-fed MN-major kernel (gate_bwd.cu)
     bool gate_dx_tma = false;    // dx by the persistent TMA-fed kernel (gate_bwd.cu)
     DevMem wsplit;               // [2][E][d] tf32 hi / lo halves of Wg^T
@@ -778,7 +780,7 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
     h->mark("begin");
     // combine backward: dO rows = w * dy[t]
     TIO* dOloc = static_cast<TIO*>(h->loc(h->dOr, h->dOloc));
-    const bool rcb = ep == 1 && h->rcb_fused && E <= 64;
+    const bool rcb = (ep == 1 || h->rcb_ep) && h->rcb_fused && E <= 64;
     // the persistent dx kernel reads tf32-rounded dL (written next to dL by the router backward)
     const bool dx_tma = std::is_same<TIO, __nv_bfloat16>::value && use_gate_tc<TIO>(h) && h->gate_dx_tma;
     float* dLr = dx_tma ? h->dLr.as<float>() : nullptr;
@@ -822,6 +824,50 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
     const bool fast = gate_fast_ok(static_cast<int>(d), E);
     const bool g2 = gate2_ok(static_cast<int>(d), E);
     cudaStream_t side = h->side;
+    // gate dW (tensor cores: split-K + fixed-order reduce) and, under EP, its
+    // sum over ranks on the comm stream (the gate is replicated)
+    const bool gtc = use_gate_tc<TIO>(h);
+    // one CTA per SM: (d/128 column tiles) x splits <= 148
+    const int tc_dw_splits = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>({16, kNumSMs / std::max<int64_t>(1, d / 128), (T + 31) / 32})));
+    auto gate_dw = [&] {
+        if constexpr (std::is_same<TIO, __nv_bfloat16>::value) {
+            if (h->gate_dw_tma)
+                launch_gate_dw_tma(x, noise, h->dL.as<float>(), h->dwg_part.as<float>(), T, static_cast<int>(d),
+                                   tc_dw_splits, st);
+            else
+                launch_gate_tc_dw<TIO>(x, noise, h->dL.as<float>(), h->dwg_part.as<float>(), T,
+                                       static_cast<int>(d), E, tc_dw_splits, st);
+        }
+        launch_splitk_reduce(h->dwg_part.as<float>(), tc_dw_splits, d * E, dgate_w, st);
+        h->mark("gate_dw");
+    };
+    auto dwg_allreduce = [&] {
+        MOE_CUDA_CHECK(cudaEventRecord(h->ev_c, st));
+        MOE_CUDA_CHECK(cudaStreamWaitEvent(h->comm_stream, h->ev_c, 0));
+        if (h->ipc) {  // stage, barrier, every rank sums all ranks' copies in rank order (deterministic)
+            cudaStream_t saved = h->stream;
+            h->stream = h->comm_stream;
+            exchange(h, {{dgate_w, h->dwg_x.p, moe_handle::P_DWG, static_cast<size_t>(d * E), ncclFloat32, 4}},
+                     /*local_only=*/true);
+            h->stream = saved;
+            const float* srcs[8] = {};
+            for (int r = 0; r < ep; ++r) srcs[r] = static_cast<const float*>(h->peer[moe_handle::P_DWG][r]);
+            launch_sum_ranks(srcs, ep, d * E, dgate_w, h->comm_stream);
+        } else {
+            NCCL_CHECK(ncclAllReduce(dgate_w, dgate_w, static_cast<size_t>(d * E), ncclFloat32, ncclSum,
+                                     h->comm, h->comm_stream));
+        }
+        MOE_CUDA_CHECK(cudaEventRecord(h->ev_comm, h->comm_stream));
+    };
+    // EP: dW of the gate first, so its all-reduce overlaps the expert backward
+    // instead of trailing the gate dx kernel (one GPU keeps it after the weight
+    // gradients, where the jitter prefetch no longer holds SMs)
+    const bool dw_early = gtc && ep > 1 && h->dw_early;
+    if (dw_early) {
+        gate_dw();
+        dwg_allreduce();
+    }
     // expert backward: dH = (dO W2^T) * [H > 0]; dX = dH W1^T; dW2 = H^T dO; dW1 = X^T dH
     // db1 = colsum(dH) comes out of the dgrad2 epilogue on the tensor-core path
     const bool db1_fused = row_gemm<TIO>(h, h->dOr.as<TIO>(), w2, h->dH.as<TIO>(), nullptr,
@@ -863,7 +909,6 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
     //   epilogue, and on the FMA path dWg = (x*noise)^T dL and
     //   dxg = (dL Wg^T) * noise.  On the tensor-core path the gate GEMMs run on
     //   the main stream after the weight gradients (gate_tc.cu).
-    const bool gtc = use_gate_tc<TIO>(h);
     MOE_CUDA_CHECK(cudaEventRecord(h->ev_a, st));
     MOE_CUDA_CHECK(cudaStreamWaitEvent(side, h->ev_a, 0));
     const int dw_splits = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(1, T / 512)));
@@ -894,42 +939,11 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
     h->pf_reserve = 0;
     wgrad_gemm<TIO>(h, h->Xr.as<TIO>(), h->dH.as<TIO>(), dw1, d, f, counts, ep);
     h->mark("ffn1_wgrad");
-    // one CTA per SM: (d/128 column tiles) x splits <= 148
-    const int tc_dw_splits = static_cast<int>(std::max<int64_t>(
-        1, std::min<int64_t>({16, kNumSMs / std::max<int64_t>(1, d / 128), (T + 31) / 32})));
-    if (gtc) {  // dWg = (x*noise)^T dL on the tensor cores, split-K + fixed-order reduce
-        if constexpr (std::is_same<TIO, __nv_bfloat16>::value) {
-            if (h->gate_dw_tma)
-                launch_gate_dw_tma(x, noise, h->dL.as<float>(), h->dwg_part.as<float>(), T, static_cast<int>(d),
-                                   tc_dw_splits, st);
-            else
-                launch_gate_tc_dw<TIO>(x, noise, h->dL.as<float>(), h->dwg_part.as<float>(), T,
-                                       static_cast<int>(d), E, tc_dw_splits, st);
-        }
-        launch_splitk_reduce(h->dwg_part.as<float>(), tc_dw_splits, d * E, dgate_w, st);
-        h->mark("gate_dw");
-    }
+    if (gtc && !dw_early) gate_dw();
     MOE_CUDA_CHECK(cudaStreamWaitEvent(st, h->ev_side, 0));
     if (ep > 1) MOE_CUDA_CHECK(cudaStreamWaitEvent(st, h->ev_comm, 0));
     h->mark("bwd_join");
-    if (ep > 1) {  // the gate is replicated: sum dWg over ranks on the comm stream, next to gate_dx
-        MOE_CUDA_CHECK(cudaEventRecord(h->ev_c, st));
-        MOE_CUDA_CHECK(cudaStreamWaitEvent(h->comm_stream, h->ev_c, 0));
-        if (h->ipc) {  // stage, barrier, every rank sums all ranks' copies in rank order (deterministic)
-            cudaStream_t saved = h->stream;
-            h->stream = h->comm_stream;
-            exchange(h, {{dgate_w, h->dwg_x.p, moe_handle::P_DWG, static_cast<size_t>(d * E), ncclFloat32, 4}},
-                     /*local_only=*/true);
-            h->stream = saved;
-            const float* srcs[8] = {};
-            for (int r = 0; r < ep; ++r) srcs[r] = static_cast<const float*>(h->peer[moe_handle::P_DWG][r]);
-            launch_sum_ranks(srcs, ep, d * E, dgate_w, h->comm_stream);
-        } else {
-            NCCL_CHECK(ncclAllReduce(dgate_w, dgate_w, static_cast<size_t>(d * E), ncclFloat32, ncclSum,
-                                     h->comm, h->comm_stream));
-        }
-        MOE_CUDA_CHECK(cudaEventRecord(h->ev_comm, h->comm_stream));
-    }
+    if (ep > 1 && !dw_early) dwg_allreduce();
     if (gtc) {  // dx = (dL Wg^T) * noise + dispatch bwd + residual, one tensor-core kernel
         if constexpr (std::is_same<TIO, __nv_bfloat16>::value) {
             if (dx_tma)
@@ -1141,6 +1155,10 @@ void alloc_workspace(moe_handle* h) {
         h->gate_fused = es == 2 && gate_fused_ok(static_cast<int>(d), E) && !(g && g[0] == '0');
         const char* r = std::getenv("MOE_B200_RCB_FUSED");
         h->rcb_fused = !(r && r[0] == '0');
+        const char* re = std::getenv("MOE_B200_RCB_EP");
+        h->rcb_ep = !(re && re[0] == '0');
+        const char* de = std::getenv("MOE_B200_DW_EARLY");
+        h->dw_early = !(de && de[0] == '0');
         const char* gd = std::getenv("MOE_B200_GATE_DW_TMA");
         h->gate_dw_tma = gate_dw_tma_ok(static_cast<int>(d), E) && !(gd && gd[0] == '0');
         const char* gx = std::getenv("MOE_B200_GATE_DX_TMA");
