@@ -314,11 +314,9 @@ def run_ours(args):
     # stream is generated during this step (moe_prefetch_jitter: MOE_B200_PF_SMS
     # = 10 CTAs on their own stream next to the forward and dgrad GEMMs, which
     # leave those SMs free).  Every step still generates exactly one stream.
-    # Only on one GPU: there the expert GEMMs stream weights from HBM and lose
-    # little with 10 SMs fewer; under expert parallelism they are tensor-bound
-    # and the prefetch costs more than it hides (measured at N=2: 7.59M with,
-    # 8.36M tokens/s without).
-    args.prefetch = args.prefetch and N == 1
+    # Under expert parallelism the generator takes 18 SMs in whole TPCs (the
+    # cta_group::2 GEMMs keep their SM pairs): N=2 8.76-8.82M tokens/s with,
+    # 8.23M without (profiles/r02k_ep_prefetch.txt).
     step_no = [0]
 
     def seed_of(i):
@@ -515,7 +513,7 @@ def run_ours(args):
             "data": "synthetic (random-init weights of the config-3 architecture, U(-1,1) tokens)",
             "config": dict(workload_config(N, E, T), seeds="per step: derive_seed(derive_seed(42, rank), step)",
                            jitter_stream="each step generates the next step's stream next to its expert GEMMs "
-                                         "(moe_prefetch_jitter, 10 SMs)" if args.prefetch
+                                         f"(moe_prefetch_jitter, {10 if N == 1 else 18} SMs)" if args.prefetch
                            else "generated at the head of each forward"),
             "roofline": roof,
             "roofline_other_families": roof_other,

@@ -204,7 +204,7 @@ struct moe_handle {
     cudaEvent_t ev_pf = nullptr, ev_rts = nullptr, ev_bal = nullptr;
     bool bal_pending = false;  // balance finalize on the side stream not yet joined
     cudaStream_t pf_stream = nullptr;  // the next forward's jitter generator (prefetch)
-    int pf_sms = 10;                   // SMs it runs on (MOE_B200_PF_SMS)
+    int pf_sms = 0;                    // SMs it runs on (MOE_B200_PF_SMS; 0: 10 on one GPU, 18 under EP)
     bool pf_hold = false;              // keep them reserved through the dW2 GEMM
     int pf_reserve = 0;                // SMs the expert GEMMs leave to it right now
     int wmode = 0;                     // weight-gradient output mode of this backward (WgradGemmArgs::c_mode)
@@ -635,6 +635,14 @@ void set_geometry(moe_handle* h, int64_t T, int phase, int& mode) {
     if (h->cap_pad > h->cap_pad_max) throw Status(MOE_SHAPE, "capacity exceeds workspace");
 }
 
+// SMs of the jitter prefetch: 10 next to one GPU's HBM-bound expert GEMMs;
+// 18 under EP, where the generator must finish inside a shorter window
+// (forward + dgrad of a ~1.9 ms step; N=2 sweep: 12-14 SMs overrun it in some
+// runs, 16-20 give 8.76-8.82M tokens/s vs 8.23M without prefetch, 24 costs
+// the GEMMs more).  Its CTAs hold whole TPCs (rng.cu), so the cta_group::2
+// GEMMs lose SM pairs, not single SMs.
+int pf_sms_of(const moe_handle* h) { return h->pf_sms > 0 ? h->pf_sms : (h->ep > 1 ? 18 : 10); }
+
 template <class TIO>
 void forward_impl(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, const TIO* w1,
                   const float* b1, const TIO* w2, const float* b2, int phase, uint64_t seed,
@@ -671,13 +679,13 @@ void forward_impl(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, c
         MOE_CUDA_CHECK(cudaEventRecord(h->ev_a, st));
         MOE_CUDA_CHECK(cudaStreamWaitEvent(h->pf_stream, h->ev_a, 0));
         launch_jitter_noise_device(h->pf_req_seed, h->pf_req_count, h->cfg.jitter_eps, h->noise_pf.as<float>(),
-                                   h->pf_stream, h->pf_sms);
+                                   h->pf_stream, pf_sms_of(h));
         MOE_CUDA_CHECK(cudaEventRecord(h->ev_pf, h->pf_stream));
         h->pf_valid = true;
         h->pf_seed = h->pf_req_seed;
         h->pf_count = h->pf_req_count;
         h->pf_req = false;
-        h->pf_reserve = h->pf_sms;
+        h->pf_reserve = pf_sms_of(h);
     }
     h->mark("assign");
     if (ep == 1) launch_combine_weights(T, E, K, h->gate_prob.as<float>(), h->wts.as<float>(), st);
@@ -828,8 +836,9 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
     // sum over ranks on the comm stream (the gate is replicated)
     const bool gtc = use_gate_tc<TIO>(h);
     // one CTA per SM: (d/128 column tiles) x splits <= 148
+    // (leaving the jitter prefetch's SMs alone while it may still run)
     const int tc_dw_splits = static_cast<int>(std::max<int64_t>(
-        1, std::min<int64_t>({16, kNumSMs / std::max<int64_t>(1, d / 128), (T + 31) / 32})));
+        1, std::min<int64_t>({16, (kNumSMs - h->pf_reserve) / std::max<int64_t>(1, d / 128), (T + 31) / 32})));
     auto gate_dw = [&] {
         if constexpr (std::is_same<TIO, __nv_bfloat16>::value) {
             if (h->gate_dw_tma)

@@ -558,8 +558,35 @@ void generate(uint64_t seed, int64_t count, double lo, double hi, float* noise, 
     // debug (timing runs only): =1 drops the stores, timing the recurrence alone
     static const bool null_out = timing && std::getenv("MOE_B200_RNG_NULL_OUT") != nullptr;
     if (null_out) noise = nullptr, raw = nullptr;
-    launch_pdl(chunk_kernel, dim3(P), dim3(kChunkThreads), smem, st, init, tab.dev, J, count, lo, hi - lo,
-               noise, raw, timing ? tdbg : nullptr);
+    static const bool pair_tpc = [] {
+        const char* e = std::getenv("MOE_B200_PF_TPC");
+        return !(e && e[0] == '0');
+    }();
+    if (pair_tpc && P < kNumSMs && P % 2 == 0) {
+        // a generator sharing the GPU with persistent GEMMs: CTAs in clusters of
+        // two, so they hold whole TPCs and leave the other TPCs' SM pairs to the
+        // cta_group::2 GEMM kernels
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[1].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(P);
+        cfg.blockDim = dim3(kChunkThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cfg.attrs = at;
+        cfg.numAttrs = 2;
+        MOE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, chunk_kernel, init, static_cast<const uint16_t*>(tab.dev), J, count, lo,
+                                          hi - lo, noise, raw, timing ? tdbg : nullptr));
+        count_launch();
+    } else {
+        launch_pdl(chunk_kernel, dim3(P), dim3(kChunkThreads), smem, st, init, tab.dev, J, count, lo, hi - lo,
+                   noise, raw, timing ? tdbg : nullptr);
+    }
     if (timing) {  // debug: per-phase times averaged over CTAs (synchronises)
         std::vector<unsigned long long> h(8 * static_cast<size_t>(P));
         MOE_CUDA_CHECK(cudaStreamSynchronize(st));
