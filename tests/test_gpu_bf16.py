@@ -282,3 +282,80 @@ def test_backward_accumulate_and_fp32_weight_grads(dtype):
         else:  # bf16(f + bf16(f)): within one bf16 rounding of 2 bf16(f)
             err = (acc[k].float() - 2 * g1[k].float()).abs()
             assert bool((err <= 2.0 ** -7 * acc[k].float().abs() + 1e-30).all()), k
+
+
+@pytest.mark.parametrize("top_k,T,jitter,res", [(1, 8192, True, False), (2, 1000, True, True),
+                                                 (1, 300, False, False), (2, 4096, False, True)])
+def test_gate_backward_tma_kernels_match_previous(top_k, T, jitter, res):
+    """The TMA-fed gate backward kernels (gate_bwd.cu: dWg by 3xBF16 MN-major
+    tcgen05, dx persistent with tf32-rounded dL / Wg) against the kernels they
+    replace (gate_tc.cu, MOE_B200_GATE_DW_TMA=0 / MOE_B200_GATE_DX_TMA=0) on
+    the same forward: top-1 / top-2, with and without jitter, an explicit
+    residual (dres) and ragged token counts (T % 128 != 0).  dx takes the same
+    tf32 products and must agree to bf16 rounding; dWg is now more precise
+    (2^-16 vs 2^-11 per operand), so it agrees to the TF32 kernel's error."""
+    import os
+
+    import paper_2109_10465_b200 as M
+    d, f, E, seed = 2048, 256, 64, 9
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    r = lambda *s: torch.rand(*s, device="cuda", generator=g) * 2 - 1  # noqa: E731
+    p = M.MoeLayerParams(r(d, E) * 0.05, (r(E, d, f) * 0.05).bfloat16(), r(E, f) * 0.01,
+                         (r(E, f, d) * 0.05).bfloat16(), r(E, d) * 0.01)
+    x, dy = r(T, d).bfloat16(), r(T, d).bfloat16()
+    resid = r(T, d).bfloat16() if res else None
+    cfg = M.RouterConfig(num_experts=E, top_k=top_k, jitter_eps=0.01 if jitter else 0.0)
+    outs = []
+    for v in ("1", "0"):
+        os.environ["MOE_B200_GATE_DW_TMA"] = v
+        os.environ["MOE_B200_GATE_DX_TMA"] = v
+        try:
+            layer = M.MoeLayer(cfg, T, d, f, torch.bfloat16)
+        finally:
+            os.environ.pop("MOE_B200_GATE_DW_TMA", None)
+            os.environ.pop("MOE_B200_GATE_DX_TMA", None)
+        layer.forward(x, p, M.Phase.TRAIN, seed, residual=resid)
+        gr = layer.backward(dy, 1.0)
+        torch.cuda.synchronize()
+        outs.append({k: (v_.float().cpu() if v_ is not None else None) for k, v_ in gr.items()})
+    new, old = outs
+    scale = float(old["dx"].abs().max())
+    assert float((new["dx"] - old["dx"]).abs().max()) <= 2.0 ** -7 * scale
+    if res:
+        assert torch.equal(new["dresidual"], old["dresidual"])
+    sw = float(old["dgate_w"].abs().max())
+    assert float((new["dgate_w"] - old["dgate_w"]).abs().max()) <= 2e-3 * sw
+    for k in ("dw1", "dw2", "db1", "db2"):
+        assert torch.equal(new[k], old[k]), k
+
+
+@pytest.mark.parametrize("top_k,T,res", [(1, 8192, False), (2, 1000, True)])
+def test_router_combine_backward_fused_is_bit_identical(top_k, T, res):
+    """router_combine_bwd_kernel (one pass over dy: dO rows, dw = <dy, O>, the
+    routing-weight / balance / softmax backward) against the two kernels it
+    replaces (MOE_B200_RCB_FUSED=0): the same operations in the same order, so
+    every gradient is bit-identical."""
+    import os
+
+    import paper_2109_10465_b200 as M
+    d, f, E, seed = 1024, 512, 64, 4
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    r = lambda *s: torch.rand(*s, device="cuda", generator=g) * 2 - 1  # noqa: E731
+    p = M.MoeLayerParams(r(d, E) * 0.05, (r(E, d, f) * 0.05).bfloat16(), r(E, f) * 0.01,
+                         (r(E, f, d) * 0.05).bfloat16(), r(E, d) * 0.01)
+    x, dy = r(T, d).bfloat16(), r(T, d).bfloat16()
+    resid = r(T, d).bfloat16() if res else None
+    outs = []
+    for v in ("1", "0"):
+        os.environ["MOE_B200_RCB_FUSED"] = v
+        try:
+            layer = M.MoeLayer(M.RouterConfig(num_experts=E, top_k=top_k), T, d, f, torch.bfloat16)
+        finally:
+            os.environ.pop("MOE_B200_RCB_FUSED", None)
+        layer.forward(x, p, M.Phase.TRAIN, seed, residual=resid)
+        gr = layer.backward(dy, 1.0)
+        torch.cuda.synchronize()
+        outs.append({k: (v_.cpu() if v_ is not None else None) for k, v_ in gr.items()})
+    for k, v_ in outs[0].items():
+        if v_ is not None:
+            assert torch.equal(v_, outs[1][k]), k
