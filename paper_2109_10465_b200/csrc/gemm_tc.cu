@@ -60,10 +60,15 @@ enum Kind { ROW = 0, WGRAD = 1 };
 #ifndef MOE_WG_EPIBUFS
 #define MOE_WG_EPIBUFS 2
 #endif
+#ifndef MOE_WG_EPIWARPS
+#define MOE_WG_EPIWARPS 4
+#endif
 template <int KIND> struct KCfg {
     static constexpr int stages = KIND == ROW ? 4 : MOE_WG_STAGES;
     static constexpr int epi_bufs = KIND == ROW ? 1 : MOE_WG_EPIBUFS;
-    static constexpr uint32_t epi_bytes = 4 * epi_bufs * kStageCBytes;
+    static constexpr int epi_warps = KIND == ROW ? 4 : MOE_WG_EPIWARPS;  // 4 or 8 (two per TMEM lane quarter)
+    static constexpr int threads = 64 + 32 * epi_warps;
+    static constexpr uint32_t epi_bytes = epi_warps * epi_bufs * kStageCBytes;
     static constexpr size_t smem = 1024 /*align slack*/ + stages * kStageBytes + epi_bytes +
                                    1024 /*barriers*/ + 4 * (kMaxSegs + 3 * kMaxGroups + 8);
 };
@@ -133,8 +138,9 @@ __device__ __forceinline__ void row_tile(const Params& p, const Sched& s, int NT
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(kThreads, 1) grouped_gemm_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(KCfg<KIND>::threads, 1) grouped_gemm_kernel(const __grid_constant__ Params p) {
     constexpr int kStages = KCfg<KIND>::stages;
+    constexpr int kEpiW = KCfg<KIND>::epi_warps;
     constexpr int kEpiBufs = KCfg<KIND>::epi_bufs;
     constexpr uint32_t kEpiBytes = KCfg<KIND>::epi_bytes;
     extern __shared__ uint8_t smem_raw[];
@@ -162,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1) grouped_gemm_kernel(const __grid_
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 128);
+            mbar_init(&tempty[i], 32 * kEpiW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         prefetch_tmap(&p.tmA);
@@ -308,8 +314,12 @@ __global__ void __launch_bounds__(kThreads, 1) grouped_gemm_kernel(const __grid_
             }
         }
     } else {
-        // ================= epilogue (warps 2..5) =================
+        // ================= epilogue (warps 2..) =================
         const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+        const int ew = warp - 2;
+        // with 8 epilogue warps, two per lane quarter split the tile's columns
+        const int c_begin = kEpiW == 8 ? (ew >> 2) * (BN / 2) : 0;
+        const int c_end = kEpiW == 8 ? c_begin + BN / 2 : BN;
         const int row_in_tile = quarter * 32 + lane;
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -349,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1) grouped_gemm_kernel(const __grid_
             const CUtensorMap* out_map = peer_r >= 0 ? &p.tmC_peer[peer_r] : &p.tmC;
             const int32_t out_row = peer_r >= 0 ? box_row - peer_r * slice_rows : box_row;
 #pragma unroll 1
-            for (int c = 0; c < BN; c += 64) {
+            for (int c = c_begin; c < c_end; c += 64) {
                 float f[64];
                 if (p.tmem_x64) {  // one 32x32b.x64 TMEM load (one wait) per 64-column chunk
                     uint32_t v[64];
@@ -365,7 +375,7 @@ __global__ void __launch_bounds__(kThreads, 1) grouped_gemm_kernel(const __grid_
 #pragma unroll
                     for (int j = 0; j < 32; ++j) f[32 + j] = __uint_as_float(v[j]);
                 }
-                if (c + 64 == BN) {  // accumulator fully read: MMA may reuse it
+                if (c + 64 == c_end) {  // accumulator fully read: MMA may reuse it
                     tc_fence_before();
                     mbar_arrive(&tempty[acc]);
                 }
@@ -432,7 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1) grouped_gemm_kernel(const __grid_
                 }
                 // stage the warp's 32 x 64 bf16 block (128B-swizzled rows) and
                 // hand it to the TMA engine; two buffers alternate per warp
-                uint8_t* sbuf = cstage + ((quarter * kEpiBufs + (cbuf % kEpiBufs)) * kStageCBytes);
+                uint8_t* sbuf = cstage + ((ew * kEpiBufs + (cbuf % kEpiBufs)) * kStageCBytes);
                 if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kEpiBufs - 1) : "memory");
                 __syncwarp();
 #pragma unroll
@@ -962,7 +972,7 @@ void launch(const Params& p, int64_t max_tiles, cudaStream_t st, int reserve) {
         attr = true;
     }
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(grid_sms(reserve), max_tiles)));
-    launch_pdl(grouped_gemm_kernel<KIND>, dim3(grid), dim3(kThreads), KCfg<KIND>::smem, st, p);
+    launch_pdl(grouped_gemm_kernel<KIND>, dim3(grid), dim3(KCfg<KIND>::threads), KCfg<KIND>::smem, st, p);
 }
 
 
