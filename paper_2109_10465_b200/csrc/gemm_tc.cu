@@ -91,6 +91,7 @@ struct __align__(64) Params {
     int c_peer;      // ROW: store origin rank r's rows through tmC_peer[r]
     int c_mode;      // WGRAD: bit 0 accumulate into C, bit 1 C is fp32 (direct stores, no TMA)
     int tmem_x64;    // epilogue TMEM loads: 1 = one x64 load per chunk, 0 = two x32 loads
+    uint64_t* relu_bits;  // ROW: ReLU mask bits [rows][N/64] (written by EPI_BIAS_RELU, read by EPI_RELU_MASK)
     CUtensorMap tmC_peer[8];  // [El*cap_pad, N] slices in the origin ranks' buffers
 };
 
@@ -395,14 +396,22 @@ __global__ void __launch_bounds__(KCfg<KIND>::threads, 1) grouped_gemm_kernel(co
                             for (int j = 0; j < 64; ++j) f[j] = f[j] > 0.f ? f[j] : 0.f;
                         }
                     } else if (p.epi == EPI_RELU_MASK) {
-                        const uint4* mp = reinterpret_cast<const uint4*>(p.mask + crow * p.N + ncol0 + c);
+                        if (p.relu_bits) {  // 64 mask bits of this row and chunk
+                            const uint64_t mb = __ldg(reinterpret_cast<const unsigned long long*>(
+                                p.relu_bits + crow * (p.N / 64) + (ncol0 + c) / 64));
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            uint4 u = __ldg(mp + q);
-                            const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u);
+                            for (int j = 0; j < 64; ++j)
+                                if (!((mb >> j) & 1ull)) f[j] = 0.f;
+                        } else {
+                            const uint4* mp = reinterpret_cast<const uint4*>(p.mask + crow * p.N + ncol0 + c);
 #pragma unroll
-                            for (int j = 0; j < 8; ++j)
-                                if (!(__bfloat162float(h[j]) > 0.f)) f[q * 8 + j] = 0.f;
+                            for (int q = 0; q < 8; ++q) {
+                                uint4 u = __ldg(mp + q);
+                                const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+                                for (int j = 0; j < 8; ++j)
+                                    if (!(__bfloat162float(h[j]) > 0.f)) f[q * 8 + j] = 0.f;
+                            }
                         }
                     }
                 }
@@ -445,13 +454,38 @@ __global__ void __launch_bounds__(KCfg<KIND>::threads, 1) grouped_gemm_kernel(co
                 uint8_t* sbuf = cstage + ((ew * kEpiBufs + (cbuf % kEpiBufs)) * kStageCBytes);
                 if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kEpiBufs - 1) : "memory");
                 __syncwarp();
+                bool staged = false;
+                if constexpr (KIND == ROW) {
+                    if (p.relu_bits && p.epi == EPI_BIAS_RELU) {  // the ReLU mask as bits for dgrad2
+                        uint64_t mb = 0;
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    uint4 u;
-                    __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+                        for (int q = 0; q < 8; ++q) {
+                            uint4 u;
+                            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) h2[j] = __floats2bfloat162_rn(f[q * 8 + 2 * j], f[q * 8 + 2 * j + 1]);
-                    sts128(smem_u32(sbuf) + lane * 128 + ((q ^ (lane & 7)) << 4), u);
+                            for (int j = 0; j < 4; ++j)
+                                h2[j] = __floats2bfloat162_rn(f[q * 8 + 2 * j], f[q * 8 + 2 * j + 1]);
+                            const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {  // stored value > 0 (ReLU output: sign bit clear)
+                                mb |= static_cast<uint64_t>((w4[j] & 0xffffu) != 0u) << (q * 8 + 2 * j);
+                                mb |= static_cast<uint64_t>((w4[j] >> 16) != 0u) << (q * 8 + 2 * j + 1);
+                            }
+                            sts128(smem_u32(sbuf) + lane * 128 + ((q ^ (lane & 7)) << 4), u);
+                        }
+                        p.relu_bits[crow * (p.N / 64) + (ncol0 + c) / 64] = mb;
+                        staged = true;
+                    }
+                }
+                if (!staged) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        uint4 u;
+                        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) h2[j] = __floats2bfloat162_rn(f[q * 8 + 2 * j], f[q * 8 + 2 * j + 1]);
+                        sts128(smem_u32(sbuf) + lane * 128 + ((q ^ (lane & 7)) << 4), u);
+                    }
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
@@ -830,14 +864,22 @@ gemm2_kernel(const __grid_constant__ Params p) {
                             for (int j = 0; j < 64; ++j) f[j] = f[j] > 0.f ? f[j] : 0.f;
                         }
                     } else if (p.epi == EPI_RELU_MASK) {
-                        const uint4* mp = reinterpret_cast<const uint4*>(p.mask + crow * p.N + ncol0 + c);
+                        if (p.relu_bits) {  // 64 mask bits of this row and chunk
+                            const uint64_t mb = __ldg(reinterpret_cast<const unsigned long long*>(
+                                p.relu_bits + crow * (p.N / 64) + (ncol0 + c) / 64));
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            uint4 u = __ldg(mp + q);
-                            const __nv_bfloat16* hh = reinterpret_cast<const __nv_bfloat16*>(&u);
+                            for (int j = 0; j < 64; ++j)
+                                if (!((mb >> j) & 1ull)) f[j] = 0.f;
+                        } else {
+                            const uint4* mp = reinterpret_cast<const uint4*>(p.mask + crow * p.N + ncol0 + c);
 #pragma unroll
-                            for (int j = 0; j < 8; ++j)
-                                if (!(__bfloat162float(hh[j]) > 0.f)) f[q * 8 + j] = 0.f;
+                            for (int q = 0; q < 8; ++q) {
+                                uint4 u = __ldg(mp + q);
+                                const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+                                for (int j = 0; j < 8; ++j)
+                                    if (!(__bfloat162float(h[j]) > 0.f)) f[q * 8 + j] = 0.f;
+                            }
                         }
                     }
                 }
@@ -846,13 +888,38 @@ gemm2_kernel(const __grid_constant__ Params p) {
                 uint8_t* sbuf = cstage + quarter * kStageCBytes;
                 if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 __syncwarp();
+                bool staged = false;
+                if constexpr (KIND == ROW) {
+                    if (p.relu_bits && p.epi == EPI_BIAS_RELU) {  // the ReLU mask as bits for dgrad2
+                        uint64_t mb = 0;
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    uint4 u;
-                    __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+                        for (int q = 0; q < 8; ++q) {
+                            uint4 u;
+                            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) h2[j] = __floats2bfloat162_rn(f[q * 8 + 2 * j], f[q * 8 + 2 * j + 1]);
-                    sts128(smem_u32(sbuf) + lane * 128 + ((q ^ (lane & 7)) << 4), u);
+                            for (int j = 0; j < 4; ++j)
+                                h2[j] = __floats2bfloat162_rn(f[q * 8 + 2 * j], f[q * 8 + 2 * j + 1]);
+                            const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {  // stored value > 0 (ReLU output: sign bit clear)
+                                mb |= static_cast<uint64_t>((w4[j] & 0xffffu) != 0u) << (q * 8 + 2 * j);
+                                mb |= static_cast<uint64_t>((w4[j] >> 16) != 0u) << (q * 8 + 2 * j + 1);
+                            }
+                            sts128(smem_u32(sbuf) + lane * 128 + ((q ^ (lane & 7)) << 4), u);
+                        }
+                        p.relu_bits[crow * (p.N / 64) + (ncol0 + c) / 64] = mb;
+                        staged = true;
+                    }
+                }
+                if (!staged) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        uint4 u;
+                        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) h2[j] = __floats2bfloat162_rn(f[q * 8 + 2 * j], f[q * 8 + 2 * j + 1]);
+                        sts128(smem_u32(sbuf) + lane * 128 + ((q ^ (lane & 7)) << 4), u);
+                    }
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
@@ -1051,6 +1118,7 @@ void launch_row_gemm_tc(const RowGemmArgs& a, cudaStream_t st) {
     p.epi = a.epi;
     p.b_mn = a.w_nmajor ? 1 : 0;
     p.colsum = a.epi == EPI_RELU_MASK ? a.colsum : nullptr;
+    p.relu_bits = (a.epi == EPI_RELU_MASK || a.epi == EPI_BIAS_RELU) ? a.relu_bits : nullptr;
     p.c_peer = 0;
     if (a.c_peer) {
         if (a.ep > 8) throw Status(8, "row gemm: peer stores support at most 8 ranks");

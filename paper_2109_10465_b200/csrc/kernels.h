@@ -152,6 +152,10 @@ struct RowGemmArgs {
     // SMs left free for a co-running kernel (the jitter prefetch); the
     // persistent grid uses the rest
     int sm_reserve = 0;
+    // optional (tensor-core path): the ReLU mask as bits, [rows][N/64] words —
+    // written by EPI_BIAS_RELU (bit j of word (row, c) = stored bf16 H > 0),
+    // read by EPI_RELU_MASK instead of the bf16 H (16x fewer bytes)
+    uint64_t* relu_bits = nullptr;
 };
 template <class T>
 void launch_row_gemm_simt(const RowGemmArgs& a, cudaStream_t st);

@@ -175,6 +175,7 @@ struct moe_handle {
     bool dw_early = true;        // EP: gate dW + its all-reduce before the expert backward (MOE_B200_DW_EARLY=0: after)
     bool gate_dw_tma = false;    // dWg by the TMA-fed MN-major kernel (gate_bwd.cu)
     bool gate_dx_tma = false;    // dx by the persistent TMA-fed kernel (gate_bwd.cu)
+    bool relu_bits_on = true;    // dgrad2 reads the ReLU mask as bits (MOE_B200_RELU_BITS=0: reads H)
     DevMem wsplit;               // [2][E][d] tf32 hi / lo halves of Wg^T
     size_t ws_bytes = 0;         // device bytes allocated by this handle  // forward under EP: the balance loss runs next to the dispatch exchange
     ~moe_handle() {
@@ -194,6 +195,7 @@ struct moe_handle {
     DevMem hist, base, gkept;
     DevMem Xloc, Xr, H, Or, Oloc, dOloc, dOr, dH, dXr, dXloc;
     DevMem dL, dLr, dxg, dwg_part, wgt;
+    DevMem hbits;                // ReLU mask of H as bits [R][f/64] (fwd1 epilogue -> dgrad2 epilogue)
     DevMem bal_term, bal_done;  // balance_finalize per-expert terms + CTA counter
     // jitter stream double buffer: `noise` is the current forward's stream;
     // `noise_pf` receives a stream generated ahead of use (moe_prefetch_jitter)
@@ -438,7 +440,7 @@ template <class TIO>
 bool row_gemm(moe_handle* h, const TIO* A, const TIO* W, TIO* C, const float* bias,
               const TIO* mask, const int32_t* counts, int64_t N, int64_t K, bool w_nmajor,
               int epi, int nseg_ep, float* colsum = nullptr, void* const* c_peer = nullptr,
-              bool* peered = nullptr) {
+              bool* peered = nullptr, uint64_t* relu_bits = nullptr) {
     RowGemmArgs a;
     a.A = A;
     a.W = W;
@@ -455,6 +457,7 @@ bool row_gemm(moe_handle* h, const TIO* A, const TIO* W, TIO* C, const float* bi
     a.epi = epi;
     a.colsum = colsum;
     a.sm_reserve = h->pf_reserve;
+    a.relu_bits = relu_bits;
     if constexpr (std::is_same<TIO, __nv_bfloat16>::value) {
         if (tc_row_gemm_supported(a)) {
             a.c_peer = c_peer;
@@ -720,8 +723,9 @@ void forward_impl(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, c
         h->mark("a2a_dispatch");
     }
     // expert FFN on occupied rows only (routing.cpp:399-405)
+    // (the ReLU mask also goes out as bits, which dgrad2 reads instead of H)
     row_gemm<TIO>(h, h->Xr.as<TIO>(), w1, h->H.as<TIO>(), b1, nullptr, counts, h->f, h->d, true,
-                  EPI_BIAS_RELU, ep);
+                  EPI_BIAS_RELU, ep, nullptr, nullptr, nullptr, h->relu_bits_on ? h->hbits.as<uint64_t>() : nullptr);
     h->mark("ffn1_fwd");
     // under EP with NVLink-mapped buffers the fwd2 epilogue stores each origin
     // rank's rows straight into that rank's O receive buffer (no copy pass)
@@ -881,7 +885,8 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
     // db1 = colsum(dH) comes out of the dgrad2 epilogue on the tensor-core path
     const bool db1_fused = row_gemm<TIO>(h, h->dOr.as<TIO>(), w2, h->dH.as<TIO>(), nullptr,
                                          h->H.as<TIO>(), counts, f, d, false, EPI_RELU_MASK, ep,
-                                         h->db1_part.as<float>());
+                                         h->db1_part.as<float>(), nullptr, nullptr,
+                                         h->relu_bits_on ? h->hbits.as<uint64_t>() : nullptr);
     h->mark("ffn2_dgrad");
     if (db1_fused) launch_colsum_parts(h->db1_part.as<float>(), f, ep, El, h->cap_pad, counts, db1, st);
     // under EP with NVLink-mapped buffers the dgrad1 epilogue returns dX rows
@@ -1126,6 +1131,7 @@ void alloc_workspace(moe_handle* h) {
     h->as.max_groups = G;
     h->Xr.alloc(es * R * d);
     h->H.alloc(es * R * f);
+    h->hbits.alloc(static_cast<size_t>(R) * (f / 64 + 1) * 8);
     h->Or.alloc(es * R * d);
     h->dOr.alloc(es * R * d);
     h->dH.alloc(es * R * f);
@@ -1170,6 +1176,8 @@ void alloc_workspace(moe_handle* h) {
         h->dw_early = !(de && de[0] == '0');
         const char* gd = std::getenv("MOE_B200_GATE_DW_TMA");
         h->gate_dw_tma = gate_dw_tma_ok(static_cast<int>(d), E) && !(gd && gd[0] == '0');
+        const char* rb = std::getenv("MOE_B200_RELU_BITS");
+        h->relu_bits_on = !(rb && rb[0] == '0');
         const char* gx = std::getenv("MOE_B200_GATE_DX_TMA");
         h->gate_dx_tma = gate_dx_tma_ok(static_cast<int>(d), E, K) && !(gx && gx[0] == '0');
     }
