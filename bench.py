@@ -495,7 +495,7 @@ def run_ours(args):
     n_kept = int(kept.sum().item()) if N == 1 else T
     n_drop = T - n_kept
     gate_parts = [k for k in ("gate_fused", "gate_logits", "softmax_topk", "balance_loss") if k in per_stage]
-    groups = {"gate": ["jitter_noise"] + gate_parts, "gate_excl_jitter": gate_parts}
+    groups = {"gate": [k for k in ["jitter_noise"] if k in per_stage] + gate_parts, "gate_excl_jitter": gate_parts}
     stage_roof = {}
     for name in ["gate", "gate_excl_jitter", "assign", "dispatch", "combine", "combine_bwd", "combine_router_bwd", "gate_dx"]:
         parts = groups.get(name, [name])
@@ -671,9 +671,10 @@ def run_extra(args):
         cap, drops, kept = layers[0].handle.stats()
         n_kept = int(kept.sum().item())
         roof = {}
-        for name, parts in (("gate", ["gate_logits", "softmax_topk", "balance_loss"]), ("assign", ["assign"]),
+        gate_parts = [k for k in ("gate_fused", "gate_logits", "softmax_topk", "balance_loss") if k in per]
+        for name, parts in (("gate", gate_parts), ("assign", ["assign"]),
                             ("dispatch", ["dispatch"]), ("combine", ["combine"])):
-            if all(p_ in per for p_ in parts):
+            if parts and all(p_ in per for p_ in parts):
                 st_ms = sum(per[p_] for p_ in parts)
                 b = stage_bytes(name, T, d, E, w["k"], n_kept, T - n_kept)
                 roof[name] = {"ms": st_ms, "GB/s": b / (st_ms / 1e3) / 1e9, "frac": b / (st_ms / 1e3) / 1e9 / hbm}

@@ -40,7 +40,9 @@ namespace gf {
 
 using namespace tc;
 
-constexpr int E = 64;              // experts (TMEM columns per accumulator)
+// Experts: the kernel is instantiated for EP = 16, 32, 64 TMEM columns per
+// accumulator (the MMA's N); E = 8 runs on the EP = 16 instance with the B
+// operand's rows 8..15 zero and those columns masked out of the routing.
 constexpr int BM = 128;            // tokens per cluster
 constexpr int BK = 32;             // fp32 K elements per MMA step (one 128 B swizzle row)
 constexpr int BKR = 64;            // K elements per raw stage (x rows of 128 B: full DRAM bursts)
@@ -52,12 +54,14 @@ constexpr int kTw = 8;             // transform warps (two per SM sub-partition)
 constexpr int kThreads = 32 * (2 + kTw);
 constexpr uint32_t kRawX = BM * BKR * 2;       // 16 KB bf16 x   [128 rows x 128 B], 128B swizzle
 constexpr uint32_t kRawN = BM * BKR * 4;       // 32 KB fp32 noise: two [128 x 128 B] halves, swizzled
-constexpr uint32_t kRawB = E * 128;            //  8 KB per hi / lo
 constexpr uint32_t kRawStage = kRawX + kRawN;                // 48 KB
-constexpr uint32_t kBStage = 2 * kRawB;                      // 16 KB
 constexpr uint32_t kOpStage = 2 * BM * 128;                  // 32 KB (A hi, A lo)
-constexpr uint32_t kRecv = 64 * E * 4;                       // 16 KB: peer's partials for my rows
-constexpr uint32_t kSmem = 1024 + kRaw * kRawStage + kB * kBStage + kOp * kOpStage + kRecv + 512;
+template <int EP> struct GCfg {
+    static constexpr uint32_t kRawB = EP * 128;              // per hi / lo: 8 KB at EP = 64
+    static constexpr uint32_t kBStage = 2 * kRawB;
+    static constexpr uint32_t kRecv = 64 * EP * 4;           // peer's partials for my rows
+    static constexpr uint32_t kSmem = 1024 + kRaw * kRawStage + kB * kBStage + kOp * kOpStage + kRecv + 512;
+};
 
 struct __align__(64) Params {
     CUtensorMap tmX, tmN, tmBh, tmBl;
@@ -69,6 +73,7 @@ struct __align__(64) Params {
     uint32_t* flags;
     int64_t T;
     int d, K, nparts, has_noise;
+    int ne;     // experts (<= the instance's EP; probs / partials rows are ne wide)
     int probe;  // timing probes (MOE_B200_GATE_PROBE): 1 no split math, 2 no MMA, 8 phase timestamps
     unsigned long long* stamps;  // probe 8: [CTA][8] %globaltimer at phase boundaries
 };
@@ -104,7 +109,22 @@ __device__ __forceinline__ void stamp(const Params& p, int i) {
     p.stamps[blockIdx.x * 8 + i] = t;
 }
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <int E>
 __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant__ Params p) {
+    constexpr uint32_t kRawB = GCfg<E>::kRawB;
+    constexpr uint32_t kBStage = GCfg<E>::kBStage;
+    constexpr uint32_t kRecv = GCfg<E>::kRecv;
+    const int ne = p.ne;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* raw = sm;
@@ -281,13 +301,20 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
         if (warp == 2 && lane == 0) stamp(p, 2);
 #pragma unroll
         for (int a = 0; a < kNAcc; ++a) {
+            if constexpr (E == 16) {
+                uint32_t v[16];
+                tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + a * E, v);
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                uint32_t v[32];
-                tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + a * E + h * 32, v);
+                for (int j = 0; j < 16; ++j) L[j] = a ? L[j] + __uint_as_float(v[j]) : __uint_as_float(v[j]);
+            } else {
 #pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    L[h * 32 + j] = a ? L[h * 32 + j] + __uint_as_float(v[j]) : __uint_as_float(v[j]);
+                for (int h = 0; h < E / 32; ++h) {
+                    uint32_t v[32];
+                    tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + a * E + h * 32, v);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        L[h * 32 + j] = a ? L[h * 32 + j] + __uint_as_float(v[j]) : __uint_as_float(v[j]);
+                }
             }
         }
         if (!mine) {  // the peer CTA owns this row: ship my half-d partial logits there
@@ -311,6 +338,9 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
         for (int j = 0; j < E; ++j) L[j] += pr[j];
         const int lr = row & 63;
         if (t < p.T) {
+#pragma unroll
+            for (int j = 0; j < E; ++j)
+                if (j >= ne) L[j] = -INFINITY;  // padded experts (E = 8 on the 16-column instance)
             float mx = L[0];
 #pragma unroll
             for (int j = 1; j < E; ++j) mx = fmaxf(mx, L[j]);
@@ -336,9 +366,10 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
                 }
             }
             if (fabsf(psum - 1.0f) > kProbRowTol) flag |= MOE_FLAG_PROB_ROWS_DEV;
-            float4* po = reinterpret_cast<float4*>(p.probs + t * E);
+            float4* po = reinterpret_cast<float4*>(p.probs + t * ne);
 #pragma unroll
-            for (int j = 0; j < E; j += 4) po[j / 4] = make_float4(L[j], L[j + 1], L[j + 2], L[j + 3]);
+            for (int j = 0; j < E; j += 4)
+                if (j < ne) po[j / 4] = make_float4(L[j], L[j + 1], L[j + 2], L[j + 3]);
             p.choice[t * p.K] = c0;
             p.gate_prob[t * p.K] = b0;
             if (p.K == 2) {  // second choice: initial candidate c0 == 0 ? 1 : 0 (routing.cpp:84-91)
@@ -369,16 +400,18 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
         const int j = row & 63;  // expert
         float cs4[4] = {0.f, 0.f, 0.f, 0.f};  // four interleaved partial sums, fixed order
         int cnt = 0;
+        if (j < ne) {
 #pragma unroll 4
-        for (int r = 0; r < 64; ++r) {
-            cs4[r & 3] += sP[r * (E + 1) + j];
-            cnt += sC[r] == j;
+            for (int r = 0; r < 64; ++r) {
+                cs4[r & 3] += sP[r * (E + 1) + j];
+                cnt += sC[r] == j;
+            }
         }
         const float cs = (cs4[0] + cs4[1]) + (cs4[2] + cs4[3]);
         const int part = static_cast<int>((t0 >> 6) + rank);
-        if (part < p.nparts) {
-            p.colsum_part[static_cast<int64_t>(part) * E + j] = cs;
-            p.count_part[static_cast<int64_t>(part) * E + j] = cnt;
+        if (part < p.nparts && j < ne) {
+            p.colsum_part[static_cast<int64_t>(part) * ne + j] = cs;
+            p.count_part[static_cast<int64_t>(part) * ne + j] = cnt;
         }
         flag = __reduce_or_sync(0xffffffffu, flag);
         if (lane == 0 && flag) atomicOr(p.flags, flag);
@@ -392,47 +425,60 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
     }
 }
 
-// Wg [d][E] -> Wg^T split into tf32 hi / lo halves [E][d] (the B operand)
-__global__ void split_kernel(const float* __restrict__ wg, float* __restrict__ hi, float* __restrict__ lo, int d) {
+// Wg [d][ne] -> Wg^T split into tf32 hi / lo halves [EP][d] (the B operand),
+// rows ne..EP-1 zero
+__global__ void split_kernel(const float* __restrict__ wg, float* __restrict__ hi, float* __restrict__ lo, int d,
+                             int ne, int EP) {
     pdl_wait();
     pdl_trigger();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= d * E) return;
-    const int j = i / E, e = i % E;
-    const float v = wg[i];
+    if (i >= d * EP) return;
+    const int j = i / EP, e = i % EP;
+    const float v = e < ne ? wg[static_cast<int64_t>(j) * ne + e] : 0.f;
     const float h = tf32_rna(v);
     hi[static_cast<int64_t>(e) * d + j] = h;
     lo[static_cast<int64_t>(e) * d + j] = tf32_rna(v - h);
 }
 
+// the kernel instance (TMEM columns per accumulator) for ne experts
+inline int padded_experts(int ne) { return ne <= 16 ? 16 : ne; }
+
 }  // namespace gf
 
-bool gate_fused_ok(int d, int E) { return E == gf::E && d % (2 * gf::BKR) == 0 && d >= 2 * gf::BKR; }
+bool gate_fused_ok(int d, int E) {
+    return (E == 8 || E == 16 || E == 32 || E == 64) && d % (2 * gf::BKR) == 0 && d >= 2 * gf::BKR;
+}
 
-void launch_gate_split(const float* wg, float* wsplit, int d, cudaStream_t st) {
-    launch_pdl(gf::split_kernel, dim3(static_cast<unsigned>(ceil_div(static_cast<int64_t>(d) * gf::E, 256))),
-               dim3(256), 0, st, wg, wsplit, wsplit + static_cast<int64_t>(d) * gf::E, d);
+size_t gate_split_floats(int d, int E) { return 2 * static_cast<size_t>(d) * gf::padded_experts(E); }
+
+void launch_gate_split(const float* wg, float* wsplit, int d, int E, cudaStream_t st) {
+    const int EP = gf::padded_experts(E);
+    launch_pdl(gf::split_kernel, dim3(static_cast<unsigned>(ceil_div(static_cast<int64_t>(d) * EP, 256))), dim3(256),
+               0, st, wg, wsplit, wsplit + static_cast<int64_t>(d) * EP, d, E, EP);
 }
 
 int gate_fused_parts(int64_t T) { return static_cast<int>(ceil_div(T, static_cast<int64_t>(64))); }
 
-void launch_gate_fused(const __nv_bfloat16* x, const float* noise, const float* wsplit, int64_t T, int d, int K,
-                       float* probs, int32_t* choice, float* gate_prob, float* colsum_part, int32_t* count_part,
-                       uint32_t* flags, cudaStream_t st) {
+namespace {
+template <int EP>
+void launch_gate_fused_ep(const __nv_bfloat16* x, const float* noise, const float* wsplit, int64_t T, int d, int K,
+                          int E, float* probs, int32_t* choice, float* gate_prob, float* colsum_part,
+                          int32_t* count_part, uint32_t* flags, cudaStream_t st) {
     using namespace gf;
+    constexpr uint32_t kSmem = GCfg<EP>::kSmem;
     static bool attr = false;
     if (!attr) {
-        MOE_CUDA_CHECK(cudaFuncSetAttribute(gate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        MOE_CUDA_CHECK(cudaFuncSetAttribute(gate_kernel<EP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             static_cast<int>(kSmem)));
         attr = true;
     }
     Params p{};
     p.tmX = tc::make_map_2d(x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, T, d, BKR, BM, true);
-    p.tmN = tc::make_map_2d(noise ? noise : wsplit, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, noise ? T : E, d, BK,
-                            noise ? BM : E, true);
-    p.tmBh = tc::make_map_2d(wsplit, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, E, d, BK, E, true);
-    p.tmBl = tc::make_map_2d(wsplit + static_cast<int64_t>(d) * E, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, E, d, BK, E,
-                             true);
+    p.tmN = tc::make_map_2d(noise ? noise : wsplit, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, noise ? T : EP, d, BK,
+                            noise ? BM : EP, true);
+    p.tmBh = tc::make_map_2d(wsplit, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, EP, d, BK, EP, true);
+    p.tmBl = tc::make_map_2d(wsplit + static_cast<int64_t>(d) * EP, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, EP, d, BK,
+                             EP, true);
     p.probs = probs;
     p.choice = choice;
     p.gate_prob = gate_prob;
@@ -442,6 +488,7 @@ void launch_gate_fused(const __nv_bfloat16* x, const float* noise, const float* 
     p.T = T;
     p.d = d;
     p.K = K;
+    p.ne = E;
     p.nparts = gate_fused_parts(T);
     p.has_noise = noise != nullptr;
     static const int probe = [] {
@@ -468,8 +515,23 @@ void launch_gate_fused(const __nv_bfloat16* x, const float* noise, const float* 
     cfg.stream = st;
     cfg.attrs = attrs;
     cfg.numAttrs = 2;
-    MOE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gate_kernel, p));
+    MOE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gate_kernel<EP>, p));
     count_launch();
+}
+}  // namespace
+
+void launch_gate_fused(const __nv_bfloat16* x, const float* noise, const float* wsplit, int64_t T, int d, int K,
+                       int E, float* probs, int32_t* choice, float* gate_prob, float* colsum_part,
+                       int32_t* count_part, uint32_t* flags, cudaStream_t st) {
+    switch (gf::padded_experts(E)) {
+        case 16: launch_gate_fused_ep<16>(x, noise, wsplit, T, d, K, E, probs, choice, gate_prob, colsum_part,
+                                          count_part, flags, st); break;
+        case 32: launch_gate_fused_ep<32>(x, noise, wsplit, T, d, K, E, probs, choice, gate_prob, colsum_part,
+                                          count_part, flags, st); break;
+        case 64: launch_gate_fused_ep<64>(x, noise, wsplit, T, d, K, E, probs, choice, gate_prob, colsum_part,
+                                          count_part, flags, st); break;
+        default: throw Status(6, "gate_fused: experts must be 8, 16, 32 or 64");
+    }
 }
 
 // debug: copy the probe-8 phase timestamps of the last launch (ncta x 8 u64)

@@ -313,17 +313,18 @@ void launch_f64_acc_copy(const double* src, double* dst, int64_t n, bool accumul
 
 namespace moe {
 // gate_fused.cu: logits + softmax + top-k + balance partials + balance finalize
-// in one cluster kernel (bf16 path, E == 64)
+// in one cluster kernel (bf16 path, E in {8, 16, 32, 64})
 bool gate_fused_ok(int d, int E);
 int gate_fused_parts(int64_t T);
-// wsplit [2][E][d]: tf32 hi / lo halves of Wg^T
-void launch_gate_split(const float* wg, float* wsplit, int d, cudaStream_t st);
+// wsplit [2][EP][d]: tf32 hi / lo halves of Wg^T, EP = max(E, 16) rows (zero-padded)
+size_t gate_split_floats(int d, int E);
+void launch_gate_split(const float* wg, float* wsplit, int d, int E, cudaStream_t st);
 int gate_fused_stamps(unsigned long long* host, int ncta);  // debug (MOE_B200_GATE_PROBE=8)
 // writes P, the decision and per-64-token balance partials [gate_fused_parts][E]
 // (finalize with launch_balance_finalize)
 void launch_gate_fused(const __nv_bfloat16* x, const float* noise, const float* wsplit, int64_t T, int d, int K,
-                       float* probs, int32_t* choice, float* gate_prob, float* colsum_part, int32_t* count_part,
-                       uint32_t* flags, cudaStream_t st);
+                       int E, float* probs, int32_t* choice, float* gate_prob, float* colsum_part,
+                       int32_t* count_part, uint32_t* flags, cudaStream_t st);
 }  // namespace moe
 
 namespace moe {

@@ -514,12 +514,12 @@ void route(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, int phas
     const bool gtc = use_gate_tc<TIO>(h);
     // fused gate (gate_fused.cu): one cluster kernel for logits, softmax,
     // top-k and the balance loss; MOE_B200_GATE_FUSED=0 keeps the split kernels
-    const bool fused = gtc && h->gate_fused;
+    const bool fused = std::is_same<TIO, __nv_bfloat16>::value && h->gate_fused;
     if (fused) {
         // tf32 hi / lo halves of Wg^T for the fused gate's B operand: a 4 us kernel
         // on the main stream (PDL hands over to the gate; a side-stream launch
         // cost more in cross-stream wait than it overlapped)
-        launch_gate_split(gate_w, h->wsplit.as<float>(), static_cast<int>(h->d), st);
+        launch_gate_split(gate_w, h->wsplit.as<float>(), static_cast<int>(h->d), E, st);
     } else if (gtc) {  // Wg^T for the logits' B operand, on the side stream next to the jitter generator
         MOE_CUDA_CHECK(cudaEventRecord(h->ev_a, st));
         MOE_CUDA_CHECK(cudaStreamWaitEvent(h->side, h->ev_a, 0));
@@ -543,7 +543,7 @@ void route(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, int phas
     if (fused) {
         if constexpr (std::is_same<TIO, __nv_bfloat16>::value) {
             launch_gate_fused(x, jitter ? h->noise.as<float>() : nullptr, h->wsplit.as<float>(), T,
-                              static_cast<int>(h->d), K, h->probs.as<float>(), h->choice.as<int32_t>(),
+                              static_cast<int>(h->d), K, E, h->probs.as<float>(), h->choice.as<int32_t>(),
                               h->gate_prob.as<float>(), h->colsum_part.as<float>(), h->count_part.as<int32_t>(),
                               h->flags.as<uint32_t>(), st);
         }
@@ -1164,7 +1164,7 @@ void alloc_workspace(moe_handle* h) {
     h->dxg.alloc(4 * T * d);
     h->dwg_part.alloc(4 * 16 * d * E);
     h->wgt.alloc(4 * d * E);
-    h->wsplit.alloc(8 * d * E);
+    h->wsplit.alloc(4 * (gate_fused_ok(static_cast<int>(d), E) ? gate_split_floats(static_cast<int>(d), E) : 2 * d * E));
     {
         const char* g = std::getenv("MOE_B200_GATE_FUSED");
         h->gate_fused = es == 2 && gate_fused_ok(static_cast<int>(d), E) && !(g && g[0] == '0');

@@ -213,17 +213,19 @@ def test_bf16_gemm_variants_subprocess(pair):
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("top_k,T", [(1, 8192), (2, 1000), (1, 300)])
-def test_fused_gate_matches_split_kernels(top_k, T):
+@pytest.mark.parametrize("top_k,T,E", [(1, 8192, 64), (2, 1000, 64), (1, 300, 64), (1, 4096, 8),
+                                       (2, 1000, 16), (1, 2048, 32), (2, 300, 32)])
+def test_fused_gate_matches_split_kernels(top_k, T, E):
     """The fused gate (gate_fused.cu: logits + softmax + top-k + balance loss in
     one cluster kernel) against the split kernels (MOE_B200_GATE_FUSED=0:
     split-K logits, softmax_topk, balance_finalize) on the same inputs:
     identical decisions, probabilities / gate_prob / aux within fp32 rounding,
-    including a ragged last tile (T % 128 != 0)."""
+    including a ragged last tile (T % 128 != 0), for every expert count the
+    fused kernel takes (E = 8 runs on the 16-column instance with padding)."""
     import os
 
     import paper_2109_10465_b200 as M
-    d, f, E, seed = 2048, 256, 64, 5
+    d, f, seed = 2048, 256, 5
     x0, gw, *_ = O.layer_inputs(T, d, 8, E, seed=seed)
     ocfg = O.make_cfg(num_experts=E, top_k=top_k)
     x = margin_guard(bf16_round(x0), gw, ocfg, O.TRAIN, seed, round_fn=bf16_round)
