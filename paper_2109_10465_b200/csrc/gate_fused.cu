@@ -74,6 +74,7 @@ struct __align__(64) Params {
     int64_t T;
     int d, K, nparts, has_noise;
     int ne;     // experts (<= the instance's EP; probs / partials rows are ne wide)
+    int csize;  // CTAs per 128-token tile: 2 (a cluster, each CTA half of d) or 1 (one CTA, all of d)
     int probe;  // timing probes (MOE_B200_GATE_PROBE): 1 no split math, 2 no MMA, 8 phase timestamps
     unsigned long long* stamps;  // probe 8: [CTA][8] %globaltimer at phase boundaries
 };
@@ -143,14 +144,15 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
-    const int64_t t0 = static_cast<int64_t>(blockIdx.x >> 1) * BM;
-    const int kspan = p.d / 2;
+    const int cs = p.csize;
+    const int64_t t0 = static_cast<int64_t>(blockIdx.x / cs) * BM;
+    const int kspan = p.d / cs;
     const int kbase = static_cast<int>(rank) * kspan;
     const int nsteps = kspan / BK;   // MMA steps
     const int nraw = kspan / BKR;    // raw stages (two MMA steps each)
     // every cluster walks its K range from a different starting stage, so the
     // 128 CTAs do not all read the same Wg^T tile from L2 at the same time
-    const int kskew = static_cast<int>((blockIdx.x >> 1) % nraw);
+    const int kskew = static_cast<int>((blockIdx.x / cs) % nraw);
 
     if (threadIdx.x == 0) stamp(p, 0);
     if (threadIdx.x == 0) {
@@ -294,7 +296,7 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
     const bool epi = warp >= 2 && warp < 6;  // one epilogue warp per TMEM lane quarter
     const int q = warp & 3;                 // TMEM lane quarter of this warp
     const int row = q * 32 + lane;          // token row inside the cluster tile
-    const bool mine = (row >> 6) == static_cast<int>(rank);
+    const bool mine = cs == 1 || (row >> 6) == static_cast<int>(rank);
     if (epi) {
         mbar_wait(acc_full, 0);
         tc_fence_after();
@@ -328,15 +330,17 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
     cluster_sync();  // every partial has landed; both CTAs stay resident until here
     if (warp == 2 && lane == 0) stamp(p, 4);
     // owner warps: logits = own half + peer half, then the row's routing
-    float* sP = reinterpret_cast<float*>(op);                // [64][E + 1] after the loop
-    int32_t* sC = reinterpret_cast<int32_t*>(sP + 64 * (E + 1));
+    float* sP = reinterpret_cast<float*>(op);                // [64 or 128][E + 1] after the loop
+    int32_t* sC = reinterpret_cast<int32_t*>(sP + 128 * (E + 1));
     const int64_t t = t0 + row;
     uint32_t flag = 0;
     if (epi && mine) {
-        const float* pr = recv + (row & 63) * E;
+        if (cs == 2) {
+            const float* pr = recv + (row & 63) * E;
 #pragma unroll
-        for (int j = 0; j < E; ++j) L[j] += pr[j];
-        const int lr = row & 63;
+            for (int j = 0; j < E; ++j) L[j] += pr[j];
+        }
+        const int lr = cs == 1 ? row : (row & 63);
         if (t < p.T) {
 #pragma unroll
             for (int j = 0; j < E; ++j)
@@ -394,23 +398,27 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
         }
     }
     // the two owner warps of this CTA: column sums / first-choice counts of their 64 rows
-    const bool owner_warp = epi && ((q >> 1) == static_cast<int>(rank));
+    // (one CTA per tile: both pairs of epilogue warps, each over its 64 rows)
+    const bool owner_warp = epi && (cs == 1 || (q >> 1) == static_cast<int>(rank));
     if (owner_warp) {
-        asm volatile("bar.sync 1, 64;" ::: "memory");
+        const int half = cs == 1 ? (q >> 1) : 0;
+        if (half == 0) asm volatile("bar.sync 1, 64;" ::: "memory");
+        else asm volatile("bar.sync 2, 64;" ::: "memory");
         const int j = row & 63;  // expert
+        const int rb = 64 * half;
         float cs4[4] = {0.f, 0.f, 0.f, 0.f};  // four interleaved partial sums, fixed order
         int cnt = 0;
         if (j < ne) {
 #pragma unroll 4
             for (int r = 0; r < 64; ++r) {
-                cs4[r & 3] += sP[r * (E + 1) + j];
-                cnt += sC[r] == j;
+                cs4[r & 3] += sP[(rb + r) * (E + 1) + j];
+                cnt += sC[rb + r] == j;
             }
         }
-        const float cs = (cs4[0] + cs4[1]) + (cs4[2] + cs4[3]);
-        const int part = static_cast<int>((t0 >> 6) + rank);
+        const float csum = (cs4[0] + cs4[1]) + (cs4[2] + cs4[3]);
+        const int part = static_cast<int>((t0 >> 6) + (cs == 1 ? half : static_cast<int>(rank)));
         if (part < p.nparts && j < ne) {
-            p.colsum_part[static_cast<int64_t>(part) * ne + j] = cs;
+            p.colsum_part[static_cast<int64_t>(part) * ne + j] = csum;
             p.count_part[static_cast<int64_t>(part) * ne + j] = cnt;
         }
         flag = __reduce_or_sync(0xffffffffu, flag);
@@ -489,6 +497,10 @@ void launch_gate_fused_ep(const __nv_bfloat16* x, const float* noise, const floa
     p.d = d;
     p.K = K;
     p.ne = E;
+    const unsigned tiles = static_cast<unsigned>(ceil_div(T, static_cast<int64_t>(BM)));
+    // more tiles than one wave of CTA pairs: one CTA per tile takes all of d,
+    // halving the per-CTA setup / pipeline fill / epilogue per byte
+    p.csize = tiles > static_cast<unsigned>(kNumSMs / 2) && d % BKR == 0 ? 1 : 2;
     p.nparts = gate_fused_parts(T);
     p.has_noise = noise != nullptr;
     static const int probe = [] {
@@ -500,16 +512,15 @@ void launch_gate_fused_ep(const __nv_bfloat16* x, const float* noise, const floa
     if ((probe & 8) && !stamps) MOE_CUDA_CHECK(cudaMalloc(&stamps, 8 * 8 * 4096));
     p.stamps = stamps;
     if (probe & 8) g_gate_stamps = stamps;
-    const unsigned tiles = static_cast<unsigned>(ceil_div(T, static_cast<int64_t>(BM)));
     cudaLaunchAttribute attrs[2];
     attrs[0].id = cudaLaunchAttributeClusterDimension;
-    attrs[0].val.clusterDim.x = 2;
+    attrs[0].val.clusterDim.x = static_cast<unsigned>(p.csize);
     attrs[0].val.clusterDim.y = 1;
     attrs[0].val.clusterDim.z = 1;
     attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attrs[1].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(2 * tiles);
+    cfg.gridDim = dim3(static_cast<unsigned>(p.csize) * tiles);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = kSmem;
     cfg.stream = st;

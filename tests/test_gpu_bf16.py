@@ -214,7 +214,8 @@ def test_bf16_gemm_variants_subprocess(pair):
 
 
 @pytest.mark.parametrize("top_k,T,E", [(1, 8192, 64), (2, 1000, 64), (1, 300, 64), (1, 4096, 8),
-                                       (2, 1000, 16), (1, 2048, 32), (2, 300, 32)])
+                                       (2, 1000, 16), (1, 2048, 32), (2, 300, 32),
+                                       (1, 16384, 64), (2, 12000, 16)])
 def test_fused_gate_matches_split_kernels(top_k, T, E):
     """The fused gate (gate_fused.cu: logits + softmax + top-k + balance loss in
     one cluster kernel) against the split kernels (MOE_B200_GATE_FUSED=0:
@@ -242,7 +243,9 @@ def test_fused_gate_matches_split_kernels(top_k, T, E):
         outs.append((dec.expert_id.cpu(), dec.slot.cpu(), dec.gate_prob.cpu(), float(aux[0]), y.float().cpu()))
     (e1, s1, g1, a1, y1), (e0, s0, g0, a0, y0) = outs
     assert torch.equal(e1, e0) and torch.equal(s1, s0)
-    assert float((g1 - g0).abs().max()) <= 2e-6
+    # the two paths sum the d products in different orders (3xTF32 in TMEM vs
+    # split-K FMA partials): a few fp32 ulps of the logits, scaled by p ~ 1/E
+    assert float((g1 - g0).abs().max()) <= (2e-6 if E == 64 else 1e-5)
     assert abs(a1 - a0) <= 1e-6 * max(1.0, abs(a0))
     assert float((y1 - y0).abs().max()) <= 2e-2 * max(1.0, float(y0.abs().max()))
 
