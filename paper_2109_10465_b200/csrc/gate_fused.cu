@@ -79,10 +79,20 @@ struct __align__(64) Params {
     unsigned long long* stamps;  // probe 8: [CTA][8] %globaltimer at phase boundaries
 };
 
+// Round to tf32, nearest with ties away from zero, on the integer pipes:
+// adding half an ulp of bit 13 to the sign-magnitude bits and clearing the 13
+// low bits is exactly cvt.rna.tf32.f32 (carries into the exponent round up to
+// the next binade or to infinity; infinities and NaNs keep their class), but
+// two ALU operations instead of a conversion on the XU pipe, which the
+// transform's two roundings per element otherwise saturate.
 __device__ __forceinline__ float tf32_rna(float v) {
+#ifdef MOE_GATE_CVT_RNA
     uint32_t r;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
     return __uint_as_float(r);
+#else
+    return __uint_as_float((__float_as_uint(v) + 0x1000u) & 0xFFFFE000u);
+#endif
 }
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
