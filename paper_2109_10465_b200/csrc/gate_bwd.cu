@@ -73,8 +73,16 @@ __device__ __forceinline__ float4 lds128f(uint32_t a) {
 __device__ __forceinline__ uint32_t swz(int r, int c) { return r * 128 + ((c ^ (r & 7)) << 4); }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+#ifdef MOE_GBW_INT_PACK
+    // round-to-nearest-even on the integer pipes (finite values and infinities)
+    uint32_t ua = __float_as_uint(a), ub = __float_as_uint(b);
+    ua += 0x7FFFu + ((ua >> 16) & 1u);
+    ub += 0x7FFFu + ((ub >> 16) & 1u);
+    return __byte_perm(ua, ub, 0x7632);
+#else
     const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<const uint32_t*>(&h);
+#endif
 }
 // hi / lo bf16 split of 8 fp32 values: hi = bf16(v), lo = bf16(v - hi)
 __device__ __forceinline__ void split8(const float (&v)[8], uint4& hi, uint4& lo) {
