@@ -172,7 +172,12 @@ struct moe_handle {
     bool gate_fused = false;     // bf16 gate in one cluster kernel (gate_fused.cu)
     bool rcb_fused = true;       // single rank: combine backward folded into router_bwd
     bool rcb_ep = true;          // ... also under EP (MOE_B200_RCB_EP=0: two kernels, dO exchange next to router_bwd)
-    bool dw_early = true;        // EP: gate dW + its all-reduce before the expert backward (MOE_B200_DW_EARLY=0: after)
+    // EP: gate dW + its all-reduce before the expert backward (MOE_B200_DW_EARLY=1).
+    // Off by default: the all-reduce's barrier after the weight gradients is
+    // the exchange point that orders this step's last read of Xr (dW1) before
+    // the peers' dispatch stores of the next step; with it moved, the next
+    // dispatch exchange first runs an extra barrier.
+    bool dw_early = false;
     bool gate_dw_tma = false;    // dWg by the TMA-fed MN-major kernel (gate_bwd.cu)
     bool gate_dx_tma = false;    // dx by the persistent TMA-fed kernel (gate_bwd.cu)
     bool relu_bits_on = true;    // dgrad2 reads the ReLU mask as bits (MOE_B200_RELU_BITS=0: reads H)
@@ -708,6 +713,9 @@ void forward_impl(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, c
         // the exchange also checks that every rank passed the same T (else
         // MOE_FLAG_UNIFORM_SHAPE and zero received counts)
         const ShapeCheck sc{static_cast<long long>(T), h->flags.as<uint32_t>(), h->counts_r.as<int32_t>(), E};
+        // (dW1 of the previous step reads Xr after the last barrier when the
+        // gate's all-reduce ran early: order it before the peers' stores)
+        if (h->dw_early && h->ipc) peer_barrier(h);
         exchange(h, {{h->kept.p, h->counts_r.p, moe_handle::P_CNT, static_cast<size_t>(El), ncclInt32, 4},
                      {Xloc, h->Xr.p, moe_handle::P_X, static_cast<size_t>(El) * h->cap_pad * h->d,
                       nccl_type(h->esz), h->esz}}, false, &sc);
@@ -1173,7 +1181,7 @@ void alloc_workspace(moe_handle* h) {
         const char* re = std::getenv("MOE_B200_RCB_EP");
         h->rcb_ep = !(re && re[0] == '0');
         const char* de = std::getenv("MOE_B200_DW_EARLY");
-        h->dw_early = !(de && de[0] == '0');
+        h->dw_early = de && de[0] == '1';
         const char* gd = std::getenv("MOE_B200_GATE_DW_TMA");
         h->gate_dw_tma = gate_dw_tma_ok(static_cast<int>(d), E) && !(gd && gd[0] == '0');
         const char* rb = std::getenv("MOE_B200_RELU_BITS");
