@@ -48,6 +48,14 @@ void launch_router_bwd(int64_t T, int d, int E, int K, const TIO* dy, const TIO*
                        const float* probs, const float* fcoef, float daux, float* dL,
                        cudaStream_t st, float* dLr = nullptr);
 
+// Row destinations under expert parallelism: p[o] = rank o's receive buffer
+// at this rank's slot (local buffer for o == rank); expert e's rows go to
+// p[e / El] at local expert e % El.  ep <= 1: the local [E][cap_pad] buffer.
+struct RowDst {
+    void* p[8];
+    int El;
+    int ep;
+};
 // router_bwd with the combine backward (dO rows = w dy[t], expert tails
 // zeroed) folded in: one pass over dy for single-rank layers.
 template <class TIO>
@@ -55,7 +63,7 @@ void launch_router_combine_bwd(int64_t T, int d, int E, int K, const TIO* dy, co
                                const int32_t* choice, const int32_t* pos, const float* gate_prob,
                                const float* probs, const float* fcoef, float daux, const float* w,
                                const int32_t* kept, TIO* dO, float* dL, cudaStream_t st,
-                               float* dLr = nullptr);
+                               float* dLr = nullptr, const RowDst* rd = nullptr);
 
 // ---- rng.cu ---------------------------------------------------------------
 // Jitter noise n[i] = lo + (hi-lo) * ((mt() >> 11) * 2^-53) for i in [0, count)
@@ -72,7 +80,7 @@ void launch_jitter_noise(const MtJumpTable* tab, uint64_t seed, int64_t count, d
 template <class TIO>
 void launch_dispatch_gather(const TIO* x, int64_t d, int E, int K, int cap_pad,
                             const int32_t* row_src, const int32_t* kept, TIO* buf,
-                            uint32_t* flags, cudaStream_t st);
+                            uint32_t* flags, cudaStream_t st, const RowDst* rd = nullptr);
 template <class TIO>
 void launch_combine(const TIO* O, int64_t T, int64_t d, int E, int K, int cap_pad,
                     const int32_t* choice, const int32_t* pos, const float* w,

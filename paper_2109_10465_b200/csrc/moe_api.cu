@@ -171,7 +171,8 @@ struct moe_handle {
     bool gemm_tc = false;        // bf16 expert GEMMs on tcgen05 (decided at create)
     bool gate_fused = false;     // bf16 gate in one cluster kernel (gate_fused.cu)
     bool rcb_fused = true;       // single rank: combine backward folded into router_bwd
-    bool rcb_ep = true;          // ... also under EP (MOE_B200_RCB_EP=0: two kernels, dO exchange next to router_bwd)
+    bool rcb_ep = true;
+    bool peer_dispatch = true;   // EP (IPC): the dispatch gather stores rows into the owners' buffers (MOE_B200_PEER_DISPATCH=0: copy pass)          // ... also under EP (MOE_B200_RCB_EP=0: two kernels, dO exchange next to router_bwd)
     // EP: gate dW + its all-reduce before the expert backward (MOE_B200_DW_EARLY=1).
     // Off by default: the all-reduce's barrier after the weight gradients is
     // the exchange point that orders this step's last read of Xr (dW1) before
@@ -699,8 +700,20 @@ void forward_impl(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, c
     if (ep == 1) launch_combine_weights(T, E, K, h->gate_prob.as<float>(), h->wts.as<float>(), st);
     // dispatch (routing.cpp:396): un-jittered x into [E, cap_pad, d]
     TIO* Xloc = static_cast<TIO*>(h->loc(h->Xr, h->Xloc));
+    // under EP with NVLink-mapped buffers the gather stores each row straight
+    // into its expert owner's receive buffer (no local copy, no copy pass)
+    const bool peer_dispatch = ep > 1 && h->ipc && !h->no_peer_epi && h->peer_dispatch && ep <= 8;
+    RowDst rd{};
+    if (peer_dispatch) {
+        rd.El = El;
+        rd.ep = ep;
+        const size_t slot = static_cast<size_t>(h->rank) * El * h->cap_pad * h->d * h->esz;
+        for (int r = 0; r < ep; ++r)
+            rd.p[r] = (r == h->rank ? static_cast<char*>(h->Xr.p) : static_cast<char*>(h->peer[moe_handle::P_X][r])) + slot;
+    }
     launch_dispatch_gather<TIO>(x, h->d, E, K, h->cap_pad, h->row_src.as<int32_t>(),
-                                h->kept.as<int32_t>(), Xloc, h->flags.as<uint32_t>(), st);
+                                h->kept.as<int32_t>(), Xloc, h->flags.as<uint32_t>(), st,
+                                peer_dispatch ? &rd : nullptr);
     h->mark("dispatch");
     const int32_t* counts = h->kept.as<int32_t>();
     if (ep > 1) {
@@ -716,9 +729,13 @@ void forward_impl(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, c
         // (dW1 of the previous step reads Xr after the last barrier when the
         // gate's all-reduce ran early: order it before the peers' stores)
         if (h->dw_early && h->ipc) peer_barrier(h);
-        exchange(h, {{h->kept.p, h->counts_r.p, moe_handle::P_CNT, static_cast<size_t>(El), ncclInt32, 4},
-                     {Xloc, h->Xr.p, moe_handle::P_X, static_cast<size_t>(El) * h->cap_pad * h->d,
-                      nccl_type(h->esz), h->esz}}, false, &sc);
+        if (peer_dispatch)  // rows already stored: counts + the barrier (with the shape check)
+            exchange(h, {{h->kept.p, h->counts_r.p, moe_handle::P_CNT, static_cast<size_t>(El), ncclInt32, 4}},
+                     false, &sc);
+        else
+            exchange(h, {{h->kept.p, h->counts_r.p, moe_handle::P_CNT, static_cast<size_t>(El), ncclInt32, 4},
+                         {Xloc, h->Xr.p, moe_handle::P_X, static_cast<size_t>(El) * h->cap_pad * h->d,
+                          nccl_type(h->esz), h->esz}}, false, &sc);
         h->stream = saved;
         MOE_CUDA_CHECK(cudaEventRecord(h->ev_comm, h->comm_stream));
         if (!h->bal_pending) balance_finalize(h, T, aux);  // (the fused gate's runs on the side stream)
@@ -804,12 +821,24 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
     // the persistent dx kernel reads tf32-rounded dL (written next to dL by the router backward)
     const bool dx_tma = std::is_same<TIO, __nv_bfloat16>::value && use_gate_tc<TIO>(h) && h->gate_dx_tma;
     float* dLr = dx_tma ? h->dLr.as<float>() : nullptr;
+    // under EP with NVLink-mapped buffers the fused kernel stores the dO rows
+    // straight into the expert owners' dO buffers (the exchange is a barrier)
+    const bool peer_do = rcb && ep > 1 && h->ipc && !h->no_peer_epi && h->peer_dispatch && ep <= 8;
+    RowDst rdo{};
+    if (peer_do) {
+        rdo.El = El;
+        rdo.ep = ep;
+        const size_t slot = static_cast<size_t>(h->rank) * El * h->cap_pad * d * h->esz;
+        for (int r = 0; r < ep; ++r)
+            rdo.p[r] = (r == h->rank ? static_cast<char*>(h->dOr.p) : static_cast<char*>(h->peer[moe_handle::P_DO][r])) + slot;
+    }
     if (rcb) {  // one pass over dy: dO rows and the routing / softmax backward -> dL
         launch_router_combine_bwd<TIO>(T, static_cast<int>(d), E, K, dy, Oloc, h->cap_pad,
                                        h->choice.as<int32_t>(), h->pos.as<int32_t>(),
                                        h->gate_prob.as<float>(), h->probs.as<float>(),
                                        h->fcoef.as<float>(), daux, h->wts.as<float>(),
-                                       h->kept.as<int32_t>(), dOloc, h->dL.as<float>(), st, dLr);
+                                       h->kept.as<int32_t>(), dOloc, h->dL.as<float>(), st, dLr,
+                                       peer_do ? &rdo : nullptr);
         h->mark("combine_router_bwd");
     } else {
         launch_combine_bwd_gather<TIO>(dy, d, E, K, h->cap_pad, h->row_src.as<int32_t>(),
@@ -822,8 +851,11 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
         MOE_CUDA_CHECK(cudaStreamWaitEvent(h->comm_stream, h->ev_c, 0));
         cudaStream_t saved = h->stream;
         h->stream = h->comm_stream;
-        exchange(h, {{dOloc, h->dOr.p, moe_handle::P_DO, static_cast<size_t>(El) * h->cap_pad * d,
-                      nccl_type(h->esz), h->esz}});
+        if (peer_do)
+            peer_barrier(h);  // every rank's dO rows have landed
+        else
+            exchange(h, {{dOloc, h->dOr.p, moe_handle::P_DO, static_cast<size_t>(El) * h->cap_pad * d,
+                          nccl_type(h->esz), h->esz}});
         h->stream = saved;
         MOE_CUDA_CHECK(cudaEventRecord(h->ev_comm, h->comm_stream));
         counts = h->counts_r.as<int32_t>();
@@ -1178,6 +1210,8 @@ void alloc_workspace(moe_handle* h) {
         h->gate_fused = es == 2 && gate_fused_ok(static_cast<int>(d), E) && !(g && g[0] == '0');
         const char* r = std::getenv("MOE_B200_RCB_FUSED");
         h->rcb_fused = !(r && r[0] == '0');
+        const char* pdp = std::getenv("MOE_B200_PEER_DISPATCH");
+        h->peer_dispatch = !(pdp && pdp[0] == '0');
         const char* re = std::getenv("MOE_B200_RCB_EP");
         h->rcb_ep = !(re && re[0] == '0');
         const char* de = std::getenv("MOE_B200_DW_EARLY");

@@ -26,7 +26,7 @@ template <class TIO, int V>
 __global__ void __launch_bounds__(kRowWarps * 32)
 dispatch_gather_kernel(const TIO* __restrict__ x, int64_t d, int E, int K, int cap_pad,
                        const int32_t* __restrict__ row_src, const int32_t* __restrict__ kept,
-                       TIO* __restrict__ buf) {
+                       TIO* __restrict__ buf, RowDst rd) {
     pdl_wait();
     pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -35,7 +35,10 @@ dispatch_gather_kernel(const TIO* __restrict__ x, int64_t d, int E, int K, int c
     const int e = (int)(r / cap_pad);
     const int p = (int)(r % cap_pad);
     const int n = kept[e];
-    TIO* dst = buf + r * d;
+    // expert parallelism: the row goes straight to its expert owner's receive
+    // buffer (NVLink store; rd.p[o] already points at this rank's slot there)
+    TIO* dst = rd.ep > 1 ? static_cast<TIO*>(rd.p[e / rd.El]) + ((int64_t)(e % rd.El) * cap_pad + p) * d
+                         : buf + r * d;
     if (p < n) {
         const int64_t t = row_src[r] / K;
         const TIO* src = x + t * d;
@@ -62,16 +65,18 @@ dispatch_gather_kernel(const TIO* __restrict__ x, int64_t d, int E, int K, int c
 template <class TIO>
 void launch_dispatch_gather(const TIO* x, int64_t d, int E, int K, int cap_pad,
                             const int32_t* row_src, const int32_t* kept, TIO* buf,
-                            uint32_t* flags, cudaStream_t st) {
+                            uint32_t* flags, cudaStream_t st, const RowDst* rd) {
     (void)flags;
     const int64_t rows = (int64_t)E * cap_pad;
     const unsigned grid = (unsigned)ceil_div(rows, kRowWarps);
+    RowDst r0{};
+    const RowDst& rdv = rd ? *rd : r0;
     if (vec_width<TIO>(d) > 1)
-        launch_pdl(dispatch_gather_kernel<TIO, 16 / sizeof(TIO)>, dim3(grid), dim3(kRowWarps * 32), 0, st, 
-            x, d, E, K, cap_pad, row_src, kept, buf);
+        launch_pdl(dispatch_gather_kernel<TIO, 16 / sizeof(TIO)>, dim3(grid), dim3(kRowWarps * 32), 0, st,
+            x, d, E, K, cap_pad, row_src, kept, buf, rdv);
     else
         launch_pdl(dispatch_gather_kernel<TIO, 1>, dim3(grid), dim3(kRowWarps * 32), 0, st, x, d, E, K, cap_pad,
-                                                                         row_src, kept, buf);
+                   row_src, kept, buf, rdv);
 }
 
 // y[t] = sum_{k kept} w[t*K+k] * O[row_k]  (accumulated from 0 in k order,
@@ -513,7 +518,8 @@ void launch_check_finite_f32(const float* p, int64_t n, uint32_t* flags, cudaStr
 
 #define INST(T)                                                                                  \
     template void launch_dispatch_gather<T>(const T*, int64_t, int, int, int, const int32_t*,   \
-                                            const int32_t*, T*, uint32_t*, cudaStream_t);       \
+                                            const int32_t*, T*, uint32_t*, cudaStream_t,        \
+                                            const RowDst*);                                      \
     template void launch_combine<T>(const T*, int64_t, int64_t, int, int, int, const int32_t*,   \
                                     const int32_t*, const float*, const T*, T*, uint32_t*,       \
                                     cudaStream_t);                                               \

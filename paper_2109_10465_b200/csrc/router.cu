@@ -499,11 +499,16 @@ router_combine_bwd_kernel(int64_t T, int d, int E, int K, const TIO* __restrict_
                           const int32_t* __restrict__ pos, const float* __restrict__ gate_prob,
                           const float* __restrict__ probs, const float* __restrict__ fcoef, float daux,
                           const float* __restrict__ w, const int32_t* __restrict__ kept,
-                          TIO* __restrict__ dO, float* __restrict__ dL, float* __restrict__ dLr) {
+                          TIO* __restrict__ dO, float* __restrict__ dL, float* __restrict__ dLr, RowDst rd) {
     pdl_wait();
     pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t tok_blocks = (T + 7) / 8;
+    // dO row (e, p): local [E][cap_pad], or under EP straight in expert e's owner
+    auto drow = [&](int e, int64_t p) -> TIO* {
+        return rd.ep > 1 ? static_cast<TIO*>(rd.p[e / rd.El]) + ((int64_t)(e % rd.El) * cap_pad + p) * d
+                         : dO + ((int64_t)e * cap_pad + p) * d;
+    };
     if ((int64_t)blockIdx.x >= tok_blocks) {  // expert tails
         const int64_t q = ((int64_t)blockIdx.x - tok_blocks) * 8 + warp;
         const int e = (int)(q / kRowAlign);
@@ -511,20 +516,23 @@ router_combine_bwd_kernel(int64_t T, int d, int E, int K, const TIO* __restrict_
         const int n = kept[e];
         const int64_t p = n + q % kRowAlign;
         if (p >= round_up_dev(n, kRowAlign)) return;
-        TIO* dst = dO + ((int64_t)e * cap_pad + p) * d;
+        TIO* dst = drow(e, p);
         for (int64_t j = (int64_t)lane * V; j < d; j += 32 * V) zero_vec<TIO, V>(dst + j);
         return;
     }
     const int64_t t = (int64_t)blockIdx.x * 8 + warp;
     if (t >= T) return;
     int64_t row[2] = {-1, -1};
+    TIO* dOr_[2] = {nullptr, nullptr};
     float wk[2] = {0.f, 0.f};
 #pragma unroll
     for (int k = 0; k < 2; ++k) {  // K <= 2
         if (k >= K) break;
         const int32_t p = pos[t * K + k];
         if (p < 0) continue;
-        row[k] = (int64_t)choice[t * K + k] * cap_pad + p;
+        const int32_t ce = choice[t * K + k];
+        row[k] = (int64_t)ce * cap_pad + p;
+        dOr_[k] = drow(ce, p);
         wk[k] = w[t * K + k];
     }
     // the softmax-backward operands, loaded ahead of the row traffic (E <= 64)
@@ -549,7 +557,7 @@ router_combine_bwd_kernel(int64_t T, int d, int E, int K, const TIO* __restrict_
             for (int k = 0; k < 2; ++k) {
                 if (row[k] < 0) continue;
                 const TIO* Ok = O + row[k] * d;
-                TIO* dOk = dO + row[k] * d;
+                TIO* dOk = dOr_[k];
                 Vec16<TIO> b[kU];
 #pragma unroll
                 for (int u = 0; u < kU; ++u)
@@ -582,7 +590,7 @@ router_combine_bwd_kernel(int64_t T, int d, int E, int K, const TIO* __restrict_
                     acc[k] = fmaf(a[q], b[q], acc[k]);
                     v[q] = a[q] * wk[k];
                 }
-                store_f<TIO, V>(dO + row[k] * d + j, v);
+                store_f<TIO, V>(dOr_[k] + j, v);
             }
         }
     }
@@ -628,25 +636,29 @@ template <class TIO>
 void launch_router_combine_bwd(int64_t T, int d, int E, int K, const TIO* dy, const TIO* O, int cap_pad,
                                const int32_t* choice, const int32_t* pos, const float* gate_prob,
                                const float* probs, const float* fcoef, float daux, const float* w,
-                               const int32_t* kept, TIO* dO, float* dL, cudaStream_t st, float* dLr) {
+                               const int32_t* kept, TIO* dO, float* dL, cudaStream_t st, float* dLr,
+                               const RowDst* rd) {
+    RowDst r0{};
+    const RowDst& rdv = rd ? *rd : r0;
     if (E > 64) throw Status(6, "router_combine_bwd: E <= 64");
     const unsigned grid = (unsigned)(ceil_div(T, (int64_t)8) + ceil_div((int64_t)E * kRowAlign, (int64_t)8));
     if (vec_width<TIO>(d) > 1)
         launch_pdl(router_combine_bwd_kernel<TIO, 16 / sizeof(TIO)>, dim3(grid), dim3(256), 0, st, T, d, E, K,
-                   dy, O, cap_pad, choice, pos, gate_prob, probs, fcoef, daux, w, kept, dO, dL, dLr);
+                   dy, O, cap_pad, choice, pos, gate_prob, probs, fcoef, daux, w, kept, dO, dL, dLr, rdv);
     else
         launch_pdl(router_combine_bwd_kernel<TIO, 1>, dim3(grid), dim3(256), 0, st, T, d, E, K, dy, O, cap_pad,
-                   choice, pos, gate_prob, probs, fcoef, daux, w, kept, dO, dL, dLr);
+                   choice, pos, gate_prob, probs, fcoef, daux, w, kept, dO, dL, dLr, rdv);
 }
 template void launch_router_combine_bwd<float>(int64_t, int, int, int, const float*, const float*, int,
                                                const int32_t*, const int32_t*, const float*, const float*,
                                                const float*, float, const float*, const int32_t*, float*,
-                                               float*, cudaStream_t, float*);
+                                               float*, cudaStream_t, float*, const RowDst*);
 template void launch_router_combine_bwd<__nv_bfloat16>(int64_t, int, int, int, const __nv_bfloat16*,
                                                        const __nv_bfloat16*, int, const int32_t*,
                                                        const int32_t*, const float*, const float*,
                                                        const float*, float, const float*, const int32_t*,
-                                                       __nv_bfloat16*, float*, cudaStream_t, float*);
+                                                       __nv_bfloat16*, float*, cudaStream_t, float*,
+                                                       const RowDst*);
 
 template <class TIO>
 void launch_router_bwd(int64_t T, int d, int E, int K, const TIO* dy, const TIO* O, int cap_pad,
