@@ -702,7 +702,9 @@ void forward_impl(moe_handle* h, int64_t T, const TIO* x, const float* gate_w, c
     TIO* Xloc = static_cast<TIO*>(h->loc(h->Xr, h->Xloc));
     // under EP with NVLink-mapped buffers the gather stores each row straight
     // into its expert owner's receive buffer (no local copy, no copy pass)
-    const bool peer_dispatch = ep > 1 && h->ipc && !h->no_peer_epi && h->peer_dispatch && ep <= 8;
+    // (not with MOE_B200_DW_EARLY=1: there the barrier that orders the previous
+    // step's dW1 read of Xr before these stores comes only with the exchange)
+    const bool peer_dispatch = ep > 1 && h->ipc && !h->no_peer_epi && h->peer_dispatch && !h->dw_early && ep <= 8;
     RowDst rd{};
     if (peer_dispatch) {
         rd.El = El;
