@@ -113,6 +113,22 @@ __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ uint32_t swz(int r, int c) { return r * 128 + ((c ^ (r & 7)) << 4); }
+// probe 16 (debug): per-stage timeline of CTAs 0..7, [cta][64] ns:
+// [r] producer issued raw stage r, [16+r] transform saw it land, [32+r]
+// transform done with it, [48+r] MMA issued its second step
+// (scripts/micro/gate_timeline.py)
+// (compiled in only with -DMOE_GATE_TIMELINE, so the hot loop carries no probe branch)
+__device__ __forceinline__ void tl(const Params& p, int slot) {
+#ifdef MOE_GATE_TIMELINE
+    if (!(p.probe & 16) || blockIdx.x >= 8 || slot >= 64) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.stamps[blockIdx.x * 64 + slot] = t;
+#else
+    (void)p;
+    (void)slot;
+#endif
+}
 __device__ __forceinline__ void stamp(const Params& p, int i) {
     if (!(p.probe & 8)) return;
     unsigned long long t;
@@ -207,6 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
                 const int k0 = kbase + ((r + kskew) % nraw) * BKR;
                 if (r >= kRaw) mbar_wait(&raw_empty[rs], ((r / kRaw) - 1) & 1);
                 uint8_t* st = raw + rs * kRawStage;
+                if (r < 16) tl(p, r);
                 mbar_expect_tx(&raw_full[rs], bytes);
                 tma_load_2d(&p.tmX, &raw_full[rs], st, k0, static_cast<int32_t>(t0));
                 if (p.has_noise) {
@@ -231,6 +248,7 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
                 const int bs = s % kB, os = s % kOp;
                 mbar_wait(&b_full[bs], (s / kB) & 1);
                 mbar_wait(&op_full[os], (s / kOp) & 1);
+                if ((s & 1) && (s >> 1) < 16) tl(p, 48 + (s >> 1));
                 tc_fence_after();
                 const uint32_t a = smem_u32(op + os * kOpStage);
                 const uint32_t b = smem_u32(bst + bs * kBStage);
@@ -258,6 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
         for (int r = 0; r < nraw; ++r) {
             const int rs = r % kRaw;
             mbar_wait(&raw_full[rs], (r / kRaw) & 1);
+            if (tw == 0 && lane == 0 && r < 16) tl(p, 16 + r);
             const uint8_t* st = raw + rs * kRawStage;
             for (int h = 0; h < 2; ++h) {
                 const int s = 2 * r + h, os = s % kOp;
@@ -298,6 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
                 if (lane == 0) mbar_arrive(&op_full[os]);
             }
             if (lane == 0) mbar_arrive(&raw_empty[rs]);
+            if (tw == 0 && lane == 0 && r < 16) tl(p, 32 + r);
         }
     }
 
@@ -519,9 +539,9 @@ void launch_gate_fused_ep(const __nv_bfloat16* x, const float* noise, const floa
     }();
     p.probe = probe;
     static unsigned long long* stamps = nullptr;
-    if ((probe & 8) && !stamps) MOE_CUDA_CHECK(cudaMalloc(&stamps, 8 * 8 * 4096));
+    if ((probe & 24) && !stamps) MOE_CUDA_CHECK(cudaMalloc(&stamps, 8 * 8 * 4096));
     p.stamps = stamps;
-    if (probe & 8) g_gate_stamps = stamps;
+    if (probe & 24) g_gate_stamps = stamps;
     cudaLaunchAttribute attrs[2];
     attrs[0].id = cudaLaunchAttributeClusterDimension;
     attrs[0].val.clusterDim.x = static_cast<unsigned>(p.csize);
