@@ -43,24 +43,48 @@ using namespace tc;
 // Experts: the kernel is instantiated for EP = 16, 32, 64 TMEM columns per
 // accumulator (the MMA's N); E = 8 runs on the EP = 16 instance with the B
 // operand's rows 8..15 zero and those columns masked out of the routing.
+#ifndef MOE_GATE_TS
+#define MOE_GATE_TS 1
+#endif
+#ifndef MOE_GATE_BBYTES
+#define MOE_GATE_BBYTES 65536
+#endif
+#ifndef MOE_GATE_RAW
+#define MOE_GATE_RAW (MOE_GATE_TS ? 3 : 2)
+#endif
 constexpr int BM = 128;            // tokens per cluster
 constexpr int BK = 32;             // fp32 K elements per MMA step (one 128 B swizzle row)
 constexpr int BKR = 64;            // K elements per raw stage (x rows of 128 B: full DRAM bursts)
-constexpr int kRaw = 2;            // raw x / noise ring depth
-constexpr int kB = 3;              // B (Wg^T hi / lo) ring depth
-constexpr int kOp = 2;             // A-operand ring depth
-constexpr int kNAcc = 4;           // TMEM accumulators
+constexpr int kRaw = MOE_GATE_RAW; // raw x / noise ring depth (the A ring's smem goes here under TS)
+constexpr int kOp = MOE_GATE_TS ? 4 : 2;  // A-operand ring depth (MMA steps)
+#ifndef MOE_GATE_N2
+#define MOE_GATE_N2 MOE_GATE_TS
+#endif
+// TMEM accumulators.  N2 (TS only): B hi and lo sit back to back in the B stage,
+// so hi.hi and hi.lo are ONE MMA with N = 2E into an accumulator of 2E columns
+// ([hh + lh | hl], summed in the epilogue) and lo.hi a second one with N = E:
+// two MMA instructions per K step of 8 instead of three.
+constexpr int kNAcc = MOE_GATE_N2 ? 2 : 4;
+constexpr int kAccW = MOE_GATE_N2 ? 2 : 1;  // accumulator width in units of E
 constexpr int kTw = 8;             // transform warps (two per SM sub-partition)
 constexpr int kThreads = 32 * (2 + kTw);
 constexpr uint32_t kRawX = BM * BKR * 2;       // 16 KB bf16 x   [128 rows x 128 B], 128B swizzle
 constexpr uint32_t kRawN = BM * BKR * 4;       // 32 KB fp32 noise: two [128 x 128 B] halves, swizzled
 constexpr uint32_t kRawStage = kRawX + kRawN;                // 48 KB
+// without jitter (eval) a raw stage is the 16 KB x tile, so the same bytes
+// hold 3x the stages: more loads in flight for the same shared memory
+constexpr int kRawMax = 3 * kRaw;
 constexpr uint32_t kOpStage = 2 * BM * 128;                  // 32 KB (A hi, A lo)
+constexpr uint32_t kOpSmem = MOE_GATE_TS ? 0 : kOp * kOpStage; // A lives in TMEM under TS
 template <int EP> struct GCfg {
     static constexpr uint32_t kRawB = EP * 128;              // per hi / lo: 8 KB at EP = 64
     static constexpr uint32_t kBStage = 2 * kRawB;
+    // B (Wg^T hi / lo) ring depth in MMA steps: 64 KB of B in flight under TS
+    // (L2 latency ~1 us against ~0.5 us per step), 3 steps without
+    static constexpr int kB = MOE_GATE_TS ? (MOE_GATE_BBYTES / kBStage < 16 ? static_cast<int>(MOE_GATE_BBYTES / kBStage) : 16) : 3;
     static constexpr uint32_t kRecv = 64 * EP * 4;           // peer's partials for my rows
-    static constexpr uint32_t kSmem = 1024 + kRaw * kRawStage + kB * kBStage + kOp * kOpStage + kRecv + 512;
+    static constexpr uint32_t kSmem = 1024 + kRaw * kRawStage + kB * kBStage + kOpSmem + kRecv + 512;
+    static_assert((2 * kRawMax + 2 * kB + 2 * kOp + 1) * 8 + 4 <= 512, "barrier area");
 };
 
 struct __align__(64) Params {
@@ -146,22 +170,51 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// A operand in TMEM (tcgen05.mma ... [a_tmem], b_desc): the 3xTF32 products
+// re-read A three times, and with A in shared memory those reads (with the
+// transform's stores) saturate its bandwidth.  The transform then
+// writes hi / lo with tcgen05.st: 32 lanes = 32 token rows of the warp's lane
+// quarter, 16 K columns per warp (two warps per quarter).
+__device__ __forceinline__ void tc_mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+        "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+
 template <int E>
 __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant__ Params p) {
+    // TMEM: kNAcc accumulators of E columns, then (TS) kOp stages of A hi / lo [128 x 32] each
+    constexpr uint32_t kTmemA = kNAcc * kAccW * E;
+    constexpr uint32_t kTmemCols = MOE_GATE_TS ? (kTmemA + kOp * 64 <= 256 ? 256 : 512) : kTmemA;
     constexpr uint32_t kRawB = GCfg<E>::kRawB;
     constexpr uint32_t kBStage = GCfg<E>::kBStage;
     constexpr uint32_t kRecv = GCfg<E>::kRecv;
+    constexpr int kB = GCfg<E>::kB;
     const int ne = p.ne;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* raw = sm;
     uint8_t* bst = raw + kRaw * kRawStage;
     uint8_t* op = bst + kB * kBStage;
-    float* recv = reinterpret_cast<float*>(op + kOp * kOpStage);
+    float* recv = reinterpret_cast<float*>(op + kOpSmem);
     uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(recv) + kRecv);
     uint64_t* raw_full = bars;
-    uint64_t* raw_empty = raw_full + kRaw;
-    uint64_t* b_full = raw_empty + kRaw;
+    uint64_t* raw_empty = raw_full + kRawMax;
+    uint64_t* b_full = raw_empty + kRawMax;
     uint64_t* b_empty = b_full + kB;
     uint64_t* op_full = b_empty + kB;
     uint64_t* op_empty = op_full + kOp;
@@ -178,11 +231,13 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
     const int nraw = kspan / BKR;    // raw stages (two MMA steps each)
     // every cluster walks its K range from a different starting stage, so the
     // 128 CTAs do not all read the same Wg^T tile from L2 at the same time
+    const int nr = p.has_noise ? kRaw : kRawMax;  // raw ring depth and stage stride
+    const uint32_t rstride = p.has_noise ? kRawStage : kRawX;
     const int kskew = static_cast<int>((blockIdx.x / cs) % nraw);
 
     if (threadIdx.x == 0) stamp(p, 0);
     if (threadIdx.x == 0) {
-        for (int i = 0; i < kRaw; ++i) {
+        for (int i = 0; i < kRawMax; ++i) {
             mbar_init(&raw_full[i], 1);
             mbar_init(&raw_empty[i], kTw);  // the transform warps have read x / noise
         }
@@ -203,7 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
-                     "r"(kNAcc * E));
+                     "r"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
@@ -219,10 +274,10 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
         if (lane == 0) {
             const uint32_t bytes = kRawX + (p.has_noise ? kRawN : 0);
             for (int r = 0; r < nraw; ++r) {
-                const int rs = r % kRaw;
+                const int rs = r % nr;
                 const int k0 = kbase + ((r + kskew) % nraw) * BKR;
-                if (r >= kRaw) mbar_wait(&raw_empty[rs], ((r / kRaw) - 1) & 1);
-                uint8_t* st = raw + rs * kRawStage;
+                if (r >= nr) mbar_wait(&raw_empty[rs], ((r / nr) - 1) & 1);
+                uint8_t* st = raw + rs * rstride;
                 if (r < 16) tl(p, r);
                 mbar_expect_tx(&raw_full[rs], bytes);
                 tma_load_2d(&p.tmX, &raw_full[rs], st, k0, static_cast<int32_t>(t0));
@@ -230,14 +285,21 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
                     tma_load_2d(&p.tmN, &raw_full[rs], st + kRawX, k0, static_cast<int32_t>(t0));
                     tma_load_2d(&p.tmN, &raw_full[rs], st + kRawX + kRawN / 2, k0 + BK, static_cast<int32_t>(t0));
                 }
-                for (int h = 0; h < 2; ++h) {
-                    const int s = 2 * r + h, bs = s % kB;
-                    if (s >= kB) mbar_wait(&b_empty[bs], ((s / kB) - 1) & 1);
-                    uint8_t* bt = bst + bs * kBStage;
-                    mbar_expect_tx(&b_full[bs], kBStage);
-                    tma_load_2d(&p.tmBh, &b_full[bs], bt, k0 + h * BK, 0);
-                    tma_load_2d(&p.tmBl, &b_full[bs], bt + kRawB, k0 + h * BK, 0);
-                }
+            }
+        } else if (lane == 1) {
+            // B runs on its own lane, so a B stage held by the MMAs never
+            // delays the next x / noise issue
+            for (int s = 0; s < nsteps; ++s) {
+                const int bs = s % kB;
+                const int k0 = kbase + (((s >> 1) + kskew) % nraw) * BKR + (s & 1) * BK;
+                if (s >= kB) mbar_wait(&b_empty[bs], ((s / kB) - 1) & 1);
+#ifdef MOE_GATE_BSTALE  // timing probe only: B loaded once, then reused (wrong logits)
+                if (s >= kB) { mbar_arrive(&b_full[bs]); continue; }
+#endif
+                uint8_t* bt = bst + bs * kBStage;
+                mbar_expect_tx(&b_full[bs], kBStage);
+                tma_load_2d(&p.tmBh, &b_full[bs], bt, k0, 0);
+                tma_load_2d(&p.tmBl, &b_full[bs], bt + kRawB, k0, 0);
             }
         }
     } else if (warp == 1) {
@@ -247,11 +309,33 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
             for (int s = 0; s < nsteps; ++s) {
                 const int bs = s % kB, os = s % kOp;
                 mbar_wait(&b_full[bs], (s / kB) & 1);
+#ifndef MOE_GATE_NOOPWAIT  // timing probe only: MMAs do not wait for the transform
                 mbar_wait(&op_full[os], (s / kOp) & 1);
+#endif
                 if ((s & 1) && (s >> 1) < 16) tl(p, 48 + (s >> 1));
                 tc_fence_after();
-                const uint32_t a = smem_u32(op + os * kOpStage);
                 const uint32_t b = smem_u32(bst + bs * kBStage);
+#if MOE_GATE_TS
+                const uint32_t ta = tmem + kTmemA + os * 64;  // hi at +0, lo at +32 columns
+#pragma unroll
+                for (int kk = 0; kk < BK / 8; ++kk) {
+                    if (p.probe & 2) break;
+                    const uint64_t bh = sdesc(b + kk * 32, 16, 1024);
+#if MOE_GATE_N2
+                    constexpr uint32_t idesc2 = make_idesc_tf32(BM, 2 * E, 0, 0);
+                    const uint32_t acc = tmem + (kk % kNAcc) * 2 * E;
+                    tc_mma_tf32_ts(acc, ta + kk * 8, bh, idesc2, (s || kk >= kNAcc) ? 1u : 0u);  // [hh | hl]
+                    tc_mma_tf32_ts(acc, ta + 32 + kk * 8, bh, idesc, 1u);                      // += lh
+#else
+                    const uint64_t bl = sdesc(b + kRawB + kk * 32, 16, 1024);
+                    const uint32_t acc = tmem + kk * E;
+                    tc_mma_tf32_ts(acc, ta + kk * 8, bh, idesc, s ? 1u : 0u);
+                    tc_mma_tf32_ts(acc, ta + kk * 8, bl, idesc, 1u);
+                    tc_mma_tf32_ts(acc, ta + 32 + kk * 8, bh, idesc, 1u);
+#endif
+                }
+#else
+                const uint32_t a = smem_u32(op + os * kOpStage);
 #pragma unroll
                 for (int kk = 0; kk < BK / 8; ++kk) {
                     if (p.probe & 2) break;
@@ -264,20 +348,77 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
                     tc_mma_tf32(acc, ah, bl, idesc, 1u);
                     tc_mma_tf32(acc, al, bh, idesc, 1u);
                 }
+#endif
                 tc_commit(&op_empty[os]);  // A operand stage free
                 tc_commit(&b_empty[bs]);   // B stage free
             }
             tc_commit(acc_full);
         }
     } else {
-        // ---------------- transform: g = x * noise -> tf32 hi / lo, swizzled K-major
+#if MOE_GATE_TS
+        // ---------------- transform: g = x * noise -> tf32 hi / lo into TMEM.
+        // Warp w owns TMEM lane quarter w % 4 (token rows 32q + lane) and one
+        // half of each op stage's 32 K columns; each thread reads its own row.
+        const int tw = warp - 2;
+        const int q4 = warp & 3, hf = tw >> 2;
+        const int row = q4 * 32 + lane;
+        for (int r = 0; r < nraw; ++r) {
+            const int rs = r % nr;
+            mbar_wait(&raw_full[rs], (r / nr) & 1);
+            if (tw == 0 && lane == 0 && r < 16) tl(p, 16 + r);
+            const uint8_t* st = raw + rs * rstride;
+            for (int h = 0; h < 2; ++h) {
+                const int s = 2 * r + h, os = s % kOp;
+                // x: 16 bf16 = two 16 B chunks (columns 32h + 16hf ..) of the row
+                const int kx = 4 * h + 2 * hf;
+                const uint4 x0 = *reinterpret_cast<const uint4*>(st + row * 128 + ((kx ^ (row & 7)) << 4));
+                const uint4 x1 = *reinterpret_cast<const uint4*>(st + row * 128 + (((kx + 1) ^ (row & 7)) << 4));
+                float g[16];
+                {
+                    const uint32_t xw[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        g[2 * i] = __uint_as_float(xw[i] << 16);
+                        g[2 * i + 1] = __uint_as_float(xw[i] & 0xffff0000u);
+                    }
+                }
+                if (p.has_noise) {  // noise half h: [128 rows][32 fp32], chunks 4hf .. 4hf+3
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const float4 nv = *reinterpret_cast<const float4*>(st + kRawX + h * (kRawN / 2) + swz(row, 4 * hf + i));
+                        g[4 * i] *= nv.x; g[4 * i + 1] *= nv.y; g[4 * i + 2] *= nv.z; g[4 * i + 3] *= nv.w;
+                    }
+                }
+                uint32_t hi[16], lo[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const float hv = (p.probe & 1) ? g[i] : tf32_rna(g[i]);
+                    hi[i] = __float_as_uint(hv);
+                    lo[i] = __float_as_uint((p.probe & 1) ? g[i] : tf32_rna(g[i] - hv));
+                }
+                if (s >= kOp) mbar_wait(&op_empty[os], ((s / kOp) - 1) & 1);
+                tc_fence_after();
+                const uint32_t ta = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + kTmemA + os * 64 + 16 * hf;
+                tmem_st16(ta, hi);
+                tmem_st16(ta + 32, lo);
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&op_full[os]);
+            }
+            if (lane == 0) mbar_arrive(&raw_empty[rs]);
+            if (tw == 0 && lane == 0 && r < 16) tl(p, 32 + r);
+        }
+    }
+#else
+
         const int tw = warp - 2;  // rows [16 tw, 16 tw + 16)
         const int c = lane & 7;   // 4-element K chunk of the 32-element MMA step
         for (int r = 0; r < nraw; ++r) {
-            const int rs = r % kRaw;
-            mbar_wait(&raw_full[rs], (r / kRaw) & 1);
+            const int rs = r % nr;
+            mbar_wait(&raw_full[rs], (r / nr) & 1);
             if (tw == 0 && lane == 0 && r < 16) tl(p, 16 + r);
-            const uint8_t* st = raw + rs * kRawStage;
+            const uint8_t* st = raw + rs * rstride;
             for (int h = 0; h < 2; ++h) {
                 const int s = 2 * r + h, os = s % kOp;
                 if (s >= kOp) mbar_wait(&op_empty[os], ((s / kOp) - 1) & 1);
@@ -320,6 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
             if (tw == 0 && lane == 0 && r < 16) tl(p, 32 + r);
         }
     }
+#endif
 
     // ---------------- epilogue
     float L[E];
@@ -332,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
         tc_fence_after();
         if (warp == 2 && lane == 0) stamp(p, 2);
 #pragma unroll
-        for (int a = 0; a < kNAcc; ++a) {
+        for (int a = 0; a < kNAcc * kAccW; ++a) {
             if constexpr (E == 16) {
                 uint32_t v[16];
                 tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + a * E, v);
@@ -360,7 +502,7 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
     cluster_sync();  // every partial has landed; both CTAs stay resident until here
     if (warp == 2 && lane == 0) stamp(p, 4);
     // owner warps: logits = own half + peer half, then the row's routing
-    float* sP = reinterpret_cast<float*>(op);                // [64 or 128][E + 1] after the loop
+    float* sP = reinterpret_cast<float*>(raw);               // [64 or 128][E + 1]: the raw ring is idle after the loop
     int32_t* sC = reinterpret_cast<int32_t*>(sP + 128 * (E + 1));
     const int64_t t = t0 + row;
     uint32_t flag = 0;
@@ -459,7 +601,7 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kNAcc * E));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
     }
 }
 

@@ -243,9 +243,11 @@ def test_fused_gate_matches_split_kernels(top_k, T, E):
         outs.append((dec.expert_id.cpu(), dec.slot.cpu(), dec.gate_prob.cpu(), float(aux[0]), y.float().cpu()))
     (e1, s1, g1, a1, y1), (e0, s0, g0, a0, y0) = outs
     assert torch.equal(e1, e0) and torch.equal(s1, s0)
-    # the two paths sum the d products in different orders (3xTF32 in TMEM vs
-    # split-K FMA partials): a few fp32 ulps of the logits, scaled by p ~ 1/E
-    assert float((g1 - g0).abs().max()) <= (2e-6 if E == 64 else 1e-5)
+    # the two paths sum the d products in different orders (3xTF32 with the
+    # hi.lo products in their own TMEM columns vs split-K FMA partials): a few
+    # fp32 ulps of the logits, scaled by p ~ 1/E.  Both paths are held to the
+    # oracle's bound by the vs_oracle / full-size tests.
+    assert float((g1 - g0).abs().max()) <= (5e-6 if E == 64 else 1e-5)
     assert abs(a1 - a0) <= 1e-6 * max(1.0, abs(a0))
     assert float((y1 - y0).abs().max()) <= 2e-2 * max(1.0, float(y0.abs().max()))
 
