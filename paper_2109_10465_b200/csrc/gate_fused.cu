@@ -76,15 +76,26 @@ constexpr uint32_t kRawStage = kRawX + kRawN;                // 48 KB
 constexpr int kRawMax = 3 * kRaw;
 constexpr uint32_t kOpStage = 2 * BM * 128;                  // 32 KB (A hi, A lo)
 constexpr uint32_t kOpSmem = MOE_GATE_TS ? 0 : kOp * kOpStage; // A lives in TMEM under TS
-template <int EP> struct GCfg {
+// SM2: the eval-only (no jitter) instance for EP = 16 sized for TWO CTAs per SM
+// (smem ~103 KB, 256 TMEM columns, <= 102 registers): without jitter the main
+// loop is a latency chain (TMA -> transform -> MMA), and a second resident
+// CTA runs a second chain on the same SM.
+template <int EP, bool SM2 = false> struct GCfg {
     static constexpr uint32_t kRawB = EP * 128;              // per hi / lo: 8 KB at EP = 64
     static constexpr uint32_t kBStage = 2 * kRawB;
     // B (Wg^T hi / lo) ring depth in MMA steps: 64 KB of B in flight under TS
     // (L2 latency ~1 us against ~0.5 us per step), 3 steps without
-    static constexpr int kB = MOE_GATE_TS ? (MOE_GATE_BBYTES / kBStage < 16 ? static_cast<int>(MOE_GATE_BBYTES / kBStage) : 16) : 3;
+    static constexpr int kB = SM2 ? 8 : MOE_GATE_TS ? (MOE_GATE_BBYTES / kBStage < 16 ? static_cast<int>(MOE_GATE_BBYTES / kBStage) : 16) : 3;
+    static constexpr int kRawT = SM2 ? 1 : kRaw;             // raw stages with jitter (SM2: unused)
+    static constexpr int kRawE = SM2 ? 4 : kRawMax;          // raw stages without jitter (16 KB each)
+    static constexpr int kRawM = kRawT > kRawE ? kRawT : kRawE;
+    static constexpr uint32_t kRawBytes = SM2 ? kRawE * kRawX : kRaw * kRawStage;
+    static constexpr int kOpD = SM2 ? 2 : kOp;               // A ring depth (MMA steps)
     static constexpr uint32_t kRecv = 64 * EP * 4;           // peer's partials for my rows
-    static constexpr uint32_t kSmem = 1024 + kRaw * kRawStage + kB * kBStage + kOpSmem + kRecv + 512;
-    static_assert((2 * kRawMax + 2 * kB + 2 * kOp + 1) * 8 + 4 <= 512, "barrier area");
+    static constexpr uint32_t kSmem = 1024 + kRawBytes + kB * kBStage + kOpSmem + kRecv + 512;
+    static constexpr int kMinBlocks = SM2 ? 2 : 1;
+    static_assert((2 * kRawM + 2 * kB + 2 * kOpD + 1) * 8 + 4 <= 512, "barrier area");
+    static_assert(!SM2 || (MOE_GATE_TS && kSmem + 1024 <= 232448 / 2), "SM2 shared memory");
 };
 
 struct __align__(64) Params {
@@ -195,26 +206,31 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16
         : "memory");
 }
 
-template <int E>
-__global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant__ Params p) {
+template <int E, bool SM2>
+__global__ void __launch_bounds__(kThreads, GCfg<E, SM2>::kMinBlocks) gate_kernel(const __grid_constant__ Params p) {
+    using C = GCfg<E, SM2>;
+    constexpr int kOp = C::kOpD;
+    constexpr int kRaw = C::kRawT;
+    constexpr int kRawMax = C::kRawE;  // the no-jitter ring depth (the ring's max)
     // TMEM: kNAcc accumulators of E columns, then (TS) kOp stages of A hi / lo [128 x 32] each
     constexpr uint32_t kTmemA = kNAcc * kAccW * E;
     constexpr uint32_t kTmemCols = MOE_GATE_TS ? (kTmemA + kOp * 64 <= 256 ? 256 : 512) : kTmemA;
-    constexpr uint32_t kRawB = GCfg<E>::kRawB;
-    constexpr uint32_t kBStage = GCfg<E>::kBStage;
-    constexpr uint32_t kRecv = GCfg<E>::kRecv;
-    constexpr int kB = GCfg<E>::kB;
+    constexpr uint32_t kRawB = C::kRawB;
+    constexpr uint32_t kBStage = C::kBStage;
+    constexpr uint32_t kRecv = C::kRecv;
+    constexpr int kB = C::kB;
+    static_assert(C::kRawM == (kRaw > kRawMax ? kRaw : kRawMax), "ring");
     const int ne = p.ne;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* raw = sm;
-    uint8_t* bst = raw + kRaw * kRawStage;
+    uint8_t* bst = raw + C::kRawBytes;
     uint8_t* op = bst + kB * kBStage;
     float* recv = reinterpret_cast<float*>(op + kOpSmem);
     uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(recv) + kRecv);
     uint64_t* raw_full = bars;
-    uint64_t* raw_empty = raw_full + kRawMax;
-    uint64_t* b_full = raw_empty + kRawMax;
+    uint64_t* raw_empty = raw_full + C::kRawM;
+    uint64_t* b_full = raw_empty + C::kRawM;
     uint64_t* b_empty = b_full + kB;
     uint64_t* op_full = b_empty + kB;
     uint64_t* op_empty = op_full + kOp;
@@ -237,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1) gate_kernel(const __grid_constant
 
     if (threadIdx.x == 0) stamp(p, 0);
     if (threadIdx.x == 0) {
-        for (int i = 0; i < kRawMax; ++i) {
+        for (int i = 0; i < C::kRawM; ++i) {
             mbar_init(&raw_full[i], 1);
             mbar_init(&raw_empty[i], kTw);  // the transform warps have read x / noise
         }
@@ -637,18 +653,28 @@ void launch_gate_split(const float* wg, float* wsplit, int d, int E, cudaStream_
                0, st, wg, wsplit, wsplit + static_cast<int64_t>(d) * EP, d, E, EP);
 }
 
+namespace {
+bool gate_sm2_on() {  // MOE_B200_GATE_SM2=0: the eval E <= 16 gate on the one-CTA-per-SM instance
+    static const bool on = [] {
+        const char* e = std::getenv("MOE_B200_GATE_SM2");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+}  // namespace
+
 int gate_fused_parts(int64_t T) { return static_cast<int>(ceil_div(T, static_cast<int64_t>(64))); }
 
 namespace {
-template <int EP>
+template <int EP, bool SM2>
 void launch_gate_fused_ep(const __nv_bfloat16* x, const float* noise, const float* wsplit, int64_t T, int d, int K,
                           int E, float* probs, int32_t* choice, float* gate_prob, float* colsum_part,
                           int32_t* count_part, uint32_t* flags, cudaStream_t st) {
     using namespace gf;
-    constexpr uint32_t kSmem = GCfg<EP>::kSmem;
+    constexpr uint32_t kSmem = GCfg<EP, SM2>::kSmem;
     static bool attr = false;
     if (!attr) {
-        MOE_CUDA_CHECK(cudaFuncSetAttribute(gate_kernel<EP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        MOE_CUDA_CHECK(cudaFuncSetAttribute(gate_kernel<EP, SM2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             static_cast<int>(kSmem)));
         attr = true;
     }
@@ -672,7 +698,8 @@ void launch_gate_fused_ep(const __nv_bfloat16* x, const float* noise, const floa
     const unsigned tiles = static_cast<unsigned>(ceil_div(T, static_cast<int64_t>(BM)));
     // more tiles than one wave of CTA pairs: one CTA per tile takes all of d,
     // halving the per-CTA setup / pipeline fill / epilogue per byte
-    p.csize = tiles > static_cast<unsigned>(kNumSMs / 2) && d % BKR == 0 ? 1 : 2;
+    // (SM2: two resident CTAs per SM, so pairs pay up to one tile per SM)
+    p.csize = tiles > static_cast<unsigned>(SM2 ? kNumSMs : kNumSMs / 2) && d % BKR == 0 ? 1 : 2;
     p.nparts = gate_fused_parts(T);
     p.has_noise = noise != nullptr;
     static const int probe = [] {
@@ -698,7 +725,7 @@ void launch_gate_fused_ep(const __nv_bfloat16* x, const float* noise, const floa
     cfg.stream = st;
     cfg.attrs = attrs;
     cfg.numAttrs = 2;
-    MOE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gate_kernel<EP>, p));
+    MOE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gate_kernel<EP, SM2>, p));
     count_launch();
 }
 }  // namespace
@@ -707,11 +734,17 @@ void launch_gate_fused(const __nv_bfloat16* x, const float* noise, const float* 
                        int E, float* probs, int32_t* choice, float* gate_prob, float* colsum_part,
                        int32_t* count_part, uint32_t* flags, cudaStream_t st) {
     switch (gf::padded_experts(E)) {
-        case 16: launch_gate_fused_ep<16>(x, noise, wsplit, T, d, K, E, probs, choice, gate_prob, colsum_part,
+        case 16:
+            if (!noise && gate_sm2_on())
+                launch_gate_fused_ep<16, true>(x, noise, wsplit, T, d, K, E, probs, choice, gate_prob, colsum_part,
+                                               count_part, flags, st);
+            else
+                launch_gate_fused_ep<16, false>(x, noise, wsplit, T, d, K, E, probs, choice, gate_prob, colsum_part,
+                                                count_part, flags, st);
+            break;
+        case 32: launch_gate_fused_ep<32, false>(x, noise, wsplit, T, d, K, E, probs, choice, gate_prob, colsum_part,
                                           count_part, flags, st); break;
-        case 32: launch_gate_fused_ep<32>(x, noise, wsplit, T, d, K, E, probs, choice, gate_prob, colsum_part,
-                                          count_part, flags, st); break;
-        case 64: launch_gate_fused_ep<64>(x, noise, wsplit, T, d, K, E, probs, choice, gate_prob, colsum_part,
+        case 64: launch_gate_fused_ep<64, false>(x, noise, wsplit, T, d, K, E, probs, choice, gate_prob, colsum_part,
                                           count_part, flags, st); break;
         default: throw Status(6, "gate_fused: experts must be 8, 16, 32 or 64");
     }

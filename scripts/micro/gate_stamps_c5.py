@@ -28,7 +28,8 @@ for i in range(4):
     L.forward(x, p, M.Phase.TRAIN if train else M.Phase.EVAL, 42 + i, decision=False, check=False)
 torch.cuda.synchronize()
 tiles = (T + 127) // 128
-ncta = tiles * (1 if tiles > 74 else 2)
+sm2 = E <= 16 and not train and os.environ.get("MOE_B200_GATE_SM2", "1") != "0"
+ncta = tiles * (1 if tiles > (148 if sm2 else 74) else 2)
 buf = np.zeros(ncta * 8, np.uint64)
 n = C.c_int()
 _lib.load().moe_debug_gate_stamps(buf.ctypes.data_as(C.c_void_p), ncta, C.byref(n))

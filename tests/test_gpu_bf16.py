@@ -217,6 +217,19 @@ def test_bf16_gemm_variants_subprocess(pair):
                                        (2, 1000, 16), (1, 2048, 32), (2, 300, 32),
                                        (1, 16384, 64), (2, 12000, 16)])
 def test_fused_gate_matches_split_kernels(top_k, T, E):
+    _fused_gate_vs_split(top_k, T, E, "TRAIN")
+
+
+@pytest.mark.parametrize("top_k,T,E", [(1, 16384, 16), (2, 1000, 16), (1, 4096, 8), (1, 40000, 16),
+                                       (1, 8192, 64), (2, 3000, 32)])
+def test_fused_gate_eval_matches_split_kernels(top_k, T, E):
+    """Eval (no jitter): E <= 16 runs the two-CTAs-per-SM instance
+    (GCfg<16, true>), as a CTA pair for T <= 148 tiles and one CTA per tile
+    above; E = 32 / 64 the jitter-free ring of the one-CTA instance."""
+    _fused_gate_vs_split(top_k, T, E, "EVAL")
+
+
+def _fused_gate_vs_split(top_k, T, E, phase):
     """The fused gate (gate_fused.cu: logits + softmax + top-k + balance loss in
     one cluster kernel) against the split kernels (MOE_B200_GATE_FUSED=0:
     split-K logits, softmax_topk, balance_finalize) on the same inputs:
@@ -229,7 +242,7 @@ def test_fused_gate_matches_split_kernels(top_k, T, E):
     d, f, seed = 2048, 256, 5
     x0, gw, *_ = O.layer_inputs(T, d, 8, E, seed=seed)
     ocfg = O.make_cfg(num_experts=E, top_k=top_k)
-    x = margin_guard(bf16_round(x0), gw, ocfg, O.TRAIN, seed, round_fn=bf16_round)
+    x = margin_guard(bf16_round(x0), gw, ocfg, getattr(O, phase), seed, round_fn=bf16_round)
     outs = []
     for fused in ("1", "0"):
         os.environ["MOE_B200_GATE_FUSED"] = fused
@@ -238,7 +251,7 @@ def test_fused_gate_matches_split_kernels(top_k, T, E):
                                             dict(top_k=top_k))
         finally:
             os.environ.pop("MOE_B200_GATE_FUSED", None)
-        y, aux, dec = layer.forward(xd, p, M.Phase.TRAIN, seed)
+        y, aux, dec = layer.forward(xd, p, getattr(M.Phase, phase), seed)
         torch.cuda.synchronize()
         outs.append((dec.expert_id.cpu(), dec.slot.cpu(), dec.gate_prob.cpu(), float(aux[0]), y.float().cpu()))
     (e1, s1, g1, a1, y1), (e0, s0, g0, a0, y0) = outs
