@@ -408,7 +408,8 @@ def run_ours(args):
         ev_c.record(st)
         with torch.cuda.stream(s_out):
             s_out.wait_event(ev_c)
-            dx_h[b].copy_(gb[b]["dx"], non_blocking=True)
+            if args.e2e_readback == "dx":
+                dx_h[b].copy_(gb[b]["dx"], non_blocking=True)
             aux_h[b].copy_(auxb[b], non_blocking=True)
             done[b].record(s_out)
 
@@ -426,7 +427,9 @@ def run_ours(args):
     clocks.mark(w0, time.time())
     clk = clocks.stop() if rank == 0 else None
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
-    assert torch.equal(dx_h[(args.steps - 1) % 2].view(torch.int16), gb[(args.steps - 1) % 2]["dx"].cpu().view(torch.int16))
+    if args.e2e_readback == "dx":
+        assert torch.equal(dx_h[(args.steps - 1) % 2].view(torch.int16),
+                           gb[(args.steps - 1) % 2]["dx"].cpu().view(torch.int16))
     e2e_value = N * T / (e2e_ms / 1e3)
     layer.handle.check()
 
@@ -521,7 +524,9 @@ def run_ours(args):
             "expert_gemms": {"ms_per_step": gemm_ms, "tflops": gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms else None,
                              "frac_of_bf16_sustained": (gemm_flops / (gemm_ms / 1e3) / 1e12) / tf_sus if gemm_ms else None},
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms,
-                    "h2d_bytes_per_step": 2 * T * d * 2, "d2h_bytes_per_step": T * d * 2 + 4},
+                    "h2d_bytes_per_step": 2 * T * d * 2,
+                    "d2h_bytes_per_step": (T * d * 2 if args.e2e_readback == "dx" else 0) + 4,
+                    "readback": args.e2e_readback},
             "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
             "clocks": clk, "stages_ms": {k: round(v["ms"], 4) for k, v in per_stage.items()},
             "stage_roofline": dict(stage_roof, note="SURVEY 8(d) algorithmic bytes; the gate stage also generates "
@@ -698,6 +703,8 @@ def main():
                     help="config-3 variant with this many experts in total (EP-overhead baselines: "
                          "1 GPU with E=64/N experts has the same rows per expert as N GPUs with E=64)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-readback", default="dx", choices=["dx", "aux"],
+                    help="e2e: read back dx + aux every step (default) or only the aux loss")
     ap.add_argument("--no-prefetch", dest="prefetch", action="store_false",
                     help="generate the next step's jitter stream during this step's backward "
                          "(moe_prefetch_jitter, default on: generate the next step's jitter stream next to "
