@@ -624,6 +624,8 @@ def run_extra(args):
     def step(i):
         h = x0
         for l in range(L):  # stack: zero residual inside blocks (model.cpp:340-350)
+            if args.prefetch and w["phase"] == 0:  # next step's stream of this layer, next to its GEMMs
+                layers[l].prefetch_jitter(M.derive_seed(M.derive_seed(M.derive_seed(42, rank), i + 1), l), T)
             layers[l].forward(h, params[l], phase, M.derive_seed(M.derive_seed(M.derive_seed(42, rank), i), l),
                               residual=zero if L > 1 else None, y=ys[l], aux=aux, decision=False,
                               check=False)
@@ -651,8 +653,9 @@ def run_extra(args):
         layers[0].handle.profile(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
+    nw = max(args.warmup, 3)  # timed steps continue the seed sequence (prefetched streams match)
     for i in range(args.steps):
-        step(i)
+        step(nw + i)
     e1.record()
     barrier()
     ms = e0.elapsed_time(e1) / args.steps
@@ -667,7 +670,9 @@ def run_extra(args):
             "dtype": w["dtype"], "data": "synthetic",
             "config": {"workload": args.workload, "desc": w["desc"], "tokens_per_gpu": T,
                        "layers": L, "experts": E, "experts_per_gpu": El, "d_model": d, "d_ff": f,
-                       "top_k": w["k"], "parallelism": f"ep{N}"},
+                       "top_k": w["k"], "parallelism": f"ep{N}",
+                       "jitter": ("prefetched one step ahead per layer" if args.prefetch else "inline")
+                       if w["phase"] == 0 else "none (eval)"},
             "expert_tflops_upper_bound_per_gpu": flops / (ms / 1e3) / 1e12}
     if prof:  # inference regime: gate / dispatch / combine against the HBM roofline
         hbm = peaks()[0]

@@ -98,9 +98,12 @@ class MoeStack:
             layer.ep_init(uid)
 
     def forward(self, x: torch.Tensor, params: list, phase: Phase, seed: int, between=None,
-                stats: bool = True):
+                stats: bool = True, next_seed: int | None = None):
         """Returns (stream_out, aux_loss [1] fp32, decisions).  ``between(l, h)``
-        (optional) maps the stream before MoE layer l (e.g. a layer norm)."""
+        (optional) maps the stream before MoE layer l (e.g. a layer norm).
+        ``next_seed`` (training): the next step's seed; each layer then
+        generates its next jitter stream during this call, next to its expert
+        GEMMs (moe_prefetch_jitter), instead of at the head of its next forward."""
         h = x
         aux_sum = torch.zeros(1, device=x.device, dtype=torch.float32)
         decisions = []
@@ -108,6 +111,8 @@ class MoeStack:
         self._inputs = []
         for ordinal, (layer, p) in enumerate(zip(self.layers, params)):
             inp = between(ordinal, h) if between is not None else h
+            if next_seed is not None and phase == Phase.TRAIN:
+                layer.prefetch_jitter(derive_seed(next_seed, ordinal), inp.shape[0])
             y, aux, dec = layer.forward(inp, p, phase, derive_seed(seed, ordinal), residual=self._zero,
                                         check=False)
             aux_sum += aux

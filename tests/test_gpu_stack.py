@@ -135,3 +135,38 @@ def test_drop_histogram_top2_rts_bf16():
     assert h1.buckets == list(map(int, b))
     assert h1.total_dropped == int((slot == -1).sum())
     assert u1.as_lists()[0] == list(map(int, np.bincount(eid[:, 0], minlength=E)))
+
+
+def test_stack_next_seed_prefetch_is_bit_identical():
+    """MoeStack.forward(next_seed=...): every layer generates its next jitter
+    stream during this call (moe_prefetch_jitter, on reserved SMs next to its
+    expert GEMMs).  The next step must be bit-identical to one whose layers
+    draw the stream at the head of their forward."""
+    import torch
+    import paper_2109_10465_b200 as M
+    from paper_2109_10465_b200.stack import MoeStack
+
+    T, d, f, E, nl = 1024, 256, 512, 16, 3
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(3)
+    r = lambda *s: torch.rand(*s, device=dev, generator=g) * 2 - 1  # noqa: E731
+    params = [M.MoeLayerParams(r(d, E) * 0.1, (r(E, d, f) * 0.05).bfloat16(), r(E, f) * 0.01,
+                               (r(E, f, d) * 0.05).bfloat16(), r(E, d) * 0.01) for _ in range(nl)]
+    x, dy = r(T, d).bfloat16(), r(T, d).bfloat16()
+    cfg = M.RouterConfig(num_experts=E)
+    outs = []
+    for pre in (True, False):
+        st = MoeStack(cfg, nl, T, d, f, torch.bfloat16)
+        if pre:
+            st.forward(x, params, M.Phase.TRAIN, 11, stats=False, next_seed=12)
+            st.backward(dy)
+        h, aux, _ = st.forward(x, params, M.Phase.TRAIN, 12, stats=False)
+        dx, grads = st.backward(dy)
+        torch.cuda.synchronize()
+        outs.append((h.clone(), aux.clone(), dx.clone(), [{k: v.clone() for k, v in gl.items() if v is not None}
+                                                          for gl in grads]))
+    (h1, a1, dx1, g1), (h0, a0, dx0, g0) = outs
+    assert torch.equal(h1, h0) and torch.equal(a1, a0) and torch.equal(dx1, dx0)
+    for l in range(nl):
+        for k in g0[l]:
+            assert torch.equal(g1[l][k], g0[l][k]), (l, k)
