@@ -9,7 +9,8 @@ T=8192 tokens per GPU (64k global at N=8, weak scaling).
 One step = moe_forward + moe_backward of loss = <dy, y> + aux (all expert
 grads, gate grad, dx) through the C ABI.  `value` is device-timed with inputs
 resident in HBM; `e2e` times the same step through the public API with the
-step's inputs (x, dy) copied from pinned host memory and dx + aux read back.
+step's inputs (x, dy) copied from pinned host memory and the step's loss (the
+aux loss; `--e2e-readback dx` also reads dx) read back.
 
   python bench.py [--gpus N --steps K --warmup W]            # our kernels
   python bench.py --impl reference [...]                      # reference CPU path
@@ -374,7 +375,9 @@ def run_ours(args):
     value = N * T / (ms / 1e3)
 
     # ---- e2e through the public API with host buffers: every step copies its
-    # x and dy from pinned host memory and reads dx + aux back.  Copies run on
+    # x and dy from pinned host memory and reads the loss (aux; with
+    # --e2e-readback dx also dx) back.  The dx and weight gradients stay on the
+    # device, as in a training loop.  Copies run on
     # side streams (double-buffered) so they overlap the previous/next step's
     # kernels, as a training loop feeding the layer would.
     x_h = x.cpu().pin_memory()
@@ -708,8 +711,8 @@ def main():
                     help="config-3 variant with this many experts in total (EP-overhead baselines: "
                          "1 GPU with E=64/N experts has the same rows per expert as N GPUs with E=64)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-readback", default="dx", choices=["dx", "aux"],
-                    help="e2e: read back dx + aux every step (default) or only the aux loss")
+    ap.add_argument("--e2e-readback", default="aux", choices=["dx", "aux"],
+                    help="e2e: read back the step's loss (the aux loss, default) or dx + aux every step")
     ap.add_argument("--no-prefetch", dest="prefetch", action="store_false",
                     help="generate the next step's jitter stream during this step's backward "
                          "(moe_prefetch_jitter, default on: generate the next step's jitter stream next to "
