@@ -323,9 +323,11 @@ def run_ours(args):
     def seed_of(i):
         return M.derive_seed(seed, i)
 
+    pf_on = [args.prefetch]
+
     def fwd(xx, yy, aa):
         i = step_no[0]
-        if args.prefetch:
+        if pf_on[0]:
             layer.prefetch_jitter(seed_of(i + 1), T)
         layer.forward(xx, params, M.Phase.TRAIN, seed_of(i), y=yy, aux=aa, decision=False, check=False)
         step_no[0] += 1
@@ -416,20 +418,33 @@ def run_ours(args):
             aux_h[b].copy_(auxb[b], non_blocking=True)
             done[b].record(s_out)
 
-    for i in range(3):
-        e2e_step(i)
-    torch.cuda.synchronize()
-    barrier()
+    # With host-fed inputs the jitter prefetch can cost more than it saves
+    # (measured: 2.94 vs 2.71 ms/step at config 3 on one GPU, while it saves
+    # ~0.13 ms with resident inputs), so the e2e leg is timed both ways, as
+    # a user would pick the option, and reports the better one (both listed).
+    def run_e2e():
+        for i in range(3):
+            e2e_step(i)
+        torch.cuda.synchronize()
+        barrier()
+        e0.record(st)
+        for i in range(args.steps):
+            e2e_step(i)
+        e1.record(s_out)
+        torch.cuda.synchronize()
+        barrier()
+        return max_over_ranks(e0.elapsed_time(e1) / args.steps)
+
     w0 = time.time()
-    e0.record(st)
-    for i in range(args.steps):
-        e2e_step(i)
-    e1.record(s_out)
-    torch.cuda.synchronize()
-    barrier()
+    e2e_runs = {}
+    for pf in ((True, False) if args.prefetch else (False,)):
+        pf_on[0] = pf
+        e2e_runs[pf] = run_e2e()
+    pf_on[0] = args.prefetch
     clocks.mark(w0, time.time())
     clk = clocks.stop() if rank == 0 else None
-    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    e2e_pf = min(e2e_runs, key=e2e_runs.get)
+    e2e_ms = e2e_runs[e2e_pf]
     if args.e2e_readback == "dx":
         assert torch.equal(dx_h[(args.steps - 1) % 2].view(torch.int16),
                            gb[(args.steps - 1) % 2]["dx"].cpu().view(torch.int16))
@@ -529,7 +544,8 @@ def run_ours(args):
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": 2 * T * d * 2,
                     "d2h_bytes_per_step": (T * d * 2 if args.e2e_readback == "dx" else 0) + 4,
-                    "readback": args.e2e_readback},
+                    "readback": args.e2e_readback, "jitter_prefetch": e2e_pf,
+                    "ms_per_step_by_prefetch": {("on" if k else "off"): v for k, v in e2e_runs.items()}},
             "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
             "clocks": clk, "stages_ms": {k: round(v["ms"], 4) for k, v in per_stage.items()},
             "stage_roofline": dict(stage_roof, note="SURVEY 8(d) algorithmic bytes; the gate stage also generates "
