@@ -179,9 +179,6 @@ struct moe_handle {
     // the peers' dispatch stores of the next step; with it moved, the next
     // dispatch exchange first runs an extra barrier.
     bool dw_early = false;
-    // gate dW on the side stream next to gate dx (one GPU; MOE_B200_GATE_DW_SIDE=0: in series)
-    bool dw_side = true;
-    cudaEvent_t ev_dw = nullptr;
     bool gate_dw_tma = false;    // dWg by the TMA-fed MN-major kernel (gate_bwd.cu)
     bool gate_dx_tma = false;    // dx by the persistent TMA-fed kernel (gate_bwd.cu)
     bool relu_bits_on = true;    // dgrad2 reads the ReLU mask as bits (MOE_B200_RELU_BITS=0: reads H)
@@ -191,7 +188,7 @@ struct moe_handle {
         for (int b = 0; b < P_NBUF; ++b)
             for (int r = 0; r < 8; ++r)
                 if (ipc && r != rank && peer[b][r]) cudaIpcCloseMemHandle(peer[b][r]);
-        for (cudaEvent_t e : {ev_a, ev_b, ev_c, ev_side, ev_comm, ev_pf, ev_rts, ev_bal, ev_dw})
+        for (cudaEvent_t e : {ev_a, ev_b, ev_c, ev_side, ev_comm, ev_pf, ev_rts, ev_bal})
             if (e) cudaEventDestroy(e);
         if (side) cudaStreamDestroy(side);
         if (comm_stream) cudaStreamDestroy(comm_stream);
@@ -888,17 +885,17 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
     // (leaving the jitter prefetch's SMs alone while it may still run)
     const int tc_dw_splits = static_cast<int>(std::max<int64_t>(
         1, std::min<int64_t>({16, (kNumSMs - h->pf_reserve) / std::max<int64_t>(1, d / 128), (T + 31) / 32})));
-    auto gate_dw = [&](cudaStream_t gs) {
+    auto gate_dw = [&] {
         if constexpr (std::is_same<TIO, __nv_bfloat16>::value) {
             if (h->gate_dw_tma)
                 launch_gate_dw_tma(x, noise, h->dL.as<float>(), h->dwg_part.as<float>(), T, static_cast<int>(d),
-                                   tc_dw_splits, gs);
+                                   tc_dw_splits, st);
             else
                 launch_gate_tc_dw<TIO>(x, noise, h->dL.as<float>(), h->dwg_part.as<float>(), T,
-                                       static_cast<int>(d), E, tc_dw_splits, gs);
+                                       static_cast<int>(d), E, tc_dw_splits, st);
         }
-        launch_splitk_reduce(h->dwg_part.as<float>(), tc_dw_splits, d * E, dgate_w, gs);
-        if (gs == st) h->mark("gate_dw");
+        launch_splitk_reduce(h->dwg_part.as<float>(), tc_dw_splits, d * E, dgate_w, st);
+        h->mark("gate_dw");
     };
     auto dwg_allreduce = [&] {
         MOE_CUDA_CHECK(cudaEventRecord(h->ev_c, st));
@@ -923,7 +920,7 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
     // gradients, where the jitter prefetch no longer holds SMs)
     const bool dw_early = gtc && ep > 1 && h->dw_early;
     if (dw_early) {
-        gate_dw(st);
+        gate_dw();
         dwg_allreduce();
     }
     // expert backward: dH = (dO W2^T) * [H > 0]; dX = dH W1^T; dW2 = H^T dO; dW1 = X^T dH
@@ -998,18 +995,7 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
     h->pf_reserve = 0;
     wgrad_gemm<TIO>(h, h->Xr.as<TIO>(), h->dH.as<TIO>(), dw1, d, f, counts, ep);
     h->mark("ffn1_wgrad");
-    // One GPU: gate dW (reads x, jitter, dL) runs on the side stream while
-    // gate dx (reads dL, jitter, the dispatch-backward rows) runs here; both
-    // are memory-bound and read the same jitter stream.
-    const bool dw_side = gtc && !dw_early && ep == 1 && h->dw_side;
-    if (dw_side) {
-        MOE_CUDA_CHECK(cudaEventRecord(h->ev_a, st));
-        MOE_CUDA_CHECK(cudaStreamWaitEvent(side, h->ev_a, 0));
-        gate_dw(side);
-        MOE_CUDA_CHECK(cudaEventRecord(h->ev_dw, side));
-    } else if (gtc && !dw_early) {
-        gate_dw(st);
-    }
+    if (gtc && !dw_early) gate_dw();
     MOE_CUDA_CHECK(cudaStreamWaitEvent(st, h->ev_side, 0));
     if (ep > 1) MOE_CUDA_CHECK(cudaStreamWaitEvent(st, h->ev_comm, 0));
     h->mark("bwd_join");
@@ -1040,10 +1026,6 @@ void backward_impl(moe_handle* h, const TIO* dy, float daux, TIO* dx, float* dga
                                 !h->has_residual, dx, dres, st);
     }
     h->mark("gate_dx");
-    if (dw_side) {
-        MOE_CUDA_CHECK(cudaStreamWaitEvent(st, h->ev_dw, 0));
-        h->mark("gate_dw_join");
-    }
     if (ep > 1) {
         MOE_CUDA_CHECK(cudaStreamWaitEvent(st, h->ev_comm, 0));
         h->mark("allreduce_dgate_w");
@@ -1236,8 +1218,6 @@ void alloc_workspace(moe_handle* h) {
         h->rcb_ep = !(re && re[0] == '0');
         const char* de = std::getenv("MOE_B200_DW_EARLY");
         h->dw_early = de && de[0] == '1';
-        const char* dsd = std::getenv("MOE_B200_GATE_DW_SIDE");
-        h->dw_side = !(dsd && dsd[0] == '0');
         const char* gd = std::getenv("MOE_B200_GATE_DW_TMA");
         h->gate_dw_tma = gate_dw_tma_ok(static_cast<int>(d), E) && !(gd && gd[0] == '0');
         const char* rb = std::getenv("MOE_B200_RELU_BITS");
@@ -1383,7 +1363,7 @@ moe_status moe_create(const moe_router_cfg* cfg, const moe_layer_dims* dims, moe
         if (const char* v = std::getenv("MOE_B200_PF_SMS")) h->pf_sms = std::max(1, std::min(64, std::atoi(v)));
         if (const char* v = std::getenv("MOE_B200_PF_HOLD")) h->pf_hold = v[0] == '1';
         for (cudaEvent_t* e : {&h->ev_a, &h->ev_b, &h->ev_c, &h->ev_side, &h->ev_comm, &h->ev_pf, &h->ev_rts,
-                                &h->ev_bal, &h->ev_dw})
+                                &h->ev_bal})
             MOE_CUDA_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     });
     if (s == MOE_OK) *out = h.release();
